@@ -1,0 +1,234 @@
+/*
+ * gbm.h -- C-ABI of libgbm.so, the B200 (sm_100a) hot path of multi-GPU histogram gradient
+ * boosting (arXiv 1806.11248, "XGBoost: Scalable GPU Accelerated Learning").
+ *
+ * Citations: P:nn = PAPER.md line nn (section), S:nn = SPEC.md line nn, R# = reading number in
+ * DESIGN.md "Readings of the paper".
+ *
+ * Conventions (apply to every entry point):
+ *  - Pointers suffixed _d are DEVICE pointers on the context's device, _h are HOST pointers.
+ *    The caller owns every buffer passed in (allocates, frees, keeps it alive for the call and
+ *    for all work the call enqueued); the library never retains a caller pointer after a call
+ *    returns.  Device buffers must be 16-byte aligned and contiguous.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).  All work is
+ *    enqueued on it, asynchronously, unless an entry says it synchronises.
+ *  - Every function returns GBM_OK (0) or a negative GBM_E_* code and never throws; the message
+ *    of the last failure on the calling thread is gbm_last_error().  Argument checks happen
+ *    before anything is enqueued.  Errors detected ON the device (a label outside {0,1} under
+ *    the logistic objective) are latched in the context and returned by the next gbm_check.
+ *  - A context is bound to one device, owns a scratch arena and (optionally) an NCCL
+ *    communicator, and is not thread-safe.  One context per (process, device).
+ *  - "Collective": with a communicator of nranks > 1 every rank must make the same call in the
+ *    same order (NCCL semantics).  Rank k owns rows [floor(k n/p), floor((k+1) n/p)) (R18).
+ *  - No CPU fallback exists: without a CUDA device every compute entry fails with GBM_E_CUDA.
+ */
+#ifndef GBM_H
+#define GBM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GBM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GBM_API __attribute__((visibility("default")))
+#else
+#define GBM_API
+#endif
+
+enum {
+    GBM_OK = 0,
+    GBM_E_ARG = -1,       /* invalid argument (null pointer, size, enum, alignment)         */
+    GBM_E_EMPTY = -2,     /* zero rows                                        */
+    GBM_E_OVERFLOW = -3,  /* symbol does not fit the bit width                       */
+    GBM_E_LABEL = -4,     /* label outside {0,1} under binary:logistic               */
+    GBM_E_NONFINITE = -5, /* +-inf feature value                                      */
+    GBM_E_MISMATCH = -6,  /* ranks disagree on sizes                                 */
+    GBM_E_STATE = -7,     /* call not valid in the context's state (e.g. no communicator)    */
+    GBM_E_CUDA = -10,     /* CUDA runtime error or no device                                 */
+    GBM_E_NCCL = -11,     /* NCCL error                                                      */
+    GBM_E_NOMEM = -12     /* device or host allocation failed                                */
+};
+
+enum { GBM_SQUARED_ERROR = 0, GBM_LOGISTIC = 1 };   /* objectives */
+enum { GBM_NODE_ABSENT = 0, GBM_NODE_SPLIT = 1, GBM_NODE_LEAF = 2 };
+
+typedef struct gbm_ctx gbm_ctx;
+
+/* ---------------------------------------------------------------- lifecycle, errors */
+GBM_API const char *gbm_last_error(void);   /* thread-local; valid until the next gbm_* call     */
+GBM_API int gbm_abi_version(void);          /* == GBM_ABI_VERSION                                  */
+GBM_API int gbm_ctx_create(int device, gbm_ctx **out);
+GBM_API int gbm_ctx_destroy(gbm_ctx *ctx);  /* frees scratch and the communicator; NULL is a no-op */
+/* Synchronises `stream` and reports asynchronous failures (CUDA errors and device-detected
+ * argument errors such as GBM_E_LABEL) latched since the last gbm_check. */
+GBM_API int gbm_check(gbm_ctx *ctx, void *stream);
+
+/* ---------------------------------------------------------------- communicator
+ * Rank 0 calls gbm_comm_unique_id and broadcasts the 128 bytes with its own process group
+ * (the Python binding uses torch.distributed); then every rank calls gbm_comm_init
+ * (collective; blocks until all ranks joined).  nranks == 1 is allowed.  Without a
+ * communicator every entry behaves as a single rank. */
+GBM_API int gbm_comm_unique_id(uint8_t id_h[128]);
+GBM_API int gbm_comm_init(gbm_ctx *ctx, const uint8_t id_h[128], int nranks, int rank);
+GBM_API int gbm_comm_info(gbm_ctx *ctx, int *nranks_h, int *rank_h);
+
+/* ---------------------------------------------------------------- §2.1 quantiles
+ * gbm_cuts: exact per-feature cut points over the GLOBAL rows (collective: the ranks'
+ * shards are all-gathered).  Rule R5: with V the sorted present values of a
+ * feature (m of them, d distinct) the cuts are the distinct values if d <= max_bins, else
+ * dedup(V[floor((j+1) m / max_bins) - 1], j = 0..max_bins-1).  NaN = missing; -0.0 counts as
+ * +0.0.
+ *   X_d          fp32 [n_rows][n_features] row-major, this rank's shard
+ *   cut_values_d fp32 [n_features * max_bins] (capacity), written compactly
+ *   cut_ptr_d    int32 [n_features + 1], exclusive prefix sum of per-feature bin counts
+ *   n_cuts_h     total bins TB = cut_ptr[F]
+ *   max_symbol_h the largest symbol gbm_quantise will store for these rows: max_bins if any
+ *                value (on any rank) is missing, else max_f(n_bins(f)) - 1 (R4)
+ * Synchronises `stream` (the sizes are returned on the host).  Errors: GBM_E_EMPTY (no
+ * rows on every rank), GBM_E_NONFINITE (+-inf), GBM_E_ARG (max_bins < 2 or > 65535). */
+GBM_API int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t n_features,
+             int32_t max_bins, float *cut_values_d, int32_t *cut_ptr_d, int32_t *n_cuts_h,
+             int32_t *max_symbol_h, void *stream);
+
+/* gbm_quantise: bin map (R6/R7): bins[i][f] = max_bins (the missing sentinel) if
+ * X[i][f] is NaN (or the feature has no cuts), else the smallest k with X[i][f] <=
+ * cuts_f[k], clamped to n_bins(f)-1.  bins_d uint16 [n_rows][n_features].  Asynchronous. */
+GBM_API int gbm_quantise(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t n_features,
+                 int32_t max_bins, const float *cut_values_d, const int32_t *cut_ptr_d,
+                 uint16_t *bins_d, void *stream);
+
+/* ---------------------------------------------------------------- §2.2 compression
+ * symbol width (R1): max(1, ceil(log2(max_symbol + 1))).  Pure, host only. */
+GBM_API int gbm_symbol_bits(int32_t max_symbol);
+/* packed buffer size in uint32 words for the layout of gbm_compress (R3): element (r, f)
+ * starts at bit r*stride + f*bits, stride = n_features*bits rounded up to row_align_bits
+ * (0, 32 or 128; 0 = SPEC's continuous stream); ceil(n*stride/32) words rounded up to a
+ * multiple of 4, plus 4 zero words.  Returns a negative GBM_E_* on bad arguments. */
+GBM_API int64_t gbm_packed_words(int64_t n_rows, int32_t n_features, int32_t bits,
+                         int32_t row_align_bits);
+/* gbm_compress: bit-pack bins into packed_d (uint32 words, little-endian bit order: bit j of
+ * a symbol is stream bit start+j, i.e. bit (s mod 32) of word floor(s/32)); every padding
+ * bit is zero.  bits in 1..16.  A symbol >= 2^bits is detected on the device and latched as
+ * GBM_E_OVERFLOW for the next gbm_check.  packed_words must be >= gbm_packed_words(...). */
+GBM_API int gbm_compress(gbm_ctx *ctx, const uint16_t *bins_d, int64_t n_rows, int32_t n_features,
+                 int32_t bits, int32_t row_align_bits, uint32_t *packed_d, int64_t packed_words,
+                 void *stream);
+/* gbm_quantise_compress: the fused a2 step -- bin map and bit-pack in one pass straight from
+ * X_d to packed_d, no uint16 intermediate.  Same layout and results as gbm_quantise followed
+ * by gbm_compress.  bits must be >= gbm_symbol_bits(max_symbol of these rows). */
+GBM_API int gbm_quantise_compress(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t n_features,
+                          int32_t max_bins, const float *cut_values_d, const int32_t *cut_ptr_d,
+                          int32_t bits, int32_t row_align_bits, uint32_t *packed_d,
+                          int64_t packed_words, void *stream);
+
+/* ---------------------------------------------------------------- the quantised matrix
+ * A rank's shard as consumed by tree construction.  cut_ptr_h is a HOST copy of cut_ptr_d
+ * (the host plans shared-memory feature groups from it without a device sync). */
+typedef struct {
+    const uint32_t *packed_d;  /* gbm_compress layout                                      */
+    int64_t n_rows;            /* rows of this shard                                       */
+    int32_t n_features;
+    int32_t bits;              /* symbol width                                             */
+    int32_t row_align_bits;    /* 0, 32 or 128                                             */
+    int32_t max_bins;          /* B; the missing sentinel symbol                           */
+    const float *cut_values_d; /* fp32 [TB]                                                */
+    const int32_t *cut_ptr_d;  /* int32 [F+1]                                              */
+    const int32_t *cut_ptr_h;  /* int32 [F+1], host copy                                   */
+} gbm_qmatrix;
+
+typedef struct {
+    int32_t objective;         /* GBM_SQUARED_ERROR | GBM_LOGISTIC                          */
+    int32_t max_depth;         /* D >= 0: root depth 0, at most 2^D leaves (R23)            */
+    int32_t grad_bits;         /* fixed-point precision P of the gradient pairs (R14); 1..30 */
+    int32_t reserved;
+    double eta, lambda, gamma, min_child_weight;   /* S:311-314, defaults 0.3/1/0/1 */
+} gbm_params;
+
+/* ---------------------------------------------------------------- §2.5 gradients
+ * gbm_gradients: per row g, h (Eq. 1-2; squared error g = yhat - y, h = 1) in fp64 with the
+ * sigmoid through det_exp (R19); then the fixed point (R14): M = max|g| over every rank's
+ * rows (collective max), E = frexp exponent of M (0 if M == 0), s = grad_bits - E,
+ * q = rint(g * 2^s) (half to even), |q| <= 2^grad_bits.  Same for h.
+ *   margin_d  fp64 [n_rows]     label_d fp32 [n_rows]
+ *   qpair_d   int32 [n_rows][2] = (q_g, q_h)
+ *   scale_d   int32 [2] device  = (s_g, s_h)
+ * Asynchronous; label-domain violations (logistic, label not 0/1) latch GBM_E_LABEL. */
+GBM_API int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const double *margin_d,
+                  const float *label_d, int64_t n_rows, int32_t *qpair_d, int32_t *scale_d,
+                  void *stream);
+
+/* ---------------------------------------------------------------- §2.3 trees (Alg. 1)
+ * A tree is a set of DEVICE arrays in heap order (root 0, children 2k+1 / 2k+2) of capacity
+ * 2^(max_depth+1) - 1.  kind: GBM_NODE_*.  For split nodes: feature, bin, threshold =
+ * cuts_feature[bin], default_left, gain.  For every present node: weight (R11: -G/(H+lambda)
+ * * eta, the leaf value for leaves), sum_qg / sum_qh (the node's fixed-point totals over all
+ * ranks).  Absent slots: kind 0, feature/bin -1, other fields 0. */
+typedef struct {
+    int8_t *kind;
+    int32_t *feature;
+    int32_t *bin;
+    float *threshold;
+    int8_t *default_left;
+    double *gain;
+    double *weight;
+    int64_t *sum_qg;
+    int64_t *sum_qh;
+} gbm_tree;
+
+/* gbm_build_tree: Algorithm 1, grown depth-wise and level-synchronously (R15):
+ * InitRoot; then per level: RepartitionInstances (stable), BuildPartialHistograms of the
+ * smaller child of every split (R17), AllReduceHistograms (collective: one NCCL int64 sum per
+ * level), sibling histogram = parent - built child (north star), EvaluateSplit for every node
+ * of the level (R8-R10).  row_leaf_d int32 [n_rows] receives the leaf each row ends in.
+ * Asynchronous (no host synchronisation inside a tree). */
+GBM_API int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *qm, const int32_t *qpair_d,
+                   const int32_t *scale_d, const gbm_params *params, const gbm_tree *tree,
+                   int32_t *row_leaf_d, void *stream);
+
+/* ---- the steps of Algorithm 1, exposed one by one (used by the parity tests) ---------- */
+/* BuildPartialHistograms: hist_d int64 [TB][2] (overwritten) = sum over the listed
+ * rows of (q_g, q_h) into bin cut_ptr[f] + symbol for every non-missing symbol.  rows_d
+ * uint32 [n_sel] row indices of this shard (NULL = all rows, n_sel ignored).  Not collective. */
+GBM_API int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *qm, const int32_t *qpair_d,
+                        int32_t grad_bits, const uint32_t *rows_d, int64_t n_sel,
+                        int64_t *hist_d, void *stream);
+/* AllReduceHistograms: in-place int64 sum over ranks (collective). */
+GBM_API int gbm_allreduce_histograms(gbm_ctx *ctx, int64_t *hist_d, int64_t count, void *stream);
+/* EvaluateSplit for n_nodes nodes: hist_d int64 [n_nodes][TB][2], totals_d
+ * int64 [n_nodes][2].  Outputs per node (device arrays of n_nodes): split_d int8 (1 iff the
+ * best valid candidate has gain > 0), feature_d, bin_d, default_left_d int8, gain_d fp64
+ * (best valid gain, 0 if none), child_d int64 [n_nodes][4] = (L_g, L_h, R_g, R_h). */
+GBM_API int gbm_evaluate_splits(gbm_ctx *ctx, const gbm_qmatrix *qm, const int64_t *hist_d,
+                        const int64_t *totals_d, int32_t n_nodes, const int32_t *scale_d,
+                        const gbm_params *params, int8_t *split_d, int32_t *feature_d,
+                        int32_t *bin_d, int8_t *default_left_d, double *gain_d,
+                        int64_t *child_d, void *stream);
+/* RepartitionInstances: stable partition of the rows rows_d uint32 [n_sel] of one
+ * node by the split (feature, bin, default_left): left rows (symbol <= bin, or missing and
+ * default_left) first, then right rows, each in input order, into out_d uint32 [n_sel];
+ * the left count is written to n_left_d int64 [1] (device). */
+GBM_API int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *qm, const uint32_t *rows_d, int64_t n_sel,
+                    int32_t feature, int32_t bin, int32_t default_left, uint32_t *out_d,
+                    int64_t *n_left_d, void *stream);
+
+/* ---------------------------------------------------------------- margins and prediction
+ * gbm_update_margins: margin[i] = margin[i] + weight[row_leaf[i]] (fp64).  */
+GBM_API int gbm_update_margins(gbm_ctx *ctx, const double *weight_d, const int32_t *row_leaf_d,
+                       int64_t n_rows, double *margin_d, void *stream);
+/* gbm_predict (§2.4): one thread per row; for every tree in order walk
+ * from the root, left iff (isnan(v) ? default_left : v <= threshold), and add the leaf
+ * weight: margin[i] = base_margin + sum_t w_t(i) in tree order.  Trees are concatenated
+ * heap arrays (device) of capacity 2^(max_depth+1)-1 each; X_d fp32 [n_rows][n_features]. */
+GBM_API int gbm_predict(gbm_ctx *ctx, int32_t n_trees, int32_t max_depth, const int8_t *kind_d,
+                const int32_t *feature_d, const float *threshold_d, const int8_t *default_left_d,
+                const double *weight_d, double base_margin, const float *X_d, int64_t n_rows,
+                int32_t n_features, double *margin_d, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GBM_H */

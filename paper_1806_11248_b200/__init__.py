@@ -1,0 +1,418 @@
+"""paper_1806_11248_b200 -- B200-native hot path of multi-GPU histogram gradient boosting
+(arXiv 1806.11248), behind the C-ABI of ``include/gbm.h`` (``libgbm.so``).
+
+This module is the thin Python binding: argument marshalling only.  torch supplies device
+memory (tensors), the current CUDA stream and the process group used to broadcast the NCCL id;
+every step of the path runs in the CUDA kernels of ``csrc/``.  There is no CPU fallback: without
+the built library or a CUDA device every call raises ``GbmError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+import threading
+
+import numpy as np
+import torch
+
+from . import build_lib
+
+__all__ = ["GbmError", "Context", "QMatrix", "Tree", "Booster", "lib", "symbol_bits",
+           "packed_words", "SQUARED_ERROR", "LOGISTIC", "OBJECTIVES"]
+
+SQUARED_ERROR, LOGISTIC = 0, 1
+OBJECTIVES = {"reg:squarederror": SQUARED_ERROR, "binary:logistic": LOGISTIC}
+NODE_ABSENT, NODE_SPLIT, NODE_LEAF = 0, 1, 2
+DEFAULT_GRAD_BITS = 15   # R14 / DESIGN.md "Gradient precision"
+
+_lock = threading.Lock()
+_lib = None
+
+
+class GbmError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: {msg} (code {code})")
+        self.code = code
+
+
+class _Params(C.Structure):
+    _fields_ = [("objective", C.c_int32), ("max_depth", C.c_int32), ("grad_bits", C.c_int32),
+                ("reserved", C.c_int32), ("eta", C.c_double), ("reg_lambda", C.c_double),
+                ("gamma", C.c_double), ("min_child_weight", C.c_double)]
+
+
+class _QM(C.Structure):
+    _fields_ = [("packed_d", C.c_void_p), ("n_rows", C.c_int64), ("n_features", C.c_int32),
+                ("bits", C.c_int32), ("row_align_bits", C.c_int32), ("max_bins", C.c_int32),
+                ("cut_values_d", C.c_void_p), ("cut_ptr_d", C.c_void_p),
+                ("cut_ptr_h", C.POINTER(C.c_int32))]
+
+
+class _Tree(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("kind", "feature", "bin", "threshold", "default_left",
+                                          "gain", "weight", "sum_qg", "sum_qh")]
+
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "gbm_last_error": (C.c_char_p, []),
+    "gbm_abi_version": (C.c_int, []),
+    "gbm_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "gbm_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "gbm_check": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gbm_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "gbm_comm_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
+    "gbm_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "gbm_cuts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                           C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p]),
+    "gbm_quantise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gbm_symbol_bits": (C.c_int, [C.c_int32]),
+    "gbm_packed_words": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
+    "gbm_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                               C.c_void_p, C.c_int64, C.c_void_p]),
+    "gbm_quantise_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                        C.c_int64, C.c_void_p]),
+    "gbm_gradients": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gbm_build_tree": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_void_p,
+                                 C.POINTER(_Params), C.POINTER(_Tree), C.c_void_p, C.c_void_p]),
+    "gbm_build_histogram": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_int32,
+                                      C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "gbm_allreduce_histograms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "gbm_evaluate_splits": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_void_p,
+                                      C.c_int32, C.c_void_p, C.POINTER(_Params), C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]),
+    "gbm_repartition": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_int64, C.c_int32,
+                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gbm_update_margins": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                     C.c_void_p]),
+    "gbm_predict": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                              C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+}
+
+
+def lib():
+    """Load (building if stale) the in-tree libgbm.so.  Raises if it cannot be built/loaded."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = build_lib.LIB
+            if build_lib.stale():
+                path = build_lib.build()
+            L = C.CDLL(path)
+            for name, (res, args) in EXPORTS.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().gbm_last_error().decode(errors="replace")
+        raise GbmError(rc, name, msg)
+    return rc
+
+
+def _p(t: torch.Tensor | None):
+    if t is None:
+        return None
+    assert t.is_contiguous(), "tensors passed to libgbm must be contiguous"
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def symbol_bits(max_symbol: int) -> int:
+    b = lib().gbm_symbol_bits(int(max_symbol))
+    if b < 0:
+        raise GbmError(b, "gbm_symbol_bits", "bad max_symbol")
+    return b
+
+
+def packed_words(n_rows: int, n_features: int, bits: int, row_align_bits: int = 32) -> int:
+    w = lib().gbm_packed_words(n_rows, n_features, bits, row_align_bits)
+    if w < 0:
+        raise GbmError(int(w), "gbm_packed_words", lib().gbm_last_error().decode())
+    return int(w)
+
+
+def _params(objective, max_depth, eta, reg_lambda, gamma, mcw, grad_bits):
+    return _Params(OBJECTIVES.get(objective, objective), max_depth, grad_bits, 0, eta,
+                   reg_lambda, gamma, mcw)
+
+
+@dataclasses.dataclass
+class QMatrix:
+    """A rank's quantised, bit-packed shard (device tensors) + its cuts."""
+    packed: torch.Tensor          # int32 view of the uint32 words
+    n_rows: int
+    n_features: int
+    bits: int
+    row_align_bits: int
+    max_bins: int
+    cut_values: torch.Tensor      # fp32 [TB]
+    cut_ptr: torch.Tensor         # int32 [F+1] (device)
+    cut_ptr_h: np.ndarray         # int32 [F+1] (host)
+
+    def c(self) -> _QM:
+        self._cp = np.ascontiguousarray(self.cut_ptr_h, dtype=np.int32)
+        cv = self.cut_values if self.cut_values.numel() else torch.zeros(1, device=self.packed.device)
+        self._cv = cv
+        return _QM(self.packed.data_ptr(), self.n_rows, self.n_features, self.bits,
+                   self.row_align_bits, self.max_bins, cv.data_ptr(), self.cut_ptr.data_ptr(),
+                   self._cp.ctypes.data_as(C.POINTER(C.c_int32)))
+
+    @property
+    def n_bins_total(self) -> int:
+        return int(self.cut_ptr_h[-1])
+
+
+TREE_FIELDS = (("kind", torch.int8), ("feature", torch.int32), ("bin", torch.int32),
+               ("threshold", torch.float32), ("default_left", torch.int8),
+               ("gain", torch.float64), ("weight", torch.float64), ("sum_qg", torch.int64),
+               ("sum_qh", torch.int64))
+
+
+class Tree:
+    """Heap-ordered device arrays of one tree (capacity 2^(D+1)-1)."""
+
+    def __init__(self, max_depth: int, device):
+        cap = (1 << (max_depth + 1)) - 1
+        self.max_depth = max_depth
+        self.arrays = {n: torch.empty(cap, dtype=dt, device=device) for n, dt in TREE_FIELDS}
+
+    def c(self) -> _Tree:
+        return _Tree(*[self.arrays[n].data_ptr() for n, _ in TREE_FIELDS])
+
+    def __getitem__(self, k):
+        return self.arrays[k]
+
+    def to_numpy(self) -> dict:
+        return {k: v.cpu().numpy() for k, v in self.arrays.items()}
+
+
+class Context:
+    """One gbm_ctx bound to a CUDA device (and optionally an NCCL communicator)."""
+
+    def __init__(self, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise GbmError(-10, "Context", "no CUDA device: libgbm has no CPU fallback")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.dev = torch.device("cuda", self.device)
+        h = C.c_void_p()
+        _call("gbm_ctx_create", self.device, C.byref(h))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gbm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ communicator
+    def comm_init_from_torch(self, group=None):
+        """NCCL communicator over the ranks of the torch.distributed (default) process group:
+        rank 0 makes the id, torch broadcasts the 128 bytes (plumbing only)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _call("gbm_comm_unique_id", buf)
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.to(self.dev)
+        dist.broadcast(t, 0, group=group)
+        ids = (C.c_uint8 * 128)(*t.cpu().tolist())
+        _call("gbm_comm_init", self.h, ids, world, rank)
+
+    def comm_init(self, id_bytes: bytes, nranks: int, rank: int):
+        ids = (C.c_uint8 * 128)(*id_bytes)
+        _call("gbm_comm_init", self.h, ids, nranks, rank)
+
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _call("gbm_comm_unique_id", buf)
+        return bytes(buf)
+
+    def check(self):
+        _call("gbm_check", self.h, _stream())
+
+    # ------------------------------------------------------------ §2.1 / §2.2
+    def cuts(self, X: torch.Tensor, max_bins: int):
+        n, F = X.shape
+        cv = torch.empty(max(1, F * max_bins), dtype=torch.float32, device=self.dev)
+        cp = torch.empty(F + 1, dtype=torch.int32, device=self.dev)
+        ncut, mx = C.c_int32(), C.c_int32()
+        _call("gbm_cuts", self.h, _p(X), n, F, max_bins, _p(cv), _p(cp), C.byref(ncut),
+              C.byref(mx), _stream())
+        return cv[: ncut.value], cp, mx.value
+
+    def quantise(self, X, max_bins, cut_values, cut_ptr):
+        n, F = X.shape
+        bins = torch.empty((n, F), dtype=torch.uint16, device=self.dev)
+        _call("gbm_quantise", self.h, _p(X), n, F, max_bins, _p(_nz(cut_values)), _p(cut_ptr),
+              _p(bins), _stream())
+        return bins
+
+    def compress(self, bins, bits, row_align_bits=32):
+        n, F = bins.shape
+        nw = packed_words(n, F, bits, row_align_bits)
+        out = torch.empty(nw, dtype=torch.int32, device=self.dev)
+        _call("gbm_compress", self.h, _p(bins), n, F, bits, row_align_bits, _p(out), nw,
+              _stream())
+        return out
+
+    def quantise_compress(self, X, max_bins, cut_values, cut_ptr, bits, row_align_bits=32):
+        n, F = X.shape
+        nw = packed_words(n, F, bits, row_align_bits)
+        out = torch.empty(nw, dtype=torch.int32, device=self.dev)
+        _call("gbm_quantise_compress", self.h, _p(X), n, F, max_bins, _p(_nz(cut_values)),
+              _p(cut_ptr), bits, row_align_bits, _p(out), nw, _stream())
+        return out
+
+    def make_qmatrix(self, X: torch.Tensor, max_bins: int, row_align_bits: int = 32,
+                     cuts=None) -> QMatrix:
+        """Fig. 1 preprocessing: global cuts (collective), then fused bin map + pack."""
+        if cuts is None:
+            cv, cp, mx = self.cuts(X, max_bins)
+        else:
+            cv, cp, mx = cuts
+        bits = symbol_bits(mx)
+        packed = self.quantise_compress(X, max_bins, cv, cp, bits, row_align_bits)
+        return QMatrix(packed, X.shape[0], X.shape[1], bits, row_align_bits, max_bins, cv, cp,
+                       cp.cpu().numpy())
+
+    # ------------------------------------------------------------ §2.5
+    def gradients(self, objective, margin, label, grad_bits=DEFAULT_GRAD_BITS, out=None,
+                  scale=None):
+        n = margin.shape[0]
+        q = out if out is not None else torch.empty((n, 2), dtype=torch.int32, device=self.dev)
+        sc = scale if scale is not None else torch.empty(2, dtype=torch.int32, device=self.dev)
+        _call("gbm_gradients", self.h, OBJECTIVES.get(objective, objective), grad_bits,
+              _p(margin), _p(label), n, _p(q), _p(sc), _stream())
+        return q, sc
+
+    # ------------------------------------------------------------ §2.3
+    def build_tree(self, qm: QMatrix, qpair, scale, *, objective, max_depth, eta=0.3,
+                   reg_lambda=1.0, gamma=0.0, min_child_weight=1.0,
+                   grad_bits=DEFAULT_GRAD_BITS, tree: Tree | None = None, row_leaf=None):
+        tree = tree if tree is not None else Tree(max_depth, self.dev)
+        rl = row_leaf if row_leaf is not None else torch.empty(qm.n_rows, dtype=torch.int32,
+                                                               device=self.dev)
+        prm = _params(objective, max_depth, eta, reg_lambda, gamma, min_child_weight, grad_bits)
+        qc, tc = qm.c(), tree.c()
+        _call("gbm_build_tree", self.h, C.byref(qc), _p(qpair), _p(scale), C.byref(prm),
+              C.byref(tc), _p(rl), _stream())
+        return tree, rl
+
+    def build_histogram(self, qm: QMatrix, qpair, grad_bits, rows=None):
+        TB = qm.n_bins_total
+        hist = torch.empty((max(TB, 1), 2), dtype=torch.int64, device=self.dev)
+        n_sel = qm.n_rows if rows is None else rows.numel()
+        _call("gbm_build_histogram", self.h, C.byref(qm.c()), _p(qpair), grad_bits, _p(rows),
+              n_sel, _p(hist), _stream())
+        return hist[:TB]
+
+    def allreduce_histograms(self, hist: torch.Tensor):
+        _call("gbm_allreduce_histograms", self.h, _p(hist), hist.numel(), _stream())
+
+    def evaluate_splits(self, qm: QMatrix, hist, totals, scale, *, eta=0.3, reg_lambda=1.0,
+                        gamma=0.0, min_child_weight=1.0, max_depth=1):
+        n = totals.shape[0]
+        d = self.dev
+        out = dict(split=torch.empty(n, dtype=torch.int8, device=d),
+                   feature=torch.empty(n, dtype=torch.int32, device=d),
+                   bin=torch.empty(n, dtype=torch.int32, device=d),
+                   default_left=torch.empty(n, dtype=torch.int8, device=d),
+                   gain=torch.empty(n, dtype=torch.float64, device=d),
+                   child=torch.empty((n, 4), dtype=torch.int64, device=d))
+        prm = _params(0, max_depth, eta, reg_lambda, gamma, min_child_weight, 15)
+        _call("gbm_evaluate_splits", self.h, C.byref(qm.c()), _p(hist), _p(totals), n, _p(scale),
+              C.byref(prm), _p(out["split"]), _p(out["feature"]), _p(out["bin"]),
+              _p(out["default_left"]), _p(out["gain"]), _p(out["child"]), _stream())
+        return out
+
+    def repartition(self, qm: QMatrix, rows, feature, bin_, default_left):
+        out = torch.empty_like(rows)
+        nl = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        _call("gbm_repartition", self.h, C.byref(qm.c()), _p(rows), rows.numel(), feature, bin_,
+              int(bool(default_left)), _p(out), _p(nl), _stream())
+        return out, nl
+
+    # ------------------------------------------------------------ margins / §2.4
+    def update_margins(self, weight, row_leaf, margin):
+        _call("gbm_update_margins", self.h, _p(weight), _p(row_leaf), margin.shape[0],
+              _p(margin), _stream())
+        return margin
+
+    def predict(self, trees: list[Tree], max_depth: int, base_margin: float, X: torch.Tensor):
+        n, F = X.shape
+        out = torch.empty(n, dtype=torch.float64, device=self.dev)
+        if trees:
+            cat = {k: torch.cat([t[k] for t in trees]) for k in
+                   ("kind", "feature", "threshold", "default_left", "weight")}
+        else:
+            cat = {k: None for k in ("kind", "feature", "threshold", "default_left", "weight")}
+        _call("gbm_predict", self.h, len(trees), max_depth, _p(cat["kind"]), _p(cat["feature"]),
+              _p(cat["threshold"]), _p(cat["default_left"]), _p(cat["weight"]),
+              float(base_margin), _p(X), n, F, _p(out), _stream())
+        return out
+
+
+def _nz(t):
+    return t if t.numel() else torch.zeros(1, dtype=t.dtype, device=t.device)
+
+
+class Booster:
+    """The Fig. 1 pipeline on one rank: quantise+compress once, then per boosting
+    round gradients (collective max) -> Alg. 1 tree (collective per level) -> margin update.
+    X / y are this rank's shard (device tensors)."""
+
+    def __init__(self, ctx: Context, X: torch.Tensor, y: torch.Tensor, *, max_bins: int,
+                 objective: str, max_depth: int, eta=0.3, reg_lambda=1.0, gamma=0.0,
+                 min_child_weight=1.0, grad_bits=DEFAULT_GRAD_BITS, row_align_bits=32,
+                 base_margin=0.0, cuts=None):
+        self.ctx, self.y = ctx, y
+        self.objective, self.max_depth, self.grad_bits = objective, max_depth, grad_bits
+        self.kw = dict(eta=eta, reg_lambda=reg_lambda, gamma=gamma,
+                       min_child_weight=min_child_weight)
+        self.qm = ctx.make_qmatrix(X, max_bins, row_align_bits, cuts=cuts)
+        self.base_margin = float(base_margin)
+        n = X.shape[0]
+        self.margin = torch.full((n,), self.base_margin, dtype=torch.float64, device=ctx.dev)
+        self.qpair = torch.empty((n, 2), dtype=torch.int32, device=ctx.dev)
+        self.scale = torch.empty(2, dtype=torch.int32, device=ctx.dev)
+        self.row_leaf = torch.empty(n, dtype=torch.int32, device=ctx.dev)
+        self.trees: list[Tree] = []
+
+    def round(self, keep_tree=True) -> Tree:
+        c = self.ctx
+        c.gradients(self.objective, self.margin, self.y, self.grad_bits, out=self.qpair,
+                    scale=self.scale)
+        tree, _ = c.build_tree(self.qm, self.qpair, self.scale, objective=self.objective,
+                               max_depth=self.max_depth, grad_bits=self.grad_bits,
+                               row_leaf=self.row_leaf, **self.kw)
+        c.update_margins(tree["weight"], self.row_leaf, self.margin)
+        if keep_tree:
+            self.trees.append(tree)
+        return tree
+
+    def predict(self, X, n_trees=None):
+        t = self.trees if n_trees is None else self.trees[:n_trees]
+        return self.ctx.predict(t, self.max_depth, self.base_margin, X)

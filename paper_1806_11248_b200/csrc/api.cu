@@ -1,0 +1,168 @@
+// api.cu -- lifecycle, errors, scratch arena and the NCCL communicator of libgbm.so.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gbm_internal.cuh"
+
+namespace gbm {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int Arena::reserve(size_t bytes) {
+    bytes = (bytes + 4095) & ~size_t(4095);
+    if (bytes <= cap) {
+        used = 0;
+        return GBM_OK;
+    }
+    if (base) {
+        cudaError_t e = cudaFree(base);  // synchronises the device: only on growth
+        if (e != cudaSuccess) return fail(GBM_E_CUDA, std::string("cudaFree: ") + cudaGetErrorString(e));
+        base = nullptr;
+        cap = 0;
+    }
+    size_t want = bytes + bytes / 4;  // head room so a slightly larger next call does not regrow
+    cudaError_t e = cudaMalloc(&base, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        e = cudaMalloc(&base, bytes);
+        want = bytes;
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            base = nullptr;
+            return fail(GBM_E_NOMEM, "scratch arena: cannot allocate " + std::to_string(bytes) + " bytes");
+        }
+    }
+    cap = want;
+    used = 0;
+    return GBM_OK;
+}
+
+int ctx_enter(gbm_ctx *ctx) {
+    if (!ctx) return fail(GBM_E_ARG, "null context");
+    GBM_CUDA(cudaSetDevice(ctx->device));
+    return GBM_OK;
+}
+
+int allreduce_i64(gbm_ctx *ctx, long long *buf, size_t count, cudaStream_t s) {
+    if (!ctx->comm || ctx->nranks == 1 || count == 0) return GBM_OK;
+    GBM_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, ctx->comm, s));
+    return GBM_OK;
+}
+
+}  // namespace gbm
+
+using namespace gbm;
+
+extern "C" {
+
+const char *gbm_last_error(void) { return g_last_error.c_str(); }
+
+int gbm_abi_version(void) { return GBM_ABI_VERSION; }
+
+int gbm_ctx_create(int device, gbm_ctx **out) {
+    if (!out) return fail(GBM_E_ARG, "gbm_ctx_create: out is null");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(GBM_E_CUDA, "gbm_ctx_create: no CUDA device available (libgbm has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return fail(GBM_E_ARG, "gbm_ctx_create: bad device ordinal");
+    GBM_CUDA(cudaSetDevice(device));
+    gbm_ctx *c = new gbm_ctx();
+    c->device = device;
+    cudaDeviceProp prop;
+    GBM_CUDA(cudaGetDeviceProperties(&prop, device));
+    c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    GBM_CUDA(cudaMalloc(&c->dev_err, sizeof(uint32_t)));
+    GBM_CUDA(cudaMemset(c->dev_err, 0, sizeof(uint32_t)));
+    *out = c;
+    return GBM_OK;
+}
+
+int gbm_ctx_destroy(gbm_ctx *ctx) {
+    if (!ctx) return GBM_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->arena.base) cudaFree(ctx->arena.base);
+    if (ctx->tree_arena.base) cudaFree(ctx->tree_arena.base);
+    if (ctx->dev_err) cudaFree(ctx->dev_err);
+    delete ctx;
+    return GBM_OK;
+}
+
+int gbm_check(gbm_ctx *ctx, void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    cudaStream_t s = (cudaStream_t)stream;
+    GBM_CUDA(cudaStreamSynchronize(s));
+    GBM_CUDA(cudaGetLastError());
+    uint32_t bits = 0;
+    GBM_CUDA(cudaMemcpy(&bits, ctx->dev_err, sizeof(bits), cudaMemcpyDeviceToHost));
+    if (bits) {
+        GBM_CUDA(cudaMemset(ctx->dev_err, 0, sizeof(uint32_t)));
+        if (bits & DERR_LABEL) return fail(GBM_E_LABEL, "label outside {0,1} under binary:logistic (S:246)");
+        if (bits & DERR_OVERFLOW) return fail(GBM_E_OVERFLOW, "symbol does not fit the bit width (S:183)");
+        if (bits & DERR_NONFINITE) return fail(GBM_E_NONFINITE, "non-finite feature value (S:32)");
+    }
+    return GBM_OK;
+}
+
+int gbm_comm_unique_id(uint8_t id_h[128]) {
+    if (!id_h) return fail(GBM_E_ARG, "gbm_comm_unique_id: null buffer");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    GBM_NCCL(ncclGetUniqueId(&id));
+    memcpy(id_h, &id, 128);
+    return GBM_OK;
+}
+
+int gbm_comm_init(gbm_ctx *ctx, const uint8_t id_h[128], int nranks, int rank) {
+    GBM_TRY(ctx_enter(ctx));
+    if (!id_h || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(GBM_E_ARG, "gbm_comm_init: bad id / nranks / rank");
+    if (ctx->comm) return fail(GBM_E_STATE, "gbm_comm_init: communicator already initialised");
+    ncclUniqueId id;
+    memcpy(&id, id_h, 128);
+    GBM_NCCL(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return GBM_OK;
+}
+
+int gbm_comm_info(gbm_ctx *ctx, int *nranks_h, int *rank_h) {
+    if (!ctx) return fail(GBM_E_ARG, "null context");
+    if (nranks_h) *nranks_h = ctx->nranks;
+    if (rank_h) *rank_h = ctx->rank;
+    return GBM_OK;
+}
+
+int gbm_symbol_bits(int32_t max_symbol) {
+    if (max_symbol < 0) return fail(GBM_E_ARG, "gbm_symbol_bits: negative max_symbol");
+    int b = 1;
+    while (b < 31 && (1ll << b) <= (long long)max_symbol) b++;
+    return b;
+}
+
+int64_t gbm_packed_words(int64_t n_rows, int32_t n_features, int32_t bits, int32_t row_align_bits) {
+    if (n_rows < 0 || n_features <= 0 || bits < 1 || bits > 16)
+        return fail(GBM_E_ARG, "gbm_packed_words: bad sizes");
+    if (row_align_bits != 0 && row_align_bits != 32 && row_align_bits != 128)
+        return fail(GBM_E_ARG, "gbm_packed_words: row_align_bits must be 0, 32 or 128");
+    long long total = n_rows * row_stride_bits(n_features, bits, row_align_bits);
+    long long w = (total + 31) / 32;
+    w = (w + 3) / 4 * 4;
+    return w + 4;
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+// gbm_internal.cuh -- shared internals of libgbm.so (device helpers, context, error plumbing).
+// Product code: never includes or links anything under oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/gbm.h"
+
+namespace gbm {
+
+// ------------------------------------------------------------------ error plumbing
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define GBM_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return ::gbm::fail(GBM_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define GBM_NCCL(call)                                                                        \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return ::gbm::fail(GBM_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+#define GBM_TRY(expr)                                                                         \
+    do {                                                                                      \
+        int rc_ = (expr);                                                                     \
+        if (rc_ != GBM_OK)                                                                    \
+            return rc_;                                                                       \
+    } while (0)
+
+#define GBM_REQUIRE(cond, code, msg)                                                          \
+    do {                                                                                      \
+        if (!(cond))                                                                          \
+            return ::gbm::fail((code), (msg));                                                \
+    } while (0)
+
+// device-latched error bits (ctx->dev_err), surfaced by gbm_check
+enum : uint32_t { DERR_LABEL = 1u, DERR_OVERFLOW = 2u, DERR_NONFINITE = 4u };
+
+// ------------------------------------------------------------------ scratch arena
+// A grow-only device buffer carved into named regions per call.  Reallocation synchronises
+// the device (cudaFree), which only happens when a call needs more scratch than before.
+struct Arena {
+    char *base = nullptr;
+    size_t cap = 0, used = 0;
+    int reserve(size_t bytes);
+    void reset() { used = 0; }
+    template <class T> T *take(size_t count) {
+        size_t off = (used + 255) & ~size_t(255);
+        used = off + count * sizeof(T);
+        return reinterpret_cast<T *>(base + off);
+    }
+};
+
+}  // namespace gbm
+
+struct gbm_ctx {
+    int device = 0;
+    int sm_count = 148;
+    size_t smem_optin = 227 * 1024;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    uint32_t *dev_err = nullptr;   // device-latched error bits
+    gbm::Arena arena;              // scratch for the current call
+    gbm::Arena tree_arena;         // scratch owned by gbm_build_tree
+};
+
+namespace gbm {
+
+int ctx_enter(gbm_ctx *ctx);  // cudaSetDevice + argument check
+int allreduce_i64(gbm_ctx *ctx, long long *buf, size_t count, cudaStream_t s);
+
+// ------------------------------------------------------------------ packed-matrix access
+// The layout of gbm_compress (R3): element (r, f) at stream bit r*stride + f*bits.
+struct QM {
+    const uint32_t *P;
+    long long stride;  // bits per row
+    int F, bits, B;    // features, symbol width, sentinel (max_bins)
+    int S;             // symbols per unit (a unit spans <= 32 bits)
+    int U;             // units per row = ceil(F / S)
+};
+
+inline long long row_stride_bits(int F, int bits, int row_align_bits) {
+    long long rb = (long long)F * bits;
+    if (row_align_bits > 0) rb = (rb + row_align_bits - 1) / row_align_bits * row_align_bits;
+    return rb;
+}
+
+inline QM make_qm(const gbm_qmatrix *q) {
+    QM m;
+    m.P = q->packed_d;
+    m.F = q->n_features;
+    m.bits = q->bits;
+    m.B = q->max_bins;
+    m.stride = row_stride_bits(q->n_features, q->bits, q->row_align_bits);
+    m.S = 32 / q->bits;
+    m.U = (q->n_features + m.S - 1) / m.S;
+    return m;
+}
+
+// nbits (<= 32) stream bits starting at bitpos; the buffer's 4 zero pad words make the
+// second word always readable.
+__device__ __forceinline__ uint32_t get_bits(const uint32_t *__restrict__ P, long long bitpos,
+                                             int nbits) {
+    long long w = bitpos >> 5;
+    int off = (int)(bitpos & 31);
+    uint32_t lo = __ldg(P + w);
+    uint64_t v = lo;
+    if (off + nbits > 32) v |= (uint64_t)__ldg(P + w + 1) << 32;
+    v >>= off;
+    return nbits == 32 ? (uint32_t)v : (uint32_t)v & ((1u << nbits) - 1u);
+}
+
+__device__ __forceinline__ uint32_t symbol_at(const QM &m, long long row, int f) {
+    return get_bits(m.P, row * m.stride + (long long)f * m.bits, m.bits);
+}
+
+// exact floor(j / d) for j < 2^32 / d via a 32-bit multiply-high (magic = ceil(2^32 / d))
+inline uint32_t div_magic(uint32_t d) { return (uint32_t)(((1ull << 32) + d - 1) / d); }
+__device__ __forceinline__ uint32_t fast_div(uint32_t j, uint32_t magic) { return __umulhi(j, magic); }
+
+// ------------------------------------------------------------------ fp64 without contraction
+// Every parity-relevant fp64 operation goes through an explicitly rounded intrinsic so that no
+// FMA contraction can occur (R20) regardless of compiler flags.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// (double)int64 rounded to nearest even, then an exact power-of-two scale (2^-s)
+__device__ __forceinline__ double fixed_to_double(long long v, int s) {
+    return scalbn(__ll2double_rn(v), -s);
+}
+
+__host__ __device__ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace gbm

@@ -1,0 +1,210 @@
+// gradients.cu -- §2.5 gradient evaluation (Eq. 1-2) with the fixed point of R14,
+// §2.4 prediction and the margin update on sm_100a.
+//
+// Bit-exactness (R19-R21): the sigmoid goes through det_exp, which uses only correctly rounded
+// IEEE +,-,*,/, fma and an exact power-of-two scale, and every fp64 op is an explicitly rounded
+// intrinsic (no contraction).  All three kernels are plain streaming kernels: HBM-bound.
+#include "gbm_internal.cuh"
+
+namespace gbm {
+
+__constant__ double DE_C[14] = {
+    0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5,
+    0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
+    0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};
+
+// det_exp(t), t <= 0
+__device__ __forceinline__ double det_exp(double t) {
+    if (t < -745.0) return 0.0;
+    double k = rint(dmul(t, 0x1.71547652b82fep+0));
+    double r = fma(-k, 0x1.62e42feep-1, t);
+    r = fma(-k, 0x1.a39ef35793c76p-33, r);
+    double p = DE_C[13];
+#pragma unroll
+    for (int i = 12; i >= 0; --i) p = fma(p, r, DE_C[i]);
+    return scalbn(p, (int)k);
+}
+
+__device__ __forceinline__ double sigmoid(double x) {
+    if (x >= 0.0) {
+        double e = det_exp(-x);
+        return ddiv(1.0, dadd(1.0, e));
+    }
+    double e = det_exp(x);
+    return ddiv(e, dadd(1.0, e));
+}
+
+// Eq. 1-2 (logistic) / squared error; returns false on a label-domain violation
+__device__ __forceinline__ bool grad_hess(int obj, double m, float yl, double &g, double &h) {
+    double y = (double)yl;
+    if (obj == GBM_SQUARED_ERROR) {
+        g = dsub(m, y);
+        h = 1.0;
+        return true;
+    }
+    double s = sigmoid(m);
+    g = dsub(s, y);
+    h = dmul(s, dsub(1.0, s));
+    return yl == 0.0f || yl == 1.0f;
+}
+
+constexpr int G_THREADS = 256;
+
+__global__ void __launch_bounds__(G_THREADS) grad_max_kernel(int obj, const double *__restrict__ margin,
+                                                             const float *__restrict__ label, long long n,
+                                                             unsigned long long *__restrict__ maxbits,
+                                                             uint32_t *dev_err) {
+    double mg = 0.0, mh = 0.0;
+    bool bad = false;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double g, h;
+        bad |= !grad_hess(obj, __ldg(margin + i), __ldg(label + i), g, h);
+        mg = fmax(mg, fabs(g));
+        mh = fmax(mh, fabs(h));
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(dev_err, DERR_LABEL);
+    for (int o = 16; o > 0; o >>= 1) {
+        mg = fmax(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+        mh = fmax(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+    }
+    __shared__ double sg[G_THREADS / 32], sh[G_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) {
+        sg[threadIdx.x >> 5] = mg;
+        sh[threadIdx.x >> 5] = mh;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < G_THREADS / 32; ++w) {
+            mg = fmax(mg, sg[w]);
+            mh = fmax(mh, sh[w]);
+        }
+        // non-negative doubles order like their bit patterns
+        atomicMax(maxbits + 0, (unsigned long long)__double_as_longlong(mg));
+        atomicMax(maxbits + 1, (unsigned long long)__double_as_longlong(mh));
+    }
+}
+
+__device__ __forceinline__ int scale_of(unsigned long long bits, int P) {
+    double M = __longlong_as_double((long long)bits);
+    int E = 0;
+    if (M > 0.0) frexp(M, &E);
+    return P - E;
+}
+
+__global__ void __launch_bounds__(G_THREADS) grad_quant_kernel(int obj, int P, const double *__restrict__ margin,
+                                                               const float *__restrict__ label, long long n,
+                                                               const unsigned long long *__restrict__ maxbits,
+                                                               int2 *__restrict__ qpair, int32_t *__restrict__ scale) {
+    const int sg = scale_of(maxbits[0], P), sh = scale_of(maxbits[1], P);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scale[0] = sg;
+        scale[1] = sh;
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double g, h;
+        grad_hess(obj, __ldg(margin + i), __ldg(label + i), g, h);
+        qpair[i] = make_int2(__double2int_rn(scalbn(g, sg)), __double2int_rn(scalbn(h, sh)));
+    }
+}
+
+__global__ void update_margins_kernel(const double *__restrict__ w, const int32_t *__restrict__ leaf,
+                                      long long n, double *__restrict__ margin) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        margin[i] = dadd(margin[i], __ldg(w + __ldg(leaf + i)));
+}
+
+__global__ void predict_kernel(int n_trees, long long cap, const int8_t *__restrict__ kind,
+                               const int32_t *__restrict__ feature, const float *__restrict__ thr,
+                               const int8_t *__restrict__ dl, const double *__restrict__ weight,
+                               double base, const float *__restrict__ X, long long n, int F,
+                               double *__restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float *x = X + i * F;
+        double m = base;
+        for (int t = 0; t < n_trees; ++t) {
+            long long o = t * cap, k = 0;
+            while (__ldg(kind + o + k) == GBM_NODE_SPLIT) {
+                int f = __ldg(feature + o + k);
+                float v = f < F ? __ldg(x + f) : __int_as_float(0x7fffffff);
+                bool left = isnan(v) ? (__ldg(dl + o + k) != 0) : (v <= __ldg(thr + o + k));
+                k = left ? 2 * k + 1 : 2 * k + 2;
+            }
+            m = dadd(m, __ldg(weight + o + k));
+        }
+        out[i] = m;
+    }
+}
+
+static int grid_for(long long work, int threads, int sm) {
+    long long g = (work + threads - 1) / threads;
+    long long cap = (long long)sm * 16;
+    return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace gbm
+
+using namespace gbm;
+
+extern "C" {
+
+int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const double *margin_d,
+                  const float *label_d, int64_t n_rows, int32_t *qpair_d, int32_t *scale_d,
+                  void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(objective == GBM_SQUARED_ERROR || objective == GBM_LOGISTIC, GBM_E_ARG,
+                "gbm_gradients: unknown objective");
+    GBM_REQUIRE(grad_bits >= 1 && grad_bits <= 30, GBM_E_ARG, "gbm_gradients: grad_bits in 1..30");
+    GBM_REQUIRE(n_rows > 0 || (ctx->comm && ctx->nranks > 1), GBM_E_EMPTY, "gbm_gradients: zero rows");
+    GBM_REQUIRE((margin_d && label_d && qpair_d) || n_rows == 0, GBM_E_ARG, "gbm_gradients: null pointer");
+    GBM_REQUIRE(scale_d, GBM_E_ARG, "gbm_gradients: null scale");
+    cudaStream_t s = (cudaStream_t)stream;
+    GBM_TRY(ctx->arena.reserve(64));
+    unsigned long long *maxbits = ctx->arena.take<unsigned long long>(2);
+    GBM_CUDA(cudaMemsetAsync(maxbits, 0, 16, s));
+    int grid = grid_for(n_rows, G_THREADS, ctx->sm_count);
+    if (n_rows > 0)
+        grad_max_kernel<<<grid, G_THREADS, 0, s>>>(objective, margin_d, label_d, n_rows, maxbits, ctx->dev_err);
+    if (ctx->comm && ctx->nranks > 1)  // C1: global max of |g|, |h| (exact, order-free)
+        GBM_NCCL(ncclAllReduce(maxbits, maxbits, 2, ncclUint64, ncclMax, ctx->comm, s));
+    grad_quant_kernel<<<grid, G_THREADS, 0, s>>>(objective, grad_bits, margin_d, label_d, n_rows, maxbits,
+                                                 reinterpret_cast<int2 *>(qpair_d), scale_d);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
+int gbm_update_margins(gbm_ctx *ctx, const double *weight_d, const int32_t *row_leaf_d,
+                       int64_t n_rows, double *margin_d, void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(n_rows >= 0 && weight_d && row_leaf_d && margin_d, GBM_E_ARG, "gbm_update_margins: bad arguments");
+    if (n_rows == 0) return GBM_OK;
+    update_margins_kernel<<<grid_for(n_rows, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
+        weight_d, row_leaf_d, n_rows, margin_d);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
+int gbm_predict(gbm_ctx *ctx, int32_t n_trees, int32_t max_depth, const int8_t *kind_d,
+                const int32_t *feature_d, const float *threshold_d, const int8_t *default_left_d,
+                const double *weight_d, double base_margin, const float *X_d, int64_t n_rows,
+                int32_t n_features, double *margin_d, void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(n_trees >= 0 && max_depth >= 0 && max_depth <= 24 && n_rows >= 0 && n_features > 0,
+                GBM_E_ARG, "gbm_predict: bad sizes");
+    GBM_REQUIRE(margin_d && (X_d || n_rows == 0) &&
+                    (n_trees == 0 || (kind_d && feature_d && threshold_d && default_left_d && weight_d)),
+                GBM_E_ARG, "gbm_predict: null pointer");
+    if (n_rows == 0) return GBM_OK;
+    long long cap = (1ll << (max_depth + 1)) - 1;
+    predict_kernel<<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
+        n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, weight_d, base_margin, X_d,
+        n_rows, n_features, margin_d);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,315 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bit-exact on cuts, bin indices, packed words, fixed-point gradients, histograms, row
+partitions, split choices and gains; leaf weights / margins / predictions are bit-exact by
+construction (identical IEEE op sequences) and asserted within the north star's 1e-6 relative
+floor as well.  Sizes span several tiles / work items and ragged tails.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_1806_11248_b200 as G
+    return G
+
+
+@pytest.fixture(scope="module")
+def ctx(G):
+    c = G.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _qm_from_oracle(G, X, B, align, cuts=None):
+    v, p = O.cuts(X, B) if cuts is None else cuts
+    s, mx = O.symbols(X, v, p, B)
+    bits = O.symbol_bits(mx)
+    words = O.pack(s, bits, align)
+    qm = G.QMatrix(dev(words.view(np.int32)), X.shape[0], X.shape[1], bits, align, B,
+                   dev(v if v.size else np.zeros(1, np.float32)), dev(p), p.copy())
+    return qm, v, p, s, bits, words
+
+
+# ------------------------------------------------------------------ a1: cuts
+CUT_CASES = [("rand", 5000, 6, 16, None, 0.0), ("ties", 9000, 5, 32, 40, 0.1),
+             ("lossless", 4097, 3, 256, 200, 0.0), ("wideB", 30000, 2, 1000, None, 0.02),
+             ("one_row", 1, 4, 16, None, 0.0), ("allnan", 100, 3, 8, None, 1.0)]
+
+
+@pytest.mark.parametrize("name,n,F,B,distinct,missing", CUT_CASES)
+def test_cuts_parity(ctx, name, n, F, B, distinct, missing):
+    X = W.random_matrix(hash(name) % 1000, n, F, distinct=distinct, missing=missing)
+    X[0, 0] = -0.0 if n > 1 else X[0, 0]
+    v, p = O.cuts(X, B)
+    cv, cp, mx = ctx.cuts(dev(X), B)
+    np.testing.assert_array_equal(cp.cpu().numpy(), p)
+    np.testing.assert_array_equal(cv.cpu().numpy().view(np.uint32), v.view(np.uint32))
+    _, omx = O.symbols(X, v, p, B)
+    assert mx == omx
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "yearmsd", "higgs", "airline"])
+def test_cuts_parity_workloads(ctx, cfg):
+    X, _ = W.generate(cfg, 0, 2000 if cfg == "tiny" else 60_000)
+    B = W.CONFIGS[cfg].max_bins
+    v, p = O.cuts(X, B)
+    cv, cp, mx = ctx.cuts(dev(X), B)
+    np.testing.assert_array_equal(cp.cpu().numpy(), p)
+    np.testing.assert_array_equal(cv.cpu().numpy(), v)
+
+
+def test_cuts_reject_inf(ctx, G):
+    X = np.ones((10, 2), np.float32)
+    X[3, 1] = np.inf
+    with pytest.raises(G.GbmError) as e:
+        ctx.cuts(dev(X), 8)
+    assert e.value.code == -5
+
+
+# ------------------------------------------------------------------ a2: bin map + pack
+@pytest.mark.parametrize("missing", [0.0, 0.05])
+def test_quantise_parity(ctx, missing):
+    X = W.random_matrix(3, 7001, 9, missing=missing)
+    B = 64
+    v, p = O.cuts(X, B)
+    s, _ = O.symbols(X, v, p, B)
+    bins = ctx.quantise(dev(X), B, dev(v), dev(p))
+    np.testing.assert_array_equal(bins.cpu().numpy(), s)
+
+
+@pytest.mark.parametrize("bits", [1, 2, 3, 4, 5, 7, 8, 9, 11, 13, 16])
+@pytest.mark.parametrize("align", [0, 32, 128])
+def test_compress_parity(ctx, bits, align):
+    rng = np.random.default_rng(bits * 7 + align)
+    n, F = 3001, 13
+    sym = rng.integers(0, 1 << bits, (n, F)).astype(np.uint16)
+    words = ctx.compress(dev(sym), bits, align)
+    np.testing.assert_array_equal(u32(words), O.pack(sym, bits, align))
+
+
+@pytest.mark.parametrize("cfg,align", [("tiny", 0), ("higgs", 32), ("airline", 128),
+                                       ("yearmsd", 32)])
+def test_quantise_compress_parity(ctx, G, cfg, align):
+    X, _ = W.generate(cfg, 0, 2000 if cfg == "tiny" else 40_000,
+                      missing=0.03 if cfg == "tiny" else 0.0)
+    B = W.CONFIGS[cfg].max_bins
+    v, p = O.cuts(X, B)
+    s, mx = O.symbols(X, v, p, B)
+    bits = O.symbol_bits(mx)
+    packed = ctx.quantise_compress(dev(X), B, dev(v), dev(p), bits, align)
+    np.testing.assert_array_equal(u32(packed), O.pack(s, bits, align))
+
+
+def test_compress_overflow_latched(ctx, G):
+    sym = np.full((4, 3), 9, np.uint16)
+    ctx.compress(dev(sym), 3, 0)
+    with pytest.raises(G.GbmError) as e:
+        ctx.check()
+    assert e.value.code == -3
+
+
+# ------------------------------------------------------------------ a3: gradients
+@pytest.mark.parametrize("obj", ["reg:squarederror", "binary:logistic"])
+@pytest.mark.parametrize("P", [15, 30, 7])
+def test_gradients_parity(ctx, obj, P):
+    rng = np.random.default_rng(P)
+    n = 300_001
+    m = rng.standard_normal(n) * (6 if obj == "binary:logistic" else 30)
+    m[:5] = [0.0, 40.0, -40.0, 709.0, -745.5]
+    y = ((rng.random(n) < 0.5).astype(np.float32) if obj == "binary:logistic"
+         else (rng.standard_normal(n) * 20).astype(np.float32))
+    _, _, q, sc = O.gradients(obj, m, y, P)
+    qg, sg = ctx.gradients(obj, dev(m), dev(y), P)
+    np.testing.assert_array_equal(qg.cpu().numpy(), q)
+    assert tuple(sg.cpu().tolist()) == sc
+
+
+def test_gradients_label_error(ctx, G):
+    y = np.array([0, 1, 2, 1], np.float32)
+    ctx.gradients("binary:logistic", dev(np.zeros(4)), dev(y), 15)
+    with pytest.raises(G.GbmError) as e:
+        ctx.check()
+    assert e.value.code == -4
+
+
+# ------------------------------------------------------------------ a4/a6: histograms
+@pytest.mark.parametrize("P", [15, 30])
+@pytest.mark.parametrize("cfg,align,missing", [("higgs", 32, 0.0), ("tiny", 0, 0.05),
+                                               ("airline", 128, 0.0), ("yearmsd", 32, 0.01)])
+def test_histogram_parity(ctx, G, P, cfg, align, missing):
+    n = 2000 if cfg == "tiny" else 150_000
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    qm, v, p, s, bits, words = _qm_from_oracle(G, X, W.CONFIGS[cfg].max_bins, align)
+    rng = np.random.default_rng(1)
+    margin = rng.standard_normal(n)
+    obj = "reg:squarederror"
+    _, _, q, sc = O.gradients(obj, margin, y, P)
+    qd = dev(q)
+    # all rows (identity) and a sorted random subset (gather)
+    for rows in (None, np.sort(rng.choice(n, n // 3, replace=False)).astype(np.uint32)):
+        sel = np.arange(n) if rows is None else rows.astype(np.int64)
+        ref = O.node_histogram(words, X.shape[1], bits, align, p, qm.max_bins, q, sel)
+        got = ctx.build_histogram(qm, qd, P, None if rows is None else dev(rows.view(np.int32)))
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ a9: EvaluateSplit
+@pytest.mark.parametrize("seed", range(4))
+def test_evaluate_parity(ctx, G, seed):
+    X, y = W.generate("higgs", 0, 20_000, seed_offset=seed)
+    qm, v, p, s, bits, words = _qm_from_oracle(G, X, 256, 32)
+    rng = np.random.default_rng(seed)
+    nodes = []
+    _, _, q, sc = O.gradients("binary:logistic", rng.standard_normal(20_000) * 0.3, y, 15)
+    for k in range(6):
+        rows = np.sort(rng.choice(20_000, 500 * (k + 1), replace=False)).astype(np.int64)
+        H = O.node_histogram(words, 28, bits, 32, p, 256, q, rows)
+        T = q[rows].astype(np.int64).sum(0)
+        nodes.append((H, T))
+    lam, gam, mcw = (1.0, 0.0, 1.0) if seed % 2 == 0 else (0.5, 0.1, 3.0)
+    hist = dev(np.stack([h for h, _ in nodes]))
+    tot = dev(np.stack([t for _, t in nodes]))
+    out = ctx.evaluate_splits(qm, hist, tot, dev(np.array(sc, np.int32)), reg_lambda=lam,
+                              gamma=gam, min_child_weight=mcw)
+    out = {k: v.cpu().numpy() for k, v in out.items()}
+    for j, (H, T) in enumerate(nodes):
+        r = O.evaluate_split(H, p, T[0], T[1], sc, lam, gam, mcw)
+        assert bool(out["split"][j]) == r["split"]
+        assert out["gain"][j] == r["gain"]
+        if r["feature"] >= 0:
+            assert (out["feature"][j], out["bin"][j], bool(out["default_left"][j])) == \
+                (r["feature"], r["bin"], r["default_left"])
+            assert tuple(out["child"][j]) == r["L"] + r["R"]
+
+
+# ------------------------------------------------------------------ a5: RepartitionInstances
+@pytest.mark.parametrize("n_sel", [0, 1, 31, 1024, 1025, 70_001])
+def test_repartition_parity(ctx, G, n_sel):
+    X, y = W.generate("higgs", 0, 80_000, missing=0.02)
+    qm, v, p, s, bits, words = _qm_from_oracle(G, X, 256, 32)
+    rng = np.random.default_rng(n_sel)
+    rows = np.sort(rng.choice(80_000, n_sel, replace=False)).astype(np.uint32)
+    f, b, dl = 3, 100, 1
+    sym = s[rows.astype(np.int64), f]
+    left = np.where(sym == 256, bool(dl), sym <= b)
+    ref = np.concatenate([rows[left], rows[~left]])
+    out, nl = ctx.repartition(qm, dev(rows.view(np.int32)), f, b, dl)
+    np.testing.assert_array_equal(u32(out), ref)
+    assert int(nl.item()) == int(left.sum())
+
+
+# ------------------------------------------------------------------ whole trees and rounds
+def _compare_tree(gt, ot):
+    for k in ("kind", "feature", "bin", "default_left", "sum_qg", "sum_qh"):
+        np.testing.assert_array_equal(gt[k], ot[k], err_msg=k)
+    np.testing.assert_array_equal(gt["threshold"].view(np.uint32), ot["threshold"].view(np.uint32))
+    np.testing.assert_array_equal(gt["gain"], ot["gain"])
+    # leaf weights: bit-exact by construction; the north-star floor is 1e-6 relative
+    np.testing.assert_allclose(gt["weight"], ot["weight"], rtol=1e-6, atol=0)
+    np.testing.assert_array_equal(gt["weight"], ot["weight"])
+
+
+TREE_CASES = [
+    # cfg, rows, missing, align, P, rounds, depth override
+    ("tiny", 2000, 0.0, 32, 15, 3, None),
+    ("tiny", 2000, 0.05, 0, 30, 3, 5),
+    ("yearmsd", 30_000, 0.0, 32, 15, 3, None),
+    ("higgs", 100_000, 0.0, 32, 15, 3, None),
+    ("higgs", 50_000, 0.02, 128, 30, 2, None),
+    ("airline", 120_000, 0.0, 32, 15, 2, None),
+]
+
+
+@pytest.mark.parametrize("cfg,n,missing,align,P,rounds,depth", TREE_CASES)
+def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth):
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    D = c.max_depth if depth is None else depth
+    kw = dict(eta=0.3, reg_lambda=1.0, gamma=0.0, mcw=1.0)
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=D, grad_bits=P,
+                   row_align_bits=align, **kw)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=D,
+                   grad_bits=P, row_align_bits=align, base_margin=ob.base_margin, eta=0.3,
+                   reg_lambda=1.0, gamma=0.0, min_child_weight=1.0)
+    np.testing.assert_array_equal(u32(gb.qm.packed), ob.words)
+    for r in range(rounds):
+        ot = ob.round()
+        gt = gb.round().to_numpy()
+        np.testing.assert_array_equal(gb.qpair.cpu().numpy(), ob.last["qpair"])
+        _compare_tree(gt, ot)
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    # prediction (§2.4) on the training rows and on fresh rows
+    Xt, _ = W.generate(cfg, n, n + 5000, n_rows=max(n + 5000, c.n_rows))
+    np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
+    np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy(), ob.predict(Xt))
+
+
+def test_max_depth_zero_and_one(ctx, G):
+    X, y = W.generate("tiny")
+    for D in (0, 1):
+        ob = O.Booster(X, y, max_bins=16, objective="reg:squarederror", max_depth=D)
+        gb = G.Booster(ctx, dev(X), dev(y), max_bins=16, objective="reg:squarederror",
+                       max_depth=D, base_margin=ob.base_margin)
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+
+
+# ------------------------------------------------------------------ full-size properties
+@pytest.mark.parametrize("cfg", ["higgs"])
+def test_full_size_round_properties(ctx, G, cfg):
+    """BASELINE.json full size, in bench.py's launch configuration: exact gradient parity for
+    every row, exact root histogram, exact child totals of every node from row_leaf, and the
+    row->leaf map of sampled rows re-derived by the oracle's predictor on the raw values."""
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg)
+    n, F = X.shape
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective,
+                   max_depth=c.max_depth, eta=c.eta)
+    # cuts on a sample of columns are checked elsewhere; here: gradients + one round
+    gb.ctx.gradients(c.objective, gb.margin, gb.y, gb.grad_bits, out=gb.qpair, scale=gb.scale)
+    _, _, q, sc = O.gradients(c.objective, np.zeros(n), y, gb.grad_bits)
+    np.testing.assert_array_equal(gb.qpair.cpu().numpy(), q)
+    words = u32(gb.qm.packed)
+    p = gb.qm.cut_ptr_h
+    root = ctx.build_histogram(gb.qm, gb.qpair, gb.grad_bits).cpu().numpy()
+    ref = O.node_histogram(words, F, gb.qm.bits, 32, p, c.max_bins, q, np.arange(n))
+    np.testing.assert_array_equal(root, ref)
+    tree = gb.round().to_numpy()
+    rl = gb.row_leaf.cpu().numpy()
+    # root split == oracle EvaluateSplit on the full root histogram
+    T = q.astype(np.int64).sum(0)
+    r = O.evaluate_split(ref, p, T[0], T[1], sc, 1.0, 0.0, 1.0)
+    assert (tree["feature"][0], tree["bin"][0], bool(tree["default_left"][0])) == \
+        (r["feature"], r["bin"], r["default_left"]) and tree["gain"][0] == r["gain"]
+    # every node's totals == sum of qpair over the rows of its subtree (exact, int64)
+    cap = tree["kind"].shape[0]
+    sums = np.zeros((cap, 2), np.int64)
+    np.add.at(sums, rl, q.astype(np.int64))
+    for k in range(cap - 1, 0, -1):
+        sums[(k - 1) // 2] += sums[k] if tree["kind"][k] else 0
+    present = tree["kind"] > 0
+    np.testing.assert_array_equal(sums[present, 0], tree["sum_qg"][present])
+    np.testing.assert_array_equal(sums[present, 1], tree["sum_qh"][present])
+    # sampled rows: the leaf the oracle's predictor reaches on raw values == row_leaf
+    idx = np.random.default_rng(0).choice(n, 20_000, replace=False)
+    tid = {k: v.copy() for k, v in tree.items()}
+    tid["weight"] = np.arange(cap, dtype=np.float64)
+    leaf = O.predict([tid], c.max_depth, 0.0, X[idx]).astype(np.int64)
+    np.testing.assert_array_equal(leaf, rl[idx])
