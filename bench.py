@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- seconds per boosting round of the B200 hot path (BASELINE.json metric).
+
+A "step" is one boosting round of the Fig. 1 pipeline over the whole configured
+workload: gradients (Eq. 1-2, fixed point, collective max) -> Algorithm 1 tree (root histogram,
+then per level partition + smaller-child histogram + NCCL allreduce + subtraction + evaluate)
+-> margin update.  One-time quantile cuts and quantise+compress are timed separately
+("one_time"), prediction too ("predict_ms").
+
+Default workload: the Higgs-shaped config (11M x 28, 256 bins, depth 6, logistic), the
+BASELINE.json config the metric "(depth 6, 256 bins) at 1/2/4/8 B200" is quoted on that fits one
+GPU.  Inputs (packed matrix 308 MB + per-row state) exceed the 126 MB
+L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config higgs]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (N > 1)
+  python bench.py --impl reference   # the CPU oracle, the reference arm of this tier
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (of fallback)
+METRIC = "sec/boosting round (depth 6, 256 bins) at 1/2/4/8 B200; histogram GB/s vs HBM peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="higgs", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=None, help="override the row count (debug)")
+    ap.add_argument("--grad-bits", type=int, default=15)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=500_000)
+    ap.add_argument("--cpu-rounds", type=int, default=3)
+    ap.add_argument("--json-out", default=None)
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    return a
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    """dram read+write bytes per launch of the histogram kernel from the committed ncu summary
+    (profiles/ncu_hist_<config>.json, written from an `ncu --set full` capture), or None."""
+    p = os.path.join(ROOT, "profiles", f"ncu_hist_{config}.json")
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None
+
+
+class Clocks:
+    """nvidia-smi sampler running across the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(gpu_index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [s for s, pw in zip(sm, power) if pw > 200.0] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(load)}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_ours(a, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1806_11248_b200 as G
+
+    torch.cuda.set_device(local)
+    cfg = W.CONFIGS[a.config]
+    n = a.rows or cfg.n_rows
+    lo, hi = W.shard_range(n, rank, world)
+    t_gen = time.time()
+    X, y = W.generate(a.config, lo, hi, n_rows=n)
+    t_gen = time.time() - t_gen
+    dev = torch.device("cuda", local)
+    # base margin: 0 (logistic) / global label mean (squared error), host-side in row order
+    if cfg.objective == "binary:logistic":
+        beta = 0.0
+    else:
+        s = torch.tensor([float(np.sum(y.astype(np.float64))), float(len(y))], dtype=torch.float64)
+        if world > 1:
+            s = s.to(dev)
+            dist.all_reduce(s)
+        beta = float(s[0] / s[1])
+    ctx = G.Context(local)
+    if world > 1:
+        ctx.comm_init_from_torch()
+    kw = dict(max_bins=cfg.max_bins, objective=cfg.objective, max_depth=cfg.max_depth,
+              eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
+              min_child_weight=cfg.min_child_weight, grad_bits=a.grad_bits, base_margin=beta)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident run: inputs already in HBM when the timed region starts
+    Xd = torch.from_numpy(X).to(dev)
+    yd = torch.from_numpy(y).to(dev)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cuts = ctx.cuts(Xd, cfg.max_bins)
+    e1.record(stream)
+    e2 = torch.cuda.Event(enable_timing=True)
+    booster = G.Booster(ctx, Xd, yd, cuts=cuts, **kw)
+    e2.record(stream)
+    torch.cuda.synchronize()
+    one_time = {"cuts_ms": max_over_ranks(e0.elapsed_time(e1)),
+                "quantise_compress_ms": max_over_ranks(e1.elapsed_time(e2)),
+                "bits": booster.qm.bits, "n_bins_total": booster.qm.n_bins_total,
+                "packed_bytes_per_gpu": booster.qm.packed.numel() * 4,
+                "generate_s_host": round(t_gen, 2)}
+    for _ in range(a.warmup):
+        booster.round(keep_tree=False)
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(a.steps):
+        booster.round(keep_tree=False)
+    t1.record(stream)
+    barrier()
+    ms_total = t0.elapsed_time(t1)
+    launches = ctx.launch_count() - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    clk = clocks.stop()
+    ms_step = max_over_ranks(ms_total / a.steps)
+
+    # ---- dominant kernel: the histogram pass (root + level launches), algorithmic bytes
+    hist_ms = prof["hist_root"]["ms"] + prof["hist_level"]["ms"]
+    hist_bytes = prof["hist_root"]["bytes"] + prof["hist_level"]["bytes"]
+    hist_launches = prof["hist_root"]["launches"] + prof["hist_level"]["launches"]
+    peak, peak_src = measured_peak()
+    achieved = hist_bytes / (hist_ms * 1e-3) / 1e9 if hist_ms > 0 else 0.0
+    traffic, traffic_src = ncu_traffic(a.config)
+    roofline = {"bound": "hbm", "kernel": "hist_kernel (root + level launches)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": hist_bytes / max(1, hist_launches),
+                "avg_launch_ms": hist_ms / max(1, hist_launches), "launches": hist_launches,
+                "peak_source": peak_src, "traffic_source": traffic_src,
+                "share_of_step": round(hist_ms / ms_total, 4) if ms_total else None}
+    stages = {k: {"ms_per_round": round(v["ms"] / a.steps, 4),
+                  "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
+              for k, v in prof.items() if v["launches"]}
+    allreduce_ms = prof["allreduce"]["ms"] / a.steps
+
+    # ---- predict (§2.4) over the training rows with the warm-up+timed trees? -> one tree set
+    booster.trees = []
+    for _ in range(10):
+        booster.round()
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    booster.predict(Xd)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    predict_ms = max_over_ranks(p0.elapsed_time(p1))
+    del booster, Xd, yd
+    torch.cuda.empty_cache()
+
+    # ---- end to end through the public API from pinned host memory
+    e2e = None
+    if not a.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        yh = torch.from_numpy(y).pin_memory()
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        Xd = Xh.to(dev, non_blocking=True)
+        yd = yh.to(dev, non_blocking=True)
+        b2 = G.Booster(ctx, Xd, yd, **kw)
+        d2h = 0
+        for _ in range(a.steps):
+            t = b2.round(keep_tree=False)
+            host_tree = {k: v.to("cpu", non_blocking=True) for k, v in t.arrays.items()}
+            d2h = sum(v.numel() * v.element_size() for v in host_tree.values())
+        s1.record(stream)
+        barrier()
+        e2e_ms = max_over_ranks(s0.elapsed_time(s1) / a.steps)
+        h2d = (X.nbytes + y.nbytes) / a.steps
+        e2e = {"value": e2e_ms / 1e3, "unit": "s/round", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "note": "train() from pinned host X,y: H2D + cuts + quantise/compress + K rounds, "
+                       "each round's tree read back; amortised per round"}
+        del b2, Xd, yd
+
+    # ---- CPU baseline: the oracle as it stands, on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a.config, min(a.cpu_rows, n), a.cpu_rounds, n)
+    return dict(ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages,
+                one_time=one_time, clocks=clk, launches=launches, e2e=e2e, cpu=cpu,
+                predict_ms=predict_ms, allreduce_ms=allreduce_ms, grad_bits=a.grad_bits)
+
+
+def cpu_baseline(config, rows, rounds, n_full):
+    import oracle as O
+    cfg = W.CONFIGS[config]
+    X, y = W.generate(config, 0, rows, n_rows=max(rows, cfg.n_rows))
+    beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
+    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective,
+                  max_depth=cfg.max_depth, eta=cfg.eta, reg_lambda=cfg.reg_lambda,
+                  gamma=cfg.gamma, mcw=cfg.min_child_weight, base_margin=beta)
+    t = time.perf_counter()
+    for _ in range(rounds):
+        b.round()
+    per = (time.perf_counter() - t) / rounds
+    return {"value": per * n_full / rows, "unit": "s/round", "cores": 1, "kind": "oracle",
+            "sample": f"{rounds} rounds on the first {rows} rows of the {config} workload, "
+                      f"{per:.3f} s/round measured, scaled x{n_full / rows:.1f} to {n_full} rows "
+                      "(histogram work is linear in rows); single-threaded C oracle, -O2"}
+
+
+def run_reference(a):
+    """Reference arm of this tier: the CPU oracle, as it stands, on the host cores."""
+    import oracle as O
+    cfg = W.CONFIGS[a.config]
+    n = a.rows or cfg.n_rows
+    budget_s = 150.0
+    per_row = 4.5e-6 * (cfg.n_features / 28.0) * (cfg.max_depth / 6.0)
+    rows = int(min(n, max(20_000, budget_s / (a.steps + a.warmup) / per_row)))
+    X, y = W.generate(a.config, 0, rows, n_rows=max(rows, cfg.n_rows))
+    beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
+    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective, max_depth=cfg.max_depth,
+                  eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
+                  mcw=cfg.min_child_weight, base_margin=beta)
+    for _ in range(a.warmup):
+        b.round()
+    t = time.perf_counter()
+    for _ in range(a.steps):
+        b.round()
+    per = (time.perf_counter() - t) / a.steps
+    value = per * n / rows
+    sample = (f"each step = one oracle boosting round on the first {rows} of {n} rows "
+              f"({per:.3f} s measured), scaled x{n / rows:.1f} to the full workload")
+    out = {"metric": METRIC, "value": value, "unit": "s/round", "n_gpus": 0, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": a.config, "rows": n, "features": cfg.n_features,
+                      "max_bins": cfg.max_bins, "max_depth": cfg.max_depth,
+                      "objective": cfg.objective},
+           "cpu_baseline": {"value": value, "unit": "s/round", "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "s/round", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    a = parse()
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if a.impl == "reference":
+        rc = 0
+        if rank == 0:
+            rc = run_reference(a)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return rc
+    r = run_ours(a, world, rank, local)
+    if rank == 0:
+        cfg = W.CONFIGS[a.config]
+        out = {
+            "metric": METRIC,
+            "value": r["ms_step"] / 1e3,
+            "unit": "s/round",
+            "n_gpus": world,
+            "steps": a.steps,
+            "warmup": a.warmup,
+            "ms_per_step": r["ms_step"],
+            "higher_is_better": False,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": a.config, "rows": r["n"], "features": cfg.n_features,
+                       "max_bins": cfg.max_bins, "max_depth": cfg.max_depth,
+                       "objective": cfg.objective, "eta": cfg.eta, "grad_bits": r["grad_bits"],
+                       "parallelism": f"dp{world} (rows sharded, NCCL histogram allreduce)",
+                       "l2": "inputs larger than L2 (packed matrix + per-row state > 126 MB)"},
+            "roofline": r["roofline"],
+            "cpu_baseline": r["cpu"],
+            "e2e": r["e2e"],
+            "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
+            "stages_ms_per_round": r["stages"],
+            "allreduce_ms_per_round": r["allreduce_ms"],
+            "one_time": r["one_time"],
+            "predict_ms_10_trees": r["predict_ms"],
+        }
+        line = json.dumps(out)
+        print(line)
+        if a.json_out:
+            open(a.json_out, "w").write(line + "\n")
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -67,6 +67,24 @@ GBM_API int gbm_ctx_destroy(gbm_ctx *ctx);  /* frees scratch and the communicato
  * argument errors such as GBM_E_LABEL) latched since the last gbm_check. */
 GBM_API int gbm_check(gbm_ctx *ctx, void *stream);
 
+/* ---------------------------------------------------------------- instrumentation
+ * Optional CUDA-event timing of every kernel launch the context issues, grouped by kernel
+ * (bench.py's per-kernel roofline).  gbm_profile_enable(1) resets and starts recording (it
+ * synchronises the device); gbm_profile_read synchronises, fills one entry per kernel
+ * category (cap >= 16) and starts a new window.  bytes = the launches' ALGORITHMIC bytes
+ * (DESIGN.md "Algorithmic bytes"), rows = rows they processed, counted on the device.
+ * gbm_launch_count: kernel launches issued by the context since creation. */
+typedef struct {
+    char name[32];
+    int64_t launches;
+    double ms;
+    double bytes;
+    double rows;
+} gbm_prof_entry;
+GBM_API int gbm_profile_enable(gbm_ctx *ctx, int enable);
+GBM_API int gbm_profile_read(gbm_ctx *ctx, gbm_prof_entry *out, int32_t cap, int32_t *n_out);
+GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
+
 /* ---------------------------------------------------------------- communicator
  * Rank 0 calls gbm_comm_unique_id and broadcasts the 128 bytes with its own process group
  * (the Python binding uses torch.distributed); then every rank calls gbm_comm_init

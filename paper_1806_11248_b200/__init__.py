@@ -54,6 +54,11 @@ class _Tree(C.Structure):
                                           "gain", "weight", "sum_qg", "sum_qh")]
 
 
+class _ProfEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
+                ("bytes", C.c_double), ("rows", C.c_double)]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "gbm_last_error": (C.c_char_p, []),
@@ -61,6 +66,10 @@ EXPORTS = {
     "gbm_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "gbm_ctx_destroy": (C.c_int, [C.c_void_p]),
     "gbm_check": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gbm_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "gbm_profile_read": (C.c_int, [C.c_void_p, C.POINTER(_ProfEntry), C.c_int32,
+                                   C.POINTER(C.c_int32)]),
+    "gbm_launch_count": (C.c_int64, [C.c_void_p]),
     "gbm_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "gbm_comm_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
     "gbm_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -252,6 +261,22 @@ class Context:
 
     def check(self):
         _call("gbm_check", self.h, _stream())
+
+    # ------------------------------------------------------------ instrumentation
+    def profile(self, enable: bool = True):
+        _call("gbm_profile_enable", self.h, int(bool(enable)))
+
+    def profile_read(self) -> dict:
+        """Per-kernel {launches, ms, bytes, rows} since the last read (synchronises)."""
+        arr = (_ProfEntry * 32)()
+        n = C.c_int32()
+        _call("gbm_profile_read", self.h, arr, 32, C.byref(n))
+        return {arr[i].name.decode(): dict(launches=arr[i].launches, ms=arr[i].ms,
+                                           bytes=arr[i].bytes, rows=arr[i].rows)
+                for i in range(n.value)}
+
+    def launch_count(self) -> int:
+        return int(lib().gbm_launch_count(self.h))
 
     # ------------------------------------------------------------ §2.1 / §2.2
     def cuts(self, X: torch.Tensor, max_bins: int):

@@ -45,6 +45,43 @@ int Arena::reserve(size_t bytes) {
     return GBM_OK;
 }
 
+const char *const PROF_NAMES[PC_N] = {
+    "grad_max", "grad_quant", "hist_root", "hist_level", "part_count", "part_scan",
+    "part_scatter", "part_final", "evaluate", "allreduce", "update_margins", "init_tree",
+    "predict", "cuts", "quantise_compress"};
+
+static cudaEvent_t pool_event(Prof &p) {
+    if (p.pool_used == p.pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        p.pool.push_back(e);
+    }
+    return p.pool[p.pool_used++];
+}
+
+unsigned long long *prof_rows_slot(gbm_ctx *ctx, int *slot) {
+    *slot = -1;
+    if (!ctx->prof.on || ctx->prof.rows_used >= ctx->prof.rows_cap) return nullptr;
+    *slot = ctx->prof.rows_used++;
+    return ctx->prof.rows_dev + *slot;
+}
+
+ProfScope::ProfScope(gbm_ctx *c_, int cat_, cudaStream_t s_, double fixed_, int slot_, double bpr_)
+    : c(c_), cat(cat_), slot(slot_), s(s_), bpr(bpr_), fixed(fixed_) {
+    c->launches += (cat_ == PC_ALLREDUCE) ? 0 : 1;
+    if (!c->prof.on) return;
+    a = pool_event(c->prof);
+    if (a) cudaEventRecord(a, s);
+}
+
+ProfScope::~ProfScope() {
+    if (!c->prof.on || !a) return;
+    cudaEvent_t b = pool_event(c->prof);
+    if (!b) return;
+    cudaEventRecord(b, s);
+    c->prof.recs.push_back(ProfRec{cat, a, b, slot, bpr, fixed});
+}
+
 int ctx_enter(gbm_ctx *ctx) {
     if (!ctx) return fail(GBM_E_ARG, "null context");
     GBM_CUDA(cudaSetDevice(ctx->device));
@@ -98,6 +135,8 @@ int gbm_ctx_destroy(gbm_ctx *ctx) {
     if (ctx->arena.base) cudaFree(ctx->arena.base);
     if (ctx->tree_arena.base) cudaFree(ctx->tree_arena.base);
     if (ctx->dev_err) cudaFree(ctx->dev_err);
+    if (ctx->prof.rows_dev) cudaFree(ctx->prof.rows_dev);
+    for (auto e : ctx->prof.pool) cudaEventDestroy(e);
     delete ctx;
     return GBM_OK;
 }
@@ -146,6 +185,55 @@ int gbm_comm_info(gbm_ctx *ctx, int *nranks_h, int *rank_h) {
     if (rank_h) *rank_h = ctx->rank;
     return GBM_OK;
 }
+
+int gbm_profile_enable(gbm_ctx *ctx, int enable) {
+    GBM_TRY(ctx_enter(ctx));
+    Prof &p = ctx->prof;
+    GBM_CUDA(cudaDeviceSynchronize());
+    p.recs.clear();
+    p.pool_used = 0;
+    p.rows_used = 0;
+    if (enable && !p.rows_dev) {
+        p.rows_cap = 1 << 16;
+        GBM_CUDA(cudaMalloc(&p.rows_dev, sizeof(unsigned long long) * p.rows_cap));
+    }
+    if (p.rows_dev) GBM_CUDA(cudaMemset(p.rows_dev, 0, sizeof(unsigned long long) * p.rows_cap));
+    p.on = enable != 0;
+    return GBM_OK;
+}
+
+int gbm_profile_read(gbm_ctx *ctx, gbm_prof_entry *out, int32_t cap, int32_t *n_out) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(out && n_out && cap >= PC_N, GBM_E_ARG, "gbm_profile_read: need room for every category");
+    Prof &p = ctx->prof;
+    GBM_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> rows(p.rows_used > 0 ? p.rows_used : 1, 0);
+    if (p.rows_used > 0)
+        GBM_CUDA(cudaMemcpy(rows.data(), p.rows_dev, sizeof(unsigned long long) * p.rows_used, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < PC_N; ++c) {
+        memset(&out[c], 0, sizeof(gbm_prof_entry));
+        strncpy(out[c].name, PROF_NAMES[c], sizeof(out[c].name) - 1);
+    }
+    for (const ProfRec &r : p.recs) {
+        float ms = 0.0f;
+        GBM_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        gbm_prof_entry &e = out[r.cat];
+        e.launches += 1;
+        e.ms += ms;
+        double rw = r.rows_slot >= 0 ? (double)rows[r.rows_slot] : 0.0;
+        e.bytes += r.fixed_bytes + rw * r.bytes_per_row;
+        e.rows += rw;
+    }
+    *n_out = PC_N;
+    // reset for the next window (keeps profiling on)
+    p.recs.clear();
+    p.pool_used = 0;
+    p.rows_used = 0;
+    if (p.rows_dev) GBM_CUDA(cudaMemset(p.rows_dev, 0, sizeof(unsigned long long) * p.rows_cap));
+    return GBM_OK;
+}
+
+int64_t gbm_launch_count(gbm_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
 int gbm_symbol_bits(int32_t max_symbol) {
     if (max_symbol < 0) return fail(GBM_E_ARG, "gbm_symbol_bits: negative max_symbol");

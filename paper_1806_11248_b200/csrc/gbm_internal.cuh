@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/gbm.h"
 
@@ -61,6 +62,34 @@ struct Arena {
     }
 };
 
+// ------------------------------------------------------------------ profiling
+// Optional per-launch CUDA-event timing inside the library (bench.py's roofline): every kernel
+// launch site is bracketed by a ProfScope; when profiling is on, two events are recorded on the
+// launching stream and the launch's algorithmic bytes are kept as  fixed + rows * bytes_per_row,
+// where `rows` is counted on the device (rows_slot) when only the device knows it.
+enum ProfCat {
+    PC_GRAD_MAX = 0, PC_GRAD_QUANT, PC_HIST_ROOT, PC_HIST_LEVEL, PC_PART_COUNT, PC_PART_SCAN,
+    PC_PART_SCATTER, PC_PART_FINAL, PC_EVAL, PC_ALLREDUCE, PC_MARGINS, PC_INIT, PC_PREDICT,
+    PC_CUTS, PC_QUANT, PC_N
+};
+extern const char *const PROF_NAMES[PC_N];
+
+struct ProfRec {
+    int cat;
+    cudaEvent_t a, b;
+    int rows_slot;
+    double bytes_per_row, fixed_bytes;
+};
+
+struct Prof {
+    bool on = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+    unsigned long long *rows_dev = nullptr;  // device row counters, one per launch slot
+    int rows_cap = 0, rows_used = 0;
+};
+
 }  // namespace gbm
 
 struct gbm_ctx {
@@ -72,11 +101,26 @@ struct gbm_ctx {
     uint32_t *dev_err = nullptr;   // device-latched error bits
     gbm::Arena arena;              // scratch for the current call
     gbm::Arena tree_arena;         // scratch owned by gbm_build_tree
+    gbm::Prof prof;                // optional event timing (gbm_profile_*)
+    long long launches = 0;        // kernel launches issued by this context
 };
 
 namespace gbm {
 
 int ctx_enter(gbm_ctx *ctx);  // cudaSetDevice + argument check
+
+// device row counter for the next profiled launch (nullptr when profiling is off)
+unsigned long long *prof_rows_slot(gbm_ctx *ctx, int *slot);
+
+struct ProfScope {
+    gbm_ctx *c;
+    int cat, slot;
+    cudaStream_t s;
+    double bpr, fixed;
+    cudaEvent_t a = nullptr;
+    ProfScope(gbm_ctx *c_, int cat_, cudaStream_t s_, double fixed_ = 0.0, int slot_ = -1, double bpr_ = 0.0);
+    ~ProfScope();
+};
 int allreduce_i64(gbm_ctx *ctx, long long *buf, size_t count, cudaStream_t s);
 
 // ------------------------------------------------------------------ packed-matrix access

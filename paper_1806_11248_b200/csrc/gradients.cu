@@ -167,12 +167,19 @@ int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const doub
     unsigned long long *maxbits = ctx->arena.take<unsigned long long>(2);
     GBM_CUDA(cudaMemsetAsync(maxbits, 0, 16, s));
     int grid = grid_for(n_rows, G_THREADS, ctx->sm_count);
-    if (n_rows > 0)
+    if (n_rows > 0) {
+        ProfScope ps(ctx, PC_GRAD_MAX, s, (double)n_rows * 12);
         grad_max_kernel<<<grid, G_THREADS, 0, s>>>(objective, margin_d, label_d, n_rows, maxbits, ctx->dev_err);
-    if (ctx->comm && ctx->nranks > 1)  // C1: global max of |g|, |h| (exact, order-free)
+    }
+    if (ctx->comm && ctx->nranks > 1) {  // C1: global max of |g|, |h| (exact, order-free)
+        ProfScope ps(ctx, PC_ALLREDUCE, s, 16.0);
         GBM_NCCL(ncclAllReduce(maxbits, maxbits, 2, ncclUint64, ncclMax, ctx->comm, s));
-    grad_quant_kernel<<<grid, G_THREADS, 0, s>>>(objective, grad_bits, margin_d, label_d, n_rows, maxbits,
-                                                 reinterpret_cast<int2 *>(qpair_d), scale_d);
+    }
+    {
+        ProfScope ps(ctx, PC_GRAD_QUANT, s, (double)n_rows * 20);
+        grad_quant_kernel<<<grid, G_THREADS, 0, s>>>(objective, grad_bits, margin_d, label_d, n_rows, maxbits,
+                                                     reinterpret_cast<int2 *>(qpair_d), scale_d);
+    }
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
@@ -182,6 +189,7 @@ int gbm_update_margins(gbm_ctx *ctx, const double *weight_d, const int32_t *row_
     GBM_TRY(ctx_enter(ctx));
     GBM_REQUIRE(n_rows >= 0 && weight_d && row_leaf_d && margin_d, GBM_E_ARG, "gbm_update_margins: bad arguments");
     if (n_rows == 0) return GBM_OK;
+    ProfScope ps(ctx, PC_MARGINS, (cudaStream_t)stream, (double)n_rows * 20);
     update_margins_kernel<<<grid_for(n_rows, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
         weight_d, row_leaf_d, n_rows, margin_d);
     GBM_CUDA(cudaGetLastError());
@@ -200,6 +208,7 @@ int gbm_predict(gbm_ctx *ctx, int32_t n_trees, int32_t max_depth, const int8_t *
                 GBM_E_ARG, "gbm_predict: null pointer");
     if (n_rows == 0) return GBM_OK;
     long long cap = (1ll << (max_depth + 1)) - 1;
+    ProfScope ps(ctx, PC_PREDICT, (cudaStream_t)stream, (double)n_rows * (4.0 * n_features + 8.0));
     predict_kernel<<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
         n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, weight_d, base_margin, X_d,
         n_rows, n_features, margin_d);

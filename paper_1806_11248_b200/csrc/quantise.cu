@@ -430,6 +430,7 @@ int gbm_quantise_compress(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_
                     max_bins <= 65535,
                 GBM_E_ARG, "gbm_quantise_compress: bad arguments");
     long long stride = row_stride_bits(F, bits, row_align_bits);
+    ProfScope ps(ctx, PC_QUANT, (cudaStream_t)stream, (double)n_rows * F * 4 + (double)packed_words * 4);
     pack_kernel<true><<<grid_for(packed_words, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
         nullptr, X_d, n_rows, F, bits, stride, cv, cp, max_bins, packed_d, packed_words,
         ctx->dev_err);
@@ -477,6 +478,7 @@ int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t 
         return fail(GBM_E_EMPTY, "gbm_cuts: zero rows");
     }
     const long long n_all = n_max;  // rows present in Xg
+    ProfScope ps(ctx, PC_CUTS, s, (double)n_total * F * 4);
     const int tiles = (int)((n_all + SORT_TILE - 1) / SORT_TILE);
     const long long n_pad = (long long)tiles * SORT_TILE;
     Arena &A = ctx->arena;

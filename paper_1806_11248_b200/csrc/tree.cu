@@ -1,27 +1,30 @@
 // tree.cu -- §2.3 decision-tree construction (Algorithm 1) on sm_100a.
 //
-// The tree is grown level-synchronously (R15): every node of a depth is handled by one launch of
-// each kernel, and one NCCL allreduce per level carries the histograms of all of that level's
-// built children.  Per level l = 1..D:
+// The tree is grown level-synchronously (R15): each depth is one pass of a fixed launch
+// sequence, and one NCCL allreduce per level carries the histograms of all of that level's
+// built children.  For level l = 1..D-1 (parents = the nodes of depth l-1):
 //
-//   part_count   RepartitionInstances, pass 1: per 1024-row tile of every split parent, the
-//                split symbol of each row (gathered from the packed matrix), a warp-ballot flag
-//                word per 32 rows, the tile's left count.  Leaf parents write row_leaf.
-//   part_scan    one block: per parent an exclusive scan of its tiles' left counts (stable
-//                order), the children's segments, the histogram work items of the built child,
-//                and the next level's tile plan.
-//   part_scatter RepartitionInstances, pass 2: stable scatter of row ids to the children.
-//   hist         BuildPartialHistograms of the smaller child of every split (R17): privatised
-//                shared-memory int32 histograms (32-bit ATOMS are native on sm_100; 64-bit
-//                shared atomics compile to a CAS loop), flushed into int64 global histograms.
-//   allreduce    AllReduceHistograms: ncclAllReduce(int64, sum) over the level's buffer.
-//   eval         one block per node: sibling = parent - built child (exact in int64), per-feature
-//                warp prefix scans, XGBoost gain in the exact op order of R8, canonical argmax.
+//   plan         1 block: tile plan of the parents (1024-row tiles of their ridx segments) and
+//                the work items of the fused kernel (runs of RUN tiles x feature groups).
+//   part_hist    RepartitionInstances + BuildPartialHistograms, fused (north star, SURVEY §8a
+//                a5+a6): per tile the split symbol of every row (warp-ballot flag words, the
+//                tile's left count), then the rows falling into the parent's smaller child
+//                (R17) are accumulated into a privatised shared-memory histogram; flushed once
+//                per work item into the parent's int64 slot.  Leaf parents write row_leaf.
+//   part_scan    1 block per parent: exclusive scan of its tiles' left counts (stable order)
+//                -> the children's ridx segments.
+//   part_scatter stable scatter of the row ids into the children's segments (flags + ridx only).
+//   allreduce    AllReduceHistograms: ncclAllReduce(int64, sum) over the level's built slots.
+//   eval_feat    one warp per (node, feature): sibling = parent - built child (exact int64),
+//                prefix scan over the feature's bins, both default directions, XGBoost gain in
+//                the op order of R8, best candidate of the feature.
+//   eval_final   1 block per node: canonical argmax over features -> split record / leaf.
 //
-// Exactness of the smem accumulators (R14): a work item covers at most 65535 rows.  With
-// grad_bits P <= 15 every |q| <= 2^15, so a bin's int32 sum stays below 65535 * 2^15 < 2^31
-// ("narrow", 2 ATOMS per update).  With 15 < P <= 30 each q is split as q = hi*2^15 + lo,
-// 0 <= lo < 2^15, |hi| <= 2^15, and hi / lo are accumulated separately ("wide", 4 ATOMS).
+// Shared-memory accumulators (R14): 32-bit ATOMS.ADD is native on sm_100 while 64-bit shared
+// atomics compile to a CAS loop, so bins are int32 and flushed into int64 global histograms
+// after at most 65535 rows.  With grad_bits P <= 15 each |q| <= 2^15 and a bin's sum stays below
+// 65535 * 2^15 < 2^31 ("narrow", 2 ATOMS per update).  With 15 < P <= 30, q = hi*2^15 + lo with
+// 0 <= lo < 2^15, |hi| <= 2^15, both accumulated ("wide", 4 ATOMS per update).
 #include <algorithm>
 #include <climits>
 #include <vector>
@@ -39,29 +42,257 @@ struct NodeDev {
     int pad;
 };
 
-struct HistItem {
+struct RangeItem {  // rows [start, start+len) of a row source, one feature group
     int slot, group;
     long long start;
     int len, pad;
 };
 
+struct TileItem {  // tiles [t0, t1) of parent j, one feature group
+    int j, group, t0, t1;
+};
+
 struct Group {
-    int u_lo, u_hi;      // units [u_lo, u_hi) of the row (a unit = S consecutive features)
+    int u_lo, u_hi;      // units [u_lo, u_hi) of a row (a unit = S consecutive features)
     int bin_lo, bin_hi;  // global bins of the group's features
 };
 
-constexpr int PT = 1024;           // partition tile (rows)
-constexpr int P_THREADS = 256;     // partition block: 8 warps x 4 flag words
-constexpr int H_THREADS = 512;     // histogram block
-constexpr int E_THREADS = 256;     // evaluate block
-constexpr int MAX_CHUNK = 65535;   // rows per histogram work item (exactness bound above)
+struct FeatBest {  // best candidate of one (node, feature)
+    double gain;
+    long long idx;  // canonical candidate order: (global bin)*2 + (dl ? 0 : 1); LLONG_MAX = none
+    long long Lg, Lh;
+};
+
+constexpr int PT = 1024;         // partition tile (rows)
+constexpr int P_THREADS = 256;   // partition kernels: 8 warps x 4 ballot words
+constexpr int H_THREADS = 512;   // histogram / fused kernels
+constexpr int RUN = 16;          // tiles per fused work item (flush amortisation)
+constexpr int E_THREADS = 256;   // evaluation kernels
+constexpr int MAX_CHUNK = 65535; // rows per flush (exactness bound above)
+constexpr int DUMMY_BINS = 256;  // scratch bins for padding features of the byte path
 
 struct EvalParams {
     double eta, lambda, gamma, mcw;
     int max_depth;
 };
 
-// ============================================================== partition
+// ============================================================== shared-memory histogram
+// Layout per channel: [bins of the group (nb)][DUMMY_BINS scratch], channels at stride hstride.
+// narrow: channel 0 = g, 1 = h;  wide: 0 = g_lo, 1 = h_lo, 2 = g_hi, 3 = h_hi.
+struct SmemHist {
+    int *base;
+    int nb, hstride;
+};
+
+template <bool WIDE>
+__device__ __forceinline__ void hist_add(int *hs, int hstride, int bin, int2 q) {
+    if (WIDE) {
+        atomicAdd(hs + bin, q.x & 0x7fff);
+        atomicAdd(hs + hstride + bin, q.y & 0x7fff);
+        atomicAdd(hs + 2 * hstride + bin, q.x >> 15);
+        atomicAdd(hs + 3 * hstride + bin, q.y >> 15);
+    } else {
+        atomicAdd(hs + bin, q.x);
+        atomicAdd(hs + hstride + bin, q.y);
+    }
+}
+
+template <bool WIDE>
+__device__ void smem_zero(const SmemHist &h) {
+    const int n = (WIDE ? 4 : 2) * h.hstride;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) h.base[i] = 0;
+}
+
+// flush the group's bins into the int64 slot (global atomics: several items share a slot)
+template <bool WIDE>
+__device__ void smem_flush(const SmemHist &h, unsigned long long *dst /* slot + 2*bin_lo */) {
+    for (int b = threadIdx.x; b < h.nb; b += blockDim.x) {
+        long long G, H;
+        if (WIDE) {
+            G = (long long)h.base[2 * h.hstride + b] * 32768 + (long long)(unsigned)h.base[b];
+            H = (long long)h.base[3 * h.hstride + b] * 32768 + (long long)(unsigned)h.base[h.hstride + b];
+        } else {
+            G = h.base[b];
+            H = h.base[h.hstride + b];
+        }
+        if (G) atomicAdd(dst + 2 * b, (unsigned long long)G);
+        if (H) atomicAdd(dst + 2 * b + 1, (unsigned long long)H);
+    }
+}
+
+// Per-thread setup of the byte path: thread -> (row lane r0, word w of the group); the bin
+// offsets of its 4 features live in registers (padding features -> the scratch bins).
+struct ByteLane {
+    int r0, rstep, w;  // r0 < 0: thread idle
+    int off[4];
+};
+
+__device__ __forceinline__ ByteLane byte_lane(const QM &qm, const Group &grp, const int *s_off, int nb) {
+    ByteLane L;
+    const int Ug = grp.u_hi - grp.u_lo;
+    const int rb = H_THREADS / Ug;
+    L.rstep = rb;
+    L.r0 = (int)threadIdx.x < rb * Ug ? (int)threadIdx.x / Ug : -1;
+    const int wr = (int)threadIdx.x - (L.r0 < 0 ? 0 : L.r0) * Ug;
+    L.w = grp.u_lo + wr;
+    const int f_lo = grp.u_lo * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        int f = L.w * 4 + j;
+        L.off[j] = (L.r0 >= 0 && f < qm.F) ? s_off[f - f_lo] : nb;  // nb = first scratch bin
+    }
+    return L;
+}
+
+// Accumulate rows [0, nrows) of a row source.  BYTE: 8-bit symbols, rows word-aligned.
+// SENT: the sentinel fits in the symbol width (missing values possible) -> skip it.
+template <bool WIDE, bool BYTE, bool SENT, class RowFn>
+__device__ __forceinline__ void accumulate(const QM &qm, const Group &grp, const int *s_off,
+                                           const SmemHist &h, const int2 *__restrict__ qpair, RowFn rowf,
+                                           int nrows, const ByteLane &L, long long *tg, long long *th,
+                                           bool totals) {
+    if (BYTE) {
+        if (L.r0 < 0) return;
+        totals = totals && L.w == grp.u_lo;   // each row's pair counted once
+        const long long sw = qm.stride >> 5;  // words per row
+        int r = L.r0;
+        for (; r + L.rstep < nrows; r += 2 * L.rstep) {  // two rows in flight
+            const uint32_t ra = rowf(r), rb2 = rowf(r + L.rstep);
+            const uint32_t wa = __ldg(qm.P + ra * sw + L.w), wb = __ldg(qm.P + rb2 * sw + L.w);
+            const int2 qa = __ldg(qpair + ra), qb = __ldg(qpair + rb2);
+            if (totals) {
+                *tg += (long long)qa.x + qb.x;
+                *th += (long long)qa.y + qb.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int sa = (wa >> (8 * j)) & 255, sb = (wb >> (8 * j)) & 255;
+                if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sa, qa);
+                if (!SENT || sb != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sb, qb);
+            }
+        }
+        if (r < nrows) {
+            const uint32_t ra = rowf(r);
+            const uint32_t wa = __ldg(qm.P + ra * sw + L.w);
+            const int2 qa = __ldg(qpair + ra);
+            if (totals) {
+                *tg += qa.x;
+                *th += qa.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int sa = (wa >> (8 * j)) & 255;
+                if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sa, qa);
+            }
+        }
+    } else {
+        // generic widths / layouts: thread -> (row, unit) over the flattened range
+        const int Ug = grp.u_hi - grp.u_lo;
+        const uint32_t magic = 0xffffffffu / (uint32_t)Ug + 1u;
+        const uint32_t total = (uint32_t)nrows * (uint32_t)Ug;
+        const int f_lo = grp.u_lo * qm.S;
+        const uint32_t mask = (1u << qm.bits) - 1u;
+        for (uint32_t j = threadIdx.x; j < total; j += H_THREADS) {
+            const uint32_t r = Ug == 1 ? j : fast_div(j, magic);
+            const int u = grp.u_lo + (int)(j - r * (uint32_t)Ug);
+            const uint32_t row = rowf((int)r);
+            const int2 q = __ldg(qpair + row);
+            if (totals && u == grp.u_lo) {
+                *tg += q.x;
+                *th += q.y;
+            }
+            const int f0 = u * qm.S;
+            const int ns = min(qm.S, qm.F - f0);
+            const uint32_t win = get_bits(qm.P, (long long)row * qm.stride + (long long)f0 * qm.bits, ns * qm.bits);
+            for (int jj = 0; jj < ns; ++jj) {
+                const int s = (int)((win >> (jj * qm.bits)) & mask);
+                if (s == qm.B) continue;  // missing: mass recovered as total - sum (R7)
+                hist_add<WIDE>(h.base, h.hstride, s_off[f0 + jj - f_lo] + s, q);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void load_group(const QM &qm, const Group &grp, const int32_t *__restrict__ cut_ptr,
+                                           int *s_off) {
+    const int f_lo = grp.u_lo * qm.S, f_hi = min(grp.u_hi * qm.S, qm.F);
+    for (int f = f_lo + threadIdx.x; f <= f_hi; f += blockDim.x) s_off[f - f_lo] = __ldg(cut_ptr + f) - grp.bin_lo;
+}
+
+__device__ __forceinline__ void block_totals(long long tg, long long th, long long *red, unsigned long long *out) {
+    for (int o = 16; o > 0; o >>= 1) {
+        tg += __shfl_xor_sync(0xffffffffu, tg, o);
+        th += __shfl_xor_sync(0xffffffffu, th, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[2 * w] = tg;
+        red[2 * w + 1] = th;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0, b = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            a += red[2 * i];
+            b += red[2 * i + 1];
+        }
+        atomicAdd(out + 0, (unsigned long long)a);
+        atomicAdd(out + 1, (unsigned long long)b);
+    }
+}
+
+// ============================================================== range histogram (root, entry)
+struct RangeArgs {
+    QM qm;
+    const int2 *qpair;
+    const uint32_t *ridx;        // null = identity rows
+    long long n_sel;             // rows
+    int chunk, n_groups;
+    const Group *groups;
+    const int32_t *cut_ptr;
+    unsigned long long *hist;    // [TB][2] (one slot)
+    unsigned long long *totals;  // [2] or null
+    unsigned long long *rows_ctr;
+    int hstride;
+};
+
+template <bool WIDE, bool BYTE, bool SENT>
+__global__ void __launch_bounds__(H_THREADS) hist_range_kernel(RangeArgs a) {
+    extern __shared__ int smem[];
+    __shared__ int s_off[2049];
+    __shared__ long long s_red[2 * H_THREADS / 32];
+    const QM &qm = a.qm;
+    const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int g = it % a.n_groups;
+        const long long start = (long long)(it / a.n_groups) * a.chunk;
+        const int len = (int)min((long long)a.chunk, a.n_sel - start);
+        const Group grp = a.groups[g];
+        SmemHist h{smem, grp.bin_hi - grp.bin_lo, a.hstride};
+        if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)len);
+        smem_zero<WIDE>(h);
+        load_group(qm, grp, a.cut_ptr, s_off);
+        __syncthreads();
+        ByteLane L = BYTE ? byte_lane(qm, grp, s_off, h.nb) : ByteLane{};
+        long long tg = 0, th = 0;
+        const bool tot = a.totals && g == 0;
+        if (a.ridx) {
+            const uint32_t *rp = a.ridx + start;
+            accumulate<WIDE, BYTE, SENT>(qm, grp, s_off, h, a.qpair, [&](int r) { return __ldg(rp + r); }, len, L,
+                                         &tg, &th, tot);
+        } else {
+            const uint32_t s0 = (uint32_t)start;
+            accumulate<WIDE, BYTE, SENT>(qm, grp, s_off, h, a.qpair, [&](int r) { return s0 + (uint32_t)r; }, len, L,
+                                         &tg, &th, tot);
+        }
+        if (tot) block_totals(tg, th, s_red, a.totals);
+        __syncthreads();
+        smem_flush<WIDE>(h, a.hist + 2ll * grp.bin_lo);
+        __syncthreads();
+    }
+}
+
+// ============================================================== partition helpers
 __device__ __forceinline__ int find_parent(const int *__restrict__ tile_base, int n_par, int t) {
     int lo = 0, hi = n_par - 1;  // largest j with tile_base[j] <= t
     while (lo < hi) {
@@ -72,62 +303,275 @@ __device__ __forceinline__ int find_parent(const int *__restrict__ tile_base, in
     return lo;
 }
 
-// mode 0: flags + tile_left (and row_leaf for leaf parents); mode 1: final level (row_leaf)
-template <bool FINAL>
-__global__ void __launch_bounds__(P_THREADS) part_count_kernel(
-    QM qm, const NodeDev *__restrict__ nodes, int first, int n_par, const int *__restrict__ tile_base,
-    const uint32_t *__restrict__ ridx_in, uint32_t *__restrict__ flags, int *__restrict__ tile_left,
-    int32_t *__restrict__ row_leaf) {
-    __shared__ int red[P_THREADS / 32];
-    const int n_tiles = tile_base[n_par];
+__device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint32_t row) {
+    const uint32_t sym = symbol_at(qm, row, nd.f);
+    return (int)sym == qm.B ? (nd.dl != 0) : ((int)sym <= nd.b);
+}
+
+// ============================================================== plan (1 block)
+// Tile plan of the parents of a level and the fused kernel's work items.  Split parents get
+// RUN-tile items for every feature group; leaf parents one group-0 item per run (row_leaf).
+__global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
+                                                    int n_groups, int *__restrict__ tile_base,
+                                                    TileItem *__restrict__ items, int *__restrict__ n_items) {
+    __shared__ long long sm32[32];
+    __shared__ int carry_t, carry_i;
+    if (threadIdx.x == 0) {
+        carry_t = 0;
+        carry_i = 0;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int j = find_parent(tile_base, n_par, t);
-        const int k = first + j;
-        const NodeDev nd = nodes[k];
-        const long long base = nd.start + (long long)(t - tile_base[j]) * PT;
-        const long long end = nd.start + nd.count;
-        int cnt = 0;
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const long long pos = base + wid * 128 + s * 32 + lane;
-            const bool valid = pos < end;
-            uint32_t row = 0;
-            if (valid) row = ridx_in ? __ldg(ridx_in + pos) : (uint32_t)pos;
-            if (nd.state == GBM_NODE_LEAF) {
-                if (valid) row_leaf[row] = k;
-                continue;
+    for (int c = 0; c < n_par; c += 1024) {
+        const int j = c + threadIdx.x;
+        int nt = 0, ni = 0;
+        if (j < n_par) {
+            const NodeDev nd = nodes[first + j];
+            if (nd.state != GBM_NODE_ABSENT && nd.count > 0) {
+                nt = (int)((nd.count + PT - 1) / PT);
+                ni = ((nt + RUN - 1) / RUN) * (nd.state == GBM_NODE_SPLIT ? n_groups : 1);
             }
-            bool left = false;
-            if (valid) {
-                uint32_t sym = symbol_at(qm, row, nd.f);
-                left = (int)sym == qm.B ? (nd.dl != 0) : ((int)sym <= nd.b);
-            }
-            if (FINAL) {
-                if (valid) row_leaf[row] = left ? 2 * k + 1 : 2 * k + 2;
-                continue;
-            }
-            uint32_t w = __ballot_sync(0xffffffffu, valid && left);
-            if (lane == 0) flags[(long long)t * (PT / 32) + wid * 4 + s] = w;
-            cnt += __popc(w);
         }
-        if (!FINAL) {
-            if (lane == 0) red[wid] = cnt;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int sum = 0;
-                for (int w = 0; w < P_THREADS / 32; ++w) sum += red[w];
-                tile_left[t] = sum;
-            }
-            __syncthreads();
+        // block exclusive scan of (nt, ni) packed in one 64-bit value
+        long long v = ((long long)nt << 32) | (unsigned)ni, x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
+        if (lane == 31) sm32[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            long long s = sm32[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                long long y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            sm32[lane] = s;
+        }
+        __syncthreads();
+        const long long ex = (wid ? sm32[wid - 1] : 0) + x - v;
+        const int tb = carry_t + (int)(ex >> 32), ib = carry_i + (int)(ex & 0xffffffff);
+        if (j < n_par) {
+            tile_base[j] = tb;
+            const NodeDev nd = nodes[first + j];
+            const int G = nd.state == GBM_NODE_SPLIT ? n_groups : 1;
+            for (int q = 0; q < ni; ++q) {
+                const int run = q / G, g = q - run * G;
+                TileItem it;
+                it.j = j;
+                it.group = g;
+                it.t0 = tb + run * RUN;
+                it.t1 = min(tb + nt, it.t0 + RUN);
+                items[ib + q] = it;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const long long tot = sm32[31];
+            carry_t += (int)(tot >> 32);
+            carry_i += (int)(tot & 0xffffffff);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        tile_base[n_par] = carry_t;
+        *n_items = carry_i;
     }
 }
 
-// Block-wide exclusive scan helper (1024 threads) over int values; returns exclusive prefix and
-// the chunk total through *total.
-__device__ __forceinline__ long long block_exscan_1024(long long v, long long *total, long long *sm32) {
+// ============================================================== fused partition + histogram
+struct FusedArgs {
+    QM qm;
+    const NodeDev *nodes;
+    int first, n_par;
+    const int *tile_base;
+    const TileItem *items;
+    const int *n_items;
+    const uint32_t *ridx_in;  // null = identity (level 1)
+    uint32_t *flags;          // [tiles][PT/32]
+    int *tile_left;           // [tiles]
+    int32_t *row_leaf;
+    const int2 *qpair;
+    const Group *groups;
+    const int32_t *cut_ptr;
+    unsigned long long *hist;  // [n_par][TB][2]
+    long long TB;
+    int hstride;
+    unsigned long long *rows_ctr;  // profiling: algorithmic BITS moved (see below)
+    int bits_parent_row;           // split symbol + ridx read, per scanned parent row
+    int bits_built_row;            // packed row + qpair, per row of the built child
+};
+
+// Warp-independent: each warp owns 64 rows of every tile of the item (no block barrier
+// inside an item).  Per 64-row batch: (A) split symbol of each row -> left flags (ballot), the
+// warp's left count into tile_left, the rows of the built child compacted into a warp-private
+// list; (B) the listed rows' words accumulated by the warp (lane -> fixed word of the row).
+template <bool WIDE, bool BYTE, bool SENT>
+__global__ void __launch_bounds__(H_THREADS) part_hist_kernel(FusedArgs a) {
+    extern __shared__ int smem[];
+    __shared__ int s_off[2049];
+    __shared__ uint32_t s_rows[H_THREADS / 32][64];
+    const QM &qm = a.qm;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n_items = *a.n_items;
+    uint32_t *wrows = s_rows[wid];
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const TileItem item = a.items[it];
+        const int k = a.first + item.j;
+        const NodeDev nd = a.nodes[k];
+        const long long seg_end = nd.start + nd.count;
+        if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
+            for (int t = item.t0; t < item.t1; ++t) {
+                const long long base = nd.start + (long long)(t - a.tile_base[item.j]) * PT;
+                for (int i = threadIdx.x; i < PT; i += H_THREADS) {
+                    const long long pos = base + i;
+                    if (pos < seg_end) a.row_leaf[a.ridx_in ? __ldg(a.ridx_in + pos) : (uint32_t)pos] = k;
+                }
+            }
+            continue;
+        }
+        const int g = item.group;
+        const Group grp = a.groups[g];
+        SmemHist h{smem, grp.bin_hi - grp.bin_lo, a.hstride};
+        smem_zero<WIDE>(h);
+        load_group(qm, grp, a.cut_ptr, s_off);
+        __syncthreads();
+        // lane -> (row slot, unit) of the group; units per row Ug <= 32 (plan_hist)
+        const int Ug = grp.u_hi - grp.u_lo;
+        const int rpp = 32 / Ug;                       // rows per pass
+        const int my_r = lane < rpp * Ug ? lane / Ug : -1;
+        const int my_u = grp.u_lo + (lane - (my_r < 0 ? 0 : my_r) * Ug);
+        const int f_lo = grp.u_lo * qm.S;
+        int off[4] = {h.nb, h.nb, h.nb, h.nb};
+        if (BYTE && my_r >= 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int f = my_u * 4 + j;
+                if (f < qm.F) off[j] = s_off[f - f_lo];
+            }
+        }
+        const bool build_left = nd.build_left != 0;
+        const long long sw = qm.stride >> 5;
+        const uint32_t mask = (1u << qm.bits) - 1u;
+        unsigned long long bits_acc = 0;
+        for (int t = item.t0; t < item.t1; ++t) {
+            const long long base = nd.start + (long long)(t - a.tile_base[item.j]) * PT + wid * 64;
+            // (A) partition flags for the warp's 64 rows
+            uint32_t row[2], bw[2];
+            int nleft = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const long long pos = base + s2 * 32 + lane;
+                const bool valid = pos < seg_end;
+                uint32_t r = 0;
+                bool left = false;
+                if (valid) {
+                    r = a.ridx_in ? __ldg(a.ridx_in + pos) : (uint32_t)pos;
+                    left = goes_left(qm, nd, r);
+                }
+                const uint32_t lw = __ballot_sync(0xffffffffu, valid && left);
+                bw[s2] = __ballot_sync(0xffffffffu, valid && (left == build_left));
+                if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 2 + s2] = lw;
+                nleft += __popc(lw);
+                row[s2] = r;
+            }
+            if (g == 0 && lane == 0) {
+                if (nleft) atomicAdd(a.tile_left + t, nleft);
+                if (a.rows_ctr) {
+                    const long long nv = max(0ll, min(64ll, seg_end - base));
+                    bits_acc += (unsigned long long)nv * a.bits_parent_row +
+                                (unsigned long long)(__popc(bw[0]) + __popc(bw[1])) * a.bits_built_row;
+                }
+            }
+            const uint32_t ltm = (1u << lane) - 1u;
+            const int n0 = __popc(bw[0]);
+            if ((bw[0] >> lane) & 1u) wrows[__popc(bw[0] & ltm)] = row[0];
+            if ((bw[1] >> lane) & 1u) wrows[n0 + __popc(bw[1] & ltm)] = row[1];
+            __syncwarp();
+            const int nbuild = n0 + __popc(bw[1]);
+            // (B) histogram of the listed rows
+            if (my_r >= 0) {
+                if (BYTE) {
+                    int rr = my_r;
+                    for (; rr + rpp < nbuild; rr += 2 * rpp) {
+                        const uint32_t ra = wrows[rr], rb = wrows[rr + rpp];
+                        const uint32_t wa = __ldg(qm.P + ra * sw + my_u), wb = __ldg(qm.P + rb * sw + my_u);
+                        const int2 qa = __ldg(a.qpair + ra), qb = __ldg(a.qpair + rb);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int sa = (wa >> (8 * j)) & 255, sb = (wb >> (8 * j)) & 255;
+                            if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[j] + sa, qa);
+                            if (!SENT || sb != qm.B) hist_add<WIDE>(h.base, h.hstride, off[j] + sb, qb);
+                        }
+                    }
+                    if (rr < nbuild) {
+                        const uint32_t ra = wrows[rr];
+                        const uint32_t wa = __ldg(qm.P + ra * sw + my_u);
+                        const int2 qa = __ldg(a.qpair + ra);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int sa = (wa >> (8 * j)) & 255;
+                            if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[j] + sa, qa);
+                        }
+                    }
+                } else {
+                    const int f0 = my_u * qm.S;
+                    const int ns = min(qm.S, qm.F - f0);
+                    for (int rr = my_r; rr < nbuild; rr += rpp) {
+                        const uint32_t ra = wrows[rr];
+                        const int2 q = __ldg(a.qpair + ra);
+                        const uint32_t win =
+                            get_bits(qm.P, (long long)ra * qm.stride + (long long)f0 * qm.bits, ns * qm.bits);
+                        for (int jj = 0; jj < ns; ++jj) {
+                            const int sy = (int)((win >> (jj * qm.bits)) & mask);
+                            if (sy == qm.B) continue;
+                            hist_add<WIDE>(h.base, h.hstride, s_off[f0 + jj - f_lo] + sy, q);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
+        __syncthreads();
+        smem_flush<WIDE>(h, a.hist + ((long long)item.j * a.TB + grp.bin_lo) * 2);
+        __syncthreads();
+    }
+}
+
+// Final level: every row's leaf by walking the tree on its packed symbols, in ROW order
+// (coalesced; no ridx, no gather).  Same decision rule as RepartitionInstances, so
+// row_leaf equals the partition the levels would have produced.
+constexpr int WALK_THREADS = 256;
+__global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const int8_t *__restrict__ kind,
+                                                                 const int32_t *__restrict__ feature,
+                                                                 const int32_t *__restrict__ bin,
+                                                                 const int8_t *__restrict__ dl, int n_internal,
+                                                                 long long n, int32_t *__restrict__ row_leaf) {
+    extern __shared__ int s_tree[];  // [n_internal] packed: feature | dl << 20 | split << 21, bin
+    int *s_f = s_tree, *s_b = s_tree + n_internal;
+    for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
+        s_f[k] = kind[k] == GBM_NODE_SPLIT ? (feature[k] | ((int)dl[k] << 20) | (1 << 21)) : 0;
+        s_b[k] = bin[k];
+    }
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)WALK_THREADS + threadIdx.x; i < n;
+         i += (long long)gridDim.x * WALK_THREADS) {
+        int k = 0;
+        while (k < n_internal) {
+            const int fk = s_f[k];
+            if (!(fk & (1 << 21))) break;
+            const uint32_t sym = symbol_at(qm, i, fk & 0xfffff);
+            const bool left = (int)sym == qm.B ? ((fk >> 20) & 1) : ((int)sym <= s_b[k]);
+            k = left ? 2 * k + 1 : 2 * k + 2;
+        }
+        row_leaf[i] = k;
+    }
+}
+
+// ============================================================== scan + scatter
+__device__ __forceinline__ long long block_exscan(long long v, long long *total, long long *sm32) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     long long x = v;
     for (int o = 1; o < 32; o <<= 1) {
         long long y = __shfl_up_sync(0xffffffffu, x, o);
@@ -136,7 +580,7 @@ __device__ __forceinline__ long long block_exscan_1024(long long v, long long *t
     if (lane == 31) sm32[wid] = x;
     __syncthreads();
     if (wid == 0) {
-        long long s = sm32[lane];
+        long long s = lane < nw ? sm32[lane] : 0;
         for (int o = 1; o < 32; o <<= 1) {
             long long y = __shfl_up_sync(0xffffffffu, s, o);
             if (lane >= o) s += y;
@@ -145,115 +589,60 @@ __device__ __forceinline__ long long block_exscan_1024(long long v, long long *t
     }
     __syncthreads();
     long long ex = (wid ? sm32[wid - 1] : 0) + x - v;
-    *total = sm32[31];
+    *total = sm32[nw - 1];
     __syncthreads();
     return ex;
 }
 
-// single block (1024 threads): children segments, hist items of the built children, next tiles
-__global__ void __launch_bounds__(1024) part_scan_kernel(
-    NodeDev *__restrict__ nodes, int first, int n_par, const int *__restrict__ tile_base,
-    const int *__restrict__ tile_left, int *__restrict__ tile_off, HistItem *__restrict__ items,
-    int *__restrict__ n_items, int n_groups, int chunk, int *__restrict__ next_tile_base,
-    int make_items) {
+// one block per parent: exclusive scan of its tiles' left counts; children segments
+__global__ void __launch_bounds__(1024) part_scan_kernel(NodeDev *__restrict__ nodes, int first,
+                                                         const int *__restrict__ tile_base,
+                                                         const int *__restrict__ tile_left, int *__restrict__ tile_off) {
     __shared__ long long sm32[32];
-    __shared__ long long item_base[1024];
-    // 1. per split parent: exclusive scan of its tiles' left counts -> tile_off, n_left
-    for (int j = 0; j < n_par; ++j) {
-        const int k = first + j;
-        NodeDev nd = nodes[k];
-        NodeDev *L = nodes + 2 * k + 1, *R = nodes + 2 * k + 2;
-        if (nd.state != GBM_NODE_SPLIT) {
-            if (threadIdx.x == 0) {
-                L->count = 0; L->start = 0; L->state = GBM_NODE_ABSENT;
-                R->count = 0; R->start = 0; R->state = GBM_NODE_ABSENT;
-            }
-            continue;
-        }
-        const int t0 = tile_base[j], t1 = tile_base[j + 1];
-        long long carry = 0;
-        for (int c = t0; c < t1; c += 1024) {
-            int t = c + threadIdx.x;
-            long long v = t < t1 ? tile_left[t] : 0;
-            long long tot;
-            long long ex = block_exscan_1024(v, &tot, sm32);
-            if (t < t1) tile_off[t] = (int)(carry + ex);
-            carry += tot;
-        }
+    const int j = blockIdx.x, k = first + j;
+    const NodeDev nd = nodes[k];
+    NodeDev *Lc = nodes + 2 * k + 1, *Rc = nodes + 2 * k + 2;
+    if (nd.state != GBM_NODE_SPLIT) {
         if (threadIdx.x == 0) {
-            L->start = nd.start; L->count = carry;
-            R->start = nd.start + carry; R->count = nd.count - carry;
+            Lc->count = 0; Lc->start = 0; Lc->state = GBM_NODE_ABSENT;
+            Rc->count = 0; Rc->start = 0; Rc->state = GBM_NODE_ABSENT;
         }
-        __syncthreads();
+        return;
     }
-    __syncthreads();
-    // 2. histogram work items of the built child of every split parent
-    if (make_items) {
-        const int nthr = 1024;
-        for (int c = 0; c < n_par; c += nthr) {
-            int j = c + threadIdx.x;
-            long long cntj = 0;
-            if (j < n_par) {
-                const int k = first + j;
-                if (nodes[k].state == GBM_NODE_SPLIT) {
-                    const NodeDev *ch = nodes + 2 * k + (nodes[k].build_left ? 1 : 2);
-                    cntj = ((ch->count + chunk - 1) / chunk) * n_groups;
-                }
-            }
-            item_base[threadIdx.x] = cntj;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                long long run = c == 0 ? 0 : (long long)*n_items;
-                for (int i = 0; i < nthr; ++i) {
-                    long long x = item_base[i];
-                    item_base[i] = run;
-                    run += x;
-                }
-                *n_items = (int)run;
-            }
-            __syncthreads();
-            if (j < n_par && cntj) {
-                const int k = first + j;
-                const NodeDev *ch = nodes + 2 * k + (nodes[k].build_left ? 1 : 2);
-                long long b = item_base[threadIdx.x];
-                for (long long q = 0; q < cntj; ++q) {
-                    long long chk = q / n_groups;
-                    int g = (int)(q - chk * n_groups);
-                    HistItem it;
-                    it.slot = j;
-                    it.group = g;
-                    it.start = ch->start + chk * chunk;
-                    it.len = (int)min((long long)chunk, ch->count - chk * chunk);
-                    it.pad = 0;
-                    items[b + q] = it;
-                }
-            }
-            __syncthreads();
+    const int t0 = nd.count > 0 ? tile_base[j] : 0, t1 = nd.count > 0 ? tile_base[j + 1] : 0;
+    constexpr int PER = 16;  // consecutive tiles per thread
+    long long carry = 0;
+    for (int c = t0; c < t1; c += 1024 * PER) {
+        const int tb = c + threadIdx.x * PER;
+        int v[PER];
+        long long loc = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            v[i] = tb + i < t1 ? tile_left[tb + i] : 0;
+            loc += v[i];
         }
-        if (n_par == 0 && threadIdx.x == 0) *n_items = 0;
+        long long tot;
+        long long ex = carry + block_exscan(loc, &tot, sm32);
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if (tb + i < t1) {
+                tile_off[tb + i] = (int)ex;
+                ex += v[i];
+            }
+        carry += tot;
     }
-    __syncthreads();
-    // 3. tile plan of the children (the next level's parents), in heap order
-    {
-        const int n_ch = 2 * n_par, cfirst = 2 * first + 1;
-        long long carry = 0;
-        for (int c = 0; c < n_ch; c += 1024) {
-            int j = c + threadIdx.x;
-            long long v = 0;
-            if (j < n_ch) v = (nodes[cfirst + j].count + PT - 1) / PT;
-            long long tot;
-            long long ex = block_exscan_1024(v, &tot, sm32);
-            if (j < n_ch) next_tile_base[j] = (int)(carry + ex);
-            carry += tot;
-        }
-        if (threadIdx.x == 0) next_tile_base[n_ch] = (int)carry;
+    if (threadIdx.x == 0) {
+        Lc->start = nd.start;
+        Lc->count = carry;
+        Rc->start = nd.start + carry;
+        Rc->count = nd.count - carry;
     }
 }
 
 __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
     const NodeDev *__restrict__ nodes, int first, int n_par, const int *__restrict__ tile_base,
-    const uint32_t *__restrict__ flags, const int *__restrict__ tile_off,
-    const uint32_t *__restrict__ ridx_in, uint32_t *__restrict__ ridx_out) {
+    const uint32_t *__restrict__ flags, const int *__restrict__ tile_off, const uint32_t *__restrict__ ridx_in,
+    uint32_t *__restrict__ ridx_out, unsigned long long *__restrict__ rows_ctr) {
     __shared__ int wpre[PT / 32];
     const int n_tiles = tile_base[n_par];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -264,18 +653,20 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
         if (nd.state != GBM_NODE_SPLIT) continue;  // uniform per block
         const long long n_left = nodes[2 * k + 1].count;
         const int lt = t - tile_base[j];
+        if (rows_ctr && threadIdx.x == 0)
+            atomicAdd(rows_ctr, (unsigned long long)min((long long)PT, nd.count - (long long)lt * PT));
         uint32_t w[4];
 #pragma unroll
         for (int s = 0; s < 4; ++s) w[s] = __ldg(flags + (long long)t * (PT / 32) + wid * 4 + s);
-        if (lane < 4) wpre[wid * 4 + lane] = __popc(w[lane]);
+        if (lane < 4) wpre[wid * 4 + lane] = __popc(lane == 0 ? w[0] : lane == 1 ? w[1] : lane == 2 ? w[2] : w[3]);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int i = 0; i < PT / 32; ++i) {
-                int x = wpre[i];
-                wpre[i] = run;
-                run += x;
+        if (threadIdx.x < 32) {
+            int v = wpre[threadIdx.x], x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
             }
+            wpre[threadIdx.x] = x - v;
         }
         __syncthreads();
         const long long off = tile_off[t];
@@ -289,162 +680,23 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
             const uint32_t row = ridx_in ? __ldg(ridx_in + pos) : (uint32_t)pos;
             const long long lb = off + wpre[wid * 4 + s] + __popc(w[s] & ltm);  // lefts before
             const bool left = (w[s] >> lane) & 1u;
-            const long long dst = left ? nd.start + lb : nd.start + n_left + (pin - lb);
-            ridx_out[dst] = row;
-        }
-        __syncthreads();
-    }
-}
-
-// ============================================================== histograms
-struct HistArgs {
-    QM qm;
-    const int2 *qpair;
-    const uint32_t *ridx;        // null = identity rows
-    const HistItem *items;       // null = arithmetic items over [0, n_sel)
-    const int *n_items_dev;
-    long long n_sel;             // arithmetic mode: rows
-    int chunk, n_groups;
-    const Group *groups;
-    const int32_t *cut_ptr;
-    long long *hist;             // [slots][TB][2]
-    long long *totals;           // arithmetic mode: root totals [2] (may be null)
-    int TB;
-};
-
-template <bool WIDE>
-__global__ void __launch_bounds__(H_THREADS) hist_kernel(HistArgs a) {
-    extern __shared__ int smem[];
-    __shared__ int s_off[2049];     // bin offset (relative to the group) per feature of the group
-    __shared__ long long s_red[2][H_THREADS / 32];
-    const QM &qm = a.qm;
-    const int n_items = a.items ? *a.n_items_dev
-                                : (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
-    const uint32_t mask = qm.bits == 32 ? 0xffffffffu : ((1u << qm.bits) - 1u);
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        int slot, g, len;
-        long long start;
-        if (a.items) {
-            HistItem hi = a.items[it];
-            slot = hi.slot; g = hi.group; start = hi.start; len = hi.len;
-        } else {
-            slot = 0;
-            g = it % a.n_groups;
-            long long ch = it / a.n_groups;
-            start = ch * a.chunk;
-            len = (int)min((long long)a.chunk, a.n_sel - start);
-        }
-        const Group grp = a.groups[g];
-        const int nb = grp.bin_hi - grp.bin_lo;
-        const int f_lo = grp.u_lo * qm.S;
-        const int f_hi = min(grp.u_hi * qm.S, qm.F);
-        int *sg0 = smem, *sh0 = smem + nb;               // narrow: g, h  | wide: g_lo, h_lo
-        int *sg1 = smem + 2 * nb, *sh1 = smem + 3 * nb;  // wide: g_hi, h_hi
-        for (int i = threadIdx.x; i < (WIDE ? 4 : 2) * nb; i += H_THREADS) smem[i] = 0;
-        for (int f = f_lo + threadIdx.x; f <= f_hi; f += H_THREADS)
-            s_off[f - f_lo] = __ldg(a.cut_ptr + f) - grp.bin_lo;
-        __syncthreads();
-        const int Ug = grp.u_hi - grp.u_lo;
-        const uint32_t magic = 0xffffffffu / (uint32_t)Ug + 1u;
-        const uint32_t total = (uint32_t)len * (uint32_t)Ug;
-        long long tg = 0, th = 0;
-        for (uint32_t j = threadIdx.x; j < total; j += H_THREADS) {
-            const uint32_t r = Ug == 1 ? j : fast_div(j, magic);
-            const int u = grp.u_lo + (int)(j - r * (uint32_t)Ug);
-            const long long pos = start + r;
-            const uint32_t row = a.ridx ? __ldg(a.ridx + pos) : (uint32_t)pos;
-            const int2 q = __ldg(a.qpair + row);
-            if (a.totals && u == grp.u_lo) {
-                tg += q.x;
-                th += q.y;
-            }
-            const int f0 = u * qm.S;
-            const int ns = min(qm.S, qm.F - f0);
-            const uint32_t win = get_bits(qm.P, (long long)row * qm.stride + (long long)f0 * qm.bits,
-                                          ns * qm.bits);
-#pragma unroll 4
-            for (int jj = 0; jj < ns; ++jj) {
-                const int s = (int)((win >> (jj * qm.bits)) & mask);
-                if (s == qm.B) continue;  // missing: mass recovered as total - sum (R7)
-                const int bin = s_off[f0 + jj - f_lo] + s;
-                if (WIDE) {
-                    atomicAdd(sg0 + bin, q.x & 0x7fff);
-                    atomicAdd(sg1 + bin, q.x >> 15);
-                    atomicAdd(sh0 + bin, q.y & 0x7fff);
-                    atomicAdd(sh1 + bin, q.y >> 15);
-                } else {
-                    atomicAdd(sg0 + bin, q.x);
-                    atomicAdd(sh0 + bin, q.y);
-                }
-            }
-        }
-        if (a.totals && g == 0) {
-            for (int o = 16; o > 0; o >>= 1) {
-                tg += __shfl_xor_sync(0xffffffffu, tg, o);
-                th += __shfl_xor_sync(0xffffffffu, th, o);
-            }
-            if ((threadIdx.x & 31) == 0) {
-                s_red[0][threadIdx.x >> 5] = tg;
-                s_red[1][threadIdx.x >> 5] = th;
-            }
-        }
-        __syncthreads();
-        if (a.totals && g == 0 && threadIdx.x == 0) {
-            long long sgt = 0, sht = 0;
-            for (int w = 0; w < H_THREADS / 32; ++w) {
-                sgt += s_red[0][w];
-                sht += s_red[1][w];
-            }
-            atomicAdd((unsigned long long *)a.totals + 0, (unsigned long long)sgt);
-            atomicAdd((unsigned long long *)a.totals + 1, (unsigned long long)sht);
-        }
-        // flush into the int64 global histogram of this slot
-        unsigned long long *dst = (unsigned long long *)a.hist + ((long long)slot * a.TB + grp.bin_lo) * 2;
-        for (int b = threadIdx.x; b < nb; b += H_THREADS) {
-            long long G, H;
-            if (WIDE) {
-                G = (long long)sg1[b] * 32768 + (long long)(unsigned)sg0[b];
-                H = (long long)sh1[b] * 32768 + (long long)(unsigned)sh0[b];
-            } else {
-                G = sg0[b];
-                H = sh0[b];
-            }
-            if (G) atomicAdd(dst + 2 * b, (unsigned long long)G);
-            if (H) atomicAdd(dst + 2 * b + 1, (unsigned long long)H);
+            ridx_out[left ? nd.start + lb : nd.start + n_left + (pin - lb)] = row;
         }
         __syncthreads();
     }
 }
 
 // ============================================================== split evaluation
-struct Best {
-    double gain;
-    long long idx;  // canonical candidate order: (global bin)*2 + (dl ? 0 : 1); LLONG_MAX = none
-    long long Lg, Lh;
-};
-
-__device__ __forceinline__ bool better(const Best &a, const Best &b) {
-    if (a.idx == LLONG_MAX) return false;
-    if (b.idx == LLONG_MAX) return true;
-    return a.gain > b.gain || (a.gain == b.gain && a.idx < b.idx);
+__device__ __forceinline__ bool better(double ga, long long ia, double gb, long long ib) {
+    if (ia == LLONG_MAX) return false;
+    if (ib == LLONG_MAX) return true;
+    return ga > gb || (ga == gb && ia < ib);
 }
 
-__device__ __forceinline__ Best shfl_best(const Best &b, int o) {
-    Best r;
-    r.gain = __shfl_xor_sync(0xffffffffu, b.gain, o);
-    r.idx = __shfl_xor_sync(0xffffffffu, b.idx, o);
-    r.Lg = __shfl_xor_sync(0xffffffffu, b.Lg, o);
-    r.Lh = __shfl_xor_sync(0xffffffffu, b.Lh, o);
-    return r;
-}
-
-// Histogram source of one node: direct (hist), or sibling = parent - build.  Optionally stores
-// the node's histogram (for the next level's subtraction).
+// Histogram source of one node: direct, or sibling = parent - build.  Optionally stored.
 struct NodeHist {
-    const long long *direct;  // [TB][2] or null
-    const long long *parent;  // [TB][2]
-    const long long *build;   // [TB][2]
-    long long *store;         // [TB][2] or null
+    const long long *direct, *parent, *build;
+    long long *store;
     __device__ __forceinline__ void get(int bin, long long &g, long long &h) const {
         if (direct) {
             g = __ldg(direct + 2 * bin);
@@ -456,96 +708,153 @@ struct NodeHist {
     }
 };
 
-// Evaluate one node with the whole block (E_THREADS).  Returns (in *out, valid on thread 0) the
-// best candidate.  Op order of every fp64 step = R8 (oracle_evaluate_split).
-__device__ void evaluate_node(const NodeHist &src, int F, const int32_t *__restrict__ cut_ptr,
-                              long long Tg, long long Th, int sg, int sh, const EvalParams &p,
-                              Best *out) {
-    __shared__ Best s_best[E_THREADS / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
-    const double e = ddiv(dmul(G, G), dadd(H, p.lambda));
-    Best best;
+// Best candidate of feature f of one node, computed by one warp (valid in every lane).
+// Op order of every fp64 step = R8 (oracle_evaluate_split).
+__device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long Tg, long long Th, int sg, int sh,
+                                 double e, const EvalParams &p) {
+    const int lane = threadIdx.x & 31;
+    long long sgs = 0, shs = 0;
+    for (int b = lane; b < nbf; b += 32) {
+        long long g, h;
+        src.get(b0 + b, g, h);
+        if (src.store) {
+            src.store[2 * (b0 + b)] = g;
+            src.store[2 * (b0 + b) + 1] = h;
+        }
+        sgs += g;
+        shs += h;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sgs += __shfl_xor_sync(0xffffffffu, sgs, o);
+        shs += __shfl_xor_sync(0xffffffffu, shs, o);
+    }
+    const long long Mg = Tg - sgs, Mh = Th - shs;  // missing mass (R7)
+    FeatBest best;
     best.gain = 0.0;
     best.idx = LLONG_MAX;
     best.Lg = best.Lh = 0;
-    for (int f = wid; f < F; f += E_THREADS / 32) {
-        const int b0 = __ldg(cut_ptr + f), nbf = __ldg(cut_ptr + f + 1) - b0;
-        // pass 1: feature sums (missing mass) and the optional store of the node histogram
-        long long sgs = 0, shs = 0;
-        for (int b = lane; b < nbf; b += 32) {
-            long long g, h;
-            src.get(b0 + b, g, h);
-            if (src.store) {
-                src.store[2 * (b0 + b)] = g;
-                src.store[2 * (b0 + b) + 1] = h;
+    long long cg = 0, ch = 0;
+    for (int c = 0; c < nbf; c += 32) {
+        const int b = c + lane;
+        long long g = 0, h = 0;
+        if (b < nbf) src.get(b0 + b, g, h);
+        long long pg = g, ph = h;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long yg = __shfl_up_sync(0xffffffffu, pg, o), yh = __shfl_up_sync(0xffffffffu, ph, o);
+            if (lane >= o) {
+                pg += yg;
+                ph += yh;
             }
-            sgs += g;
-            shs += h;
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            sgs += __shfl_xor_sync(0xffffffffu, sgs, o);
-            shs += __shfl_xor_sync(0xffffffffu, shs, o);
-        }
-        const long long Mg = Tg - sgs, Mh = Th - shs;
-        // pass 2: prefix scan in chunks of 32 bins, both default directions
-        long long cg = 0, ch = 0;  // carry: prefix of earlier chunks
-        for (int c = 0; c < nbf; c += 32) {
-            const int b = c + lane;
-            long long g = 0, h = 0;
-            if (b < nbf) src.get(b0 + b, g, h);
-            long long pg = g, ph = h;
-            for (int o = 1; o < 32; o <<= 1) {
-                long long yg = __shfl_up_sync(0xffffffffu, pg, o);
-                long long yh = __shfl_up_sync(0xffffffffu, ph, o);
-                if (lane >= o) {
-                    pg += yg;
-                    ph += yh;
-                }
-            }
-            const long long Pg = cg + pg, Ph = ch + ph;
-            cg += __shfl_sync(0xffffffffu, pg, 31);
-            ch += __shfl_sync(0xffffffffu, ph, 31);
-            if (b < nbf) {
+        const long long Pg = cg + pg, Ph = ch + ph;
+        cg += __shfl_sync(0xffffffffu, pg, 31);
+        ch += __shfl_sync(0xffffffffu, ph, 31);
+        if (b < nbf) {
 #pragma unroll
-                for (int dli = 0; dli < 2; ++dli) {
-                    const bool dl = dli == 0;  // true first (R9)
-                    const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
-                    const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
-                    const double GR = fixed_to_double(Tg - Lg, sg), HR = fixed_to_double(Th - Lh, sh);
-                    if (!(HL >= p.mcw && HR >= p.mcw && dadd(HL, p.lambda) > 0.0 &&
-                          dadd(HR, p.lambda) > 0.0))
-                        continue;
-                    double a = dmul(GL, GL);
-                    a = ddiv(a, dadd(HL, p.lambda));
-                    double cc = dmul(GR, GR);
-                    cc = ddiv(cc, dadd(HR, p.lambda));
-                    double d = dadd(a, cc);
-                    d = dsub(d, e);
-                    d = dmul(0.5, d);
-                    Best cand;
-                    cand.gain = dsub(d, p.gamma);
-                    cand.idx = (long long)(b0 + b) * 2 + dli;
-                    cand.Lg = Lg;
-                    cand.Lh = Lh;
-                    if (better(cand, best)) best = cand;
+            for (int dli = 0; dli < 2; ++dli) {
+                const bool dl = dli == 0;  // true first (R9)
+                const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
+                const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
+                const double GR = fixed_to_double(Tg - Lg, sg), HR = fixed_to_double(Th - Lh, sh);
+                if (!(HL >= p.mcw && HR >= p.mcw && dadd(HL, p.lambda) > 0.0 && dadd(HR, p.lambda) > 0.0)) continue;
+                double aa = dmul(GL, GL);
+                aa = ddiv(aa, dadd(HL, p.lambda));
+                double cc = dmul(GR, GR);
+                cc = ddiv(cc, dadd(HR, p.lambda));
+                double d = dadd(aa, cc);
+                d = dsub(d, e);
+                d = dmul(0.5, d);
+                const double gain = dsub(d, p.gamma);
+                const long long idx = (long long)(b0 + b) * 2 + dli;
+                if (better(gain, idx, best.gain, best.idx)) {
+                    best.gain = gain;
+                    best.idx = idx;
+                    best.Lg = Lg;
+                    best.Lh = Lh;
                 }
             }
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
-        Best other = shfl_best(best, o);
-        if (better(other, best)) best = other;
+        const double og = __shfl_xor_sync(0xffffffffu, best.gain, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, best.idx, o);
+        const long long olg = __shfl_xor_sync(0xffffffffu, best.Lg, o), olh = __shfl_xor_sync(0xffffffffu, best.Lh, o);
+        if (better(og, oi, best.gain, best.idx)) {
+            best.gain = og;
+            best.idx = oi;
+            best.Lg = olg;
+            best.Lh = olh;
+        }
     }
-    if (lane == 0) s_best[wid] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        Best b = s_best[0];
-        for (int w = 1; w < E_THREADS / 32; ++w)
-            if (better(s_best[w], b)) b = s_best[w];
-        *out = b;
+    return best;
+}
+
+struct EvalArgs {
+    int level, first, F, n_nodes;
+    long long TB;
+    const int32_t *cut_ptr;
+    const float *cut_values;
+    const int32_t *scale;
+    EvalParams p;
+    NodeDev *nodes;                 // tree mode
+    const long long *hist_root;     // tree mode: root hist + totals
+    const long long *hist_build;    // tree mode: built children, per parent slot
+    const long long *hist_prev;     // tree mode: parent level hists
+    long long *hist_store;          // tree mode: this level's hists (or null)
+    const long long *hist_direct;   // direct mode: [n_nodes][TB][2]
+    const long long *totals_direct; // direct mode: [n_nodes][2]
+    FeatBest *fb;                   // [n_nodes][F]
+};
+
+// Node j's histogram source and totals; false if the node does not exist.
+__device__ __forceinline__ bool node_source(const EvalArgs &a, int j, NodeHist &src, long long &Tg, long long &Th) {
+    src.direct = src.parent = src.build = nullptr;
+    src.store = nullptr;
+    if (a.hist_direct) {
+        src.direct = a.hist_direct + (long long)j * a.TB * 2;
+        Tg = a.totals_direct[2 * j];
+        Th = a.totals_direct[2 * j + 1];
+        return true;
     }
-    __syncthreads();
+    const int k = a.first + j;
+    if (a.level == 0) {
+        src.direct = a.hist_root;
+        Tg = a.hist_root[2 * a.TB];
+        Th = a.hist_root[2 * a.TB + 1];
+    } else {
+        const int pk = (k - 1) / 2;
+        const int pslot = pk - ((1 << (a.level - 1)) - 1);
+        if (a.nodes[pk].state != GBM_NODE_SPLIT) return false;
+        Tg = a.nodes[k].Tg;
+        Th = a.nodes[k].Th;
+        const bool is_left = (k & 1) == 1;
+        const bool built = a.nodes[pk].build_left ? is_left : !is_left;
+        const long long *bh = a.hist_build + (long long)pslot * a.TB * 2;
+        if (built) {
+            src.direct = bh;
+        } else {
+            src.parent = a.level == 1 ? a.hist_root : a.hist_prev + (long long)pslot * a.TB * 2;
+            src.build = bh;
+        }
+    }
+    if (a.hist_store) src.store = a.hist_store + (long long)j * a.TB * 2;
+    return true;
+}
+
+// one warp per (node, feature)
+__global__ void __launch_bounds__(E_THREADS) eval_feat_kernel(EvalArgs a) {
+    const long long gw = ((long long)blockIdx.x * E_THREADS + threadIdx.x) >> 5;
+    if (gw >= (long long)a.n_nodes * a.F) return;
+    const int j = (int)(gw / a.F), f = (int)(gw - (long long)j * a.F);
+    NodeHist src;
+    long long Tg, Th;
+    if (!node_source(a, j, src, Tg, Th)) return;
+    const int sg = a.scale[0], sh = a.scale[1];
+    const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
+    const double e = ddiv(dmul(G, G), dadd(H, a.p.lambda));
+    const int b0 = __ldg(a.cut_ptr + f), nbf = __ldg(a.cut_ptr + f + 1) - b0;
+    const FeatBest b = eval_feature(src, b0, nbf, Tg, Th, sg, sh, e, a.p);
+    if ((threadIdx.x & 31) == 0) a.fb[gw] = b;
 }
 
 __device__ __forceinline__ double leaf_weight(long long Tg, long long Th, int sg, int sh, double lambda, double eta) {
@@ -574,151 +883,138 @@ __device__ __forceinline__ void write_leaf(const TreeDev &t, int k, long long Tg
     t.weight[k] = leaf_weight(Tg, Th, sg, sh, p.lambda, p.eta);
 }
 
-// Evaluate every node of level l (heap ids first .. first + 2^l - 1).  One block per node.
-//   level 0: hist = root buffer (totals at hist_root[2*TB]).
-//   level l > 0: node k, parent pk; absent if the parent did not split; otherwise the built
-//   child's histogram is hist_build[parent slot], the sibling's = hist_prev[slot] - build.
-__global__ void __launch_bounds__(E_THREADS) eval_level_kernel(
-    int level, int first, int F, int TB, const int32_t *__restrict__ cut_ptr,
-    const float *__restrict__ cut_values, const int32_t *__restrict__ scale, EvalParams p,
-    NodeDev *__restrict__ nodes, const long long *__restrict__ hist_root,
-    const long long *__restrict__ hist_build, const long long *__restrict__ hist_prev,
-    long long *__restrict__ hist_store, TreeDev t) {
-    __shared__ Best s_out;
-    const int j = blockIdx.x;
-    const int k = first + j;
-    const int sg = scale[0], sh = scale[1];
-    NodeHist src;
-    src.direct = nullptr;
-    src.parent = src.build = nullptr;
-    src.store = nullptr;
-    long long Tg, Th;
-    if (level == 0) {
-        Tg = hist_root[2 * (long long)TB];
-        Th = hist_root[2 * (long long)TB + 1];
-        src.direct = hist_root;
-        if (threadIdx.x == 0) {
-            nodes[0].Tg = Tg;
-            nodes[0].Th = Th;
-        }
-    } else {
-        const int pk = (k - 1) / 2;
-        const int pslot = pk - ((1 << (level - 1)) - 1);
-        if (nodes[pk].state != GBM_NODE_SPLIT) {
-            if (threadIdx.x == 0) nodes[k].state = GBM_NODE_ABSENT;
-            return;
-        }
-        Tg = nodes[k].Tg;
-        Th = nodes[k].Th;
-        const bool is_left = (k & 1) == 1;
-        const bool built = nodes[pk].build_left ? is_left : !is_left;
-        const long long *bh = hist_build + (long long)pslot * TB * 2;
-        if (built) {
-            src.direct = bh;
-        } else {
-            src.parent = (level == 1 ? hist_root : hist_prev + (long long)pslot * TB * 2);
-            src.build = bh;
+__device__ __forceinline__ int feature_of_bin(const int32_t *__restrict__ cut_ptr, int F, int gbin) {
+    int lo = 0, hi = F - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(cut_ptr + mid) <= gbin) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// block-wide canonical argmax over the features of node j
+__device__ FeatBest reduce_node(const EvalArgs &a, int j) {
+    __shared__ double s_g[E_THREADS / 32];
+    __shared__ long long s_i[E_THREADS / 32], s_lg[E_THREADS / 32], s_lh[E_THREADS / 32];
+    double bg = 0.0;
+    long long bi = LLONG_MAX, blg = 0, blh = 0;
+    for (int f = threadIdx.x; f < a.F; f += E_THREADS) {
+        const FeatBest c = a.fb[(long long)j * a.F + f];
+        if (better(c.gain, c.idx, bg, bi)) {
+            bg = c.gain; bi = c.idx; blg = c.Lg; blh = c.Lh;
         }
     }
-    if (hist_store && level < p.max_depth - 1) src.store = hist_store + (long long)j * TB * 2;
-    if (level >= p.max_depth) {  // (max_depth == 0) the root is a leaf
+    for (int o = 16; o > 0; o >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const long long olg = __shfl_xor_sync(0xffffffffu, blg, o), olh = __shfl_xor_sync(0xffffffffu, blh, o);
+        if (better(og, oi, bg, bi)) {
+            bg = og; bi = oi; blg = olg; blh = olh;
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_g[w] = bg; s_i[w] = bi; s_lg[w] = blg; s_lh[w] = blh;
+    }
+    __syncthreads();
+    FeatBest r;
+    r.gain = s_g[0]; r.idx = s_i[0]; r.Lg = s_lg[0]; r.Lh = s_lh[0];
+    for (int i = 1; i < E_THREADS / 32; ++i)
+        if (better(s_g[i], s_i[i], r.gain, r.idx)) {
+            r.gain = s_g[i]; r.idx = s_i[i]; r.Lg = s_lg[i]; r.Lh = s_lh[i];
+        }
+    return r;
+}
+
+// tree mode: one block per node of the level
+__global__ void __launch_bounds__(E_THREADS) eval_final_kernel(EvalArgs a, TreeDev t) {
+    const int j = blockIdx.x, k = a.first + j;
+    NodeHist src;
+    long long Tg, Th;
+    const bool exists = node_source(a, j, src, Tg, Th);
+    if (!exists) {
+        if (threadIdx.x == 0) a.nodes[k].state = GBM_NODE_ABSENT;
+        return;
+    }
+    const int sg = a.scale[0], sh = a.scale[1];
+    const EvalParams &p = a.p;
+    if (a.level >= p.max_depth) {  // max_depth == 0: the root is a leaf
         if (threadIdx.x == 0) {
             write_leaf(t, k, Tg, Th, sg, sh, p);
-            nodes[k].state = GBM_NODE_LEAF;
+            a.nodes[k].state = GBM_NODE_LEAF;
+            a.nodes[k].Tg = Tg;
+            a.nodes[k].Th = Th;
         }
         return;
     }
-    evaluate_node(src, F, cut_ptr, Tg, Th, sg, sh, p, &s_out);
-    if (threadIdx.x == 0) {
-        Best b = s_out;
-        const bool split = b.idx != LLONG_MAX && b.gain > 0.0;
-        t.sum_qg[k] = Tg;
-        t.sum_qh[k] = Th;
-        t.weight[k] = leaf_weight(Tg, Th, sg, sh, p.lambda, p.eta);
-        if (!split) {
-            t.kind[k] = GBM_NODE_LEAF;
-            nodes[k].state = GBM_NODE_LEAF;
-        } else {
-            const int gbin = (int)(b.idx >> 1), dl = (b.idx & 1) == 0;
-            int f = 0;  // feature owning global bin gbin
-            {
-                int lo = 0, hi = F - 1;
-                while (lo < hi) {
-                    int mid = (lo + hi + 1) >> 1;
-                    if (__ldg(cut_ptr + mid) <= gbin) lo = mid;
-                    else hi = mid - 1;
-                }
-                f = lo;
-            }
-            const int bb = gbin - __ldg(cut_ptr + f);
-            t.kind[k] = GBM_NODE_SPLIT;
-            t.feature[k] = f;
-            t.bin[k] = bb;
-            t.threshold[k] = __ldg(cut_values + gbin);
-            t.default_left[k] = (int8_t)dl;
-            t.gain[k] = b.gain;
-            NodeDev &nd = nodes[k];
-            nd.state = GBM_NODE_SPLIT;
-            nd.f = f;
-            nd.b = bb;
-            nd.dl = dl;
-            const long long Lg = b.Lg, Lh = b.Lh, Rg = Tg - b.Lg, Rh = Th - b.Lh;
-            nd.build_left = Lh <= Rh;  // smaller hessian sum; ties -> left (R17)
-            nodes[2 * k + 1].Tg = Lg;
-            nodes[2 * k + 1].Th = Lh;
-            nodes[2 * k + 2].Tg = Rg;
-            nodes[2 * k + 2].Th = Rh;
-            if (level + 1 == p.max_depth) {  // children at depth D are leaves
-                write_leaf(t, 2 * k + 1, Lg, Lh, sg, sh, p);
-                write_leaf(t, 2 * k + 2, Rg, Rh, sg, sh, p);
-            }
-        }
+    const FeatBest b = reduce_node(a, j);
+    if (threadIdx.x != 0) return;
+    NodeDev &nd = a.nodes[k];
+    nd.Tg = Tg;
+    nd.Th = Th;
+    const bool split = b.idx != LLONG_MAX && b.gain > 0.0;
+    t.sum_qg[k] = Tg;
+    t.sum_qh[k] = Th;
+    t.weight[k] = leaf_weight(Tg, Th, sg, sh, p.lambda, p.eta);
+    if (!split) {
+        t.kind[k] = GBM_NODE_LEAF;
+        nd.state = GBM_NODE_LEAF;
+        return;
+    }
+    const int gbin = (int)(b.idx >> 1), dl = (b.idx & 1) == 0;
+    const int f = feature_of_bin(a.cut_ptr, a.F, gbin);
+    const int bb = gbin - __ldg(a.cut_ptr + f);
+    t.kind[k] = GBM_NODE_SPLIT;
+    t.feature[k] = f;
+    t.bin[k] = bb;
+    t.threshold[k] = __ldg(a.cut_values + gbin);
+    t.default_left[k] = (int8_t)dl;
+    t.gain[k] = b.gain;
+    nd.state = GBM_NODE_SPLIT;
+    nd.f = f;
+    nd.b = bb;
+    nd.dl = dl;
+    const long long Lg = b.Lg, Lh = b.Lh, Rg = Tg - b.Lg, Rh = Th - b.Lh;
+    nd.build_left = Lh <= Rh;  // smaller hessian sum; ties -> left (R17)
+    a.nodes[2 * k + 1].Tg = Lg;
+    a.nodes[2 * k + 1].Th = Lh;
+    a.nodes[2 * k + 2].Tg = Rg;
+    a.nodes[2 * k + 2].Th = Rh;
+    if (a.level + 1 == p.max_depth) {  // children at depth D are leaves
+        write_leaf(t, 2 * k + 1, Lg, Lh, sg, sh, p);
+        write_leaf(t, 2 * k + 2, Rg, Rh, sg, sh, p);
     }
 }
 
-// standalone EvaluateSplit over n_nodes given histograms (gbm_evaluate_splits)
-__global__ void __launch_bounds__(E_THREADS) eval_many_kernel(
-    int F, int TB, const int32_t *__restrict__ cut_ptr, const int32_t *__restrict__ scale, EvalParams p,
-    const long long *__restrict__ hist, const long long *__restrict__ totals, int8_t *split_d,
-    int32_t *feature_d, int32_t *bin_d, int8_t *dl_d, double *gain_d, long long *child_d) {
-    __shared__ Best s_out;
+// direct mode (gbm_evaluate_splits)
+__global__ void __launch_bounds__(E_THREADS) eval_out_kernel(EvalArgs a, int8_t *split_d, int32_t *feature_d,
+                                                             int32_t *bin_d, int8_t *dl_d, double *gain_d,
+                                                             long long *child_d) {
     const int j = blockIdx.x;
-    NodeHist src;
-    src.direct = hist + (long long)j * TB * 2;
-    src.parent = src.build = nullptr;
-    src.store = nullptr;
-    const long long Tg = totals[2 * j], Th = totals[2 * j + 1];
-    evaluate_node(src, F, cut_ptr, Tg, Th, scale[0], scale[1], p, &s_out);
-    if (threadIdx.x == 0) {
-        Best b = s_out;
-        const bool found = b.idx != LLONG_MAX;
-        split_d[j] = found && b.gain > 0.0;
-        gain_d[j] = found ? b.gain : 0.0;
-        int f = -1, bb = -1, dl = 0;
-        if (found) {
-            const int gbin = (int)(b.idx >> 1);
-            dl = (b.idx & 1) == 0;
-            int lo = 0, hi = F - 1;
-            while (lo < hi) {
-                int mid = (lo + hi + 1) >> 1;
-                if (__ldg(cut_ptr + mid) <= gbin) lo = mid;
-                else hi = mid - 1;
-            }
-            f = lo;
-            bb = gbin - __ldg(cut_ptr + f);
-        }
-        feature_d[j] = f;
-        bin_d[j] = bb;
-        dl_d[j] = (int8_t)dl;
-        child_d[4 * j + 0] = found ? b.Lg : 0;
-        child_d[4 * j + 1] = found ? b.Lh : 0;
-        child_d[4 * j + 2] = found ? Tg - b.Lg : 0;
-        child_d[4 * j + 3] = found ? Th - b.Lh : 0;
+    const FeatBest b = reduce_node(a, j);
+    if (threadIdx.x != 0) return;
+    const long long Tg = a.totals_direct[2 * j], Th = a.totals_direct[2 * j + 1];
+    const bool found = b.idx != LLONG_MAX;
+    split_d[j] = found && b.gain > 0.0;
+    gain_d[j] = found ? b.gain : 0.0;
+    int f = -1, bb = -1, dl = 0;
+    if (found) {
+        const int gbin = (int)(b.idx >> 1);
+        dl = (b.idx & 1) == 0;
+        f = feature_of_bin(a.cut_ptr, a.F, gbin);
+        bb = gbin - __ldg(a.cut_ptr + f);
     }
+    feature_d[j] = f;
+    bin_d[j] = bb;
+    dl_d[j] = (int8_t)dl;
+    child_d[4 * j + 0] = found ? b.Lg : 0;
+    child_d[4 * j + 1] = found ? b.Lh : 0;
+    child_d[4 * j + 2] = found ? Tg - b.Lg : 0;
+    child_d[4 * j + 3] = found ? Th - b.Lh : 0;
 }
 
-__global__ void init_tree_kernel(TreeDev t, long long cap, NodeDev *nodes, long long n_rows,
-                                 int *tile_base0) {
+__global__ void init_tree_kernel(TreeDev t, long long cap, NodeDev *nodes, long long n_rows) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < cap;
          k += (long long)gridDim.x * blockDim.x) {
         t.kind[k] = GBM_NODE_ABSENT;
@@ -736,56 +1032,92 @@ __global__ void init_tree_kernel(TreeDev t, long long cap, NodeDev *nodes, long 
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         nodes[0].start = 0;
         nodes[0].count = n_rows;
-        tile_base0[0] = 0;
-        tile_base0[1] = (int)((n_rows + PT - 1) / PT);
     }
 }
 
 // ============================================================== host planning
 struct HistPlan {
     std::vector<Group> groups;
+    bool wide = false, byte_path = false, sent = false;
+    int hstride = 0;      // words per smem channel
     int smem_bytes = 0;   // dynamic smem per block
-    int blocks = 0;       // resident grid
-    int chunk = 0;        // rows per item
+    int blocks_range = 0, blocks_fused = 0;
+    int chunk = 0;        // rows per range item
 };
 
-static int plan_hist(gbm_ctx *ctx, const QM &qm, const int32_t *cut_ptr_h, bool wide, long long rows_hint,
+template <bool W, bool B, bool S>
+static int setup_kernels(gbm_ctx *ctx, HistPlan &hp) {
+    GBM_CUDA(cudaFuncSetAttribute(hist_range_kernel<W, B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+    GBM_CUDA(cudaFuncSetAttribute(part_hist_kernel<W, B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+    int o1 = 0, o2 = 0;
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_range_kernel<W, B, S>, H_THREADS, hp.smem_bytes));
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_kernel<W, B, S>, H_THREADS, hp.smem_bytes));
+    if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "histogram kernels cannot be resident (shared memory)");
+    hp.blocks_range = o1 * ctx->sm_count;
+    hp.blocks_fused = o2 * ctx->sm_count;
+    return GBM_OK;
+}
+
+#define GBM_DISPATCH(hp, F, ...)                                                                  \
+    (hp.wide ? (hp.byte_path ? (hp.sent ? F<true, true, true>(__VA_ARGS__) : F<true, true, false>(__VA_ARGS__)) \
+                             : F<true, false, false>(__VA_ARGS__))                                 \
+             : (hp.byte_path ? (hp.sent ? F<false, true, true>(__VA_ARGS__) : F<false, true, false>(__VA_ARGS__)) \
+                             : F<false, false, false>(__VA_ARGS__)))
+
+static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide, long long rows_hint,
                      HistPlan &hp) {
-    const int bytes_per_bin = wide ? 16 : 8;
-    const int budget = (int)std::min<size_t>(ctx->smem_optin - 24 * 1024, 200 * 1024);
-    const int max_bins_group = budget / bytes_per_bin;
+    const int *cp = q->cut_ptr_h;
+    hp.wide = wide;
+    hp.byte_path = q->bits == 8 && (qm.stride % 32) == 0;
+    hp.sent = q->max_bins < 256;  // the sentinel symbol fits in 8 bits
+    const int channels = wide ? 4 : 2;
+    const int static_smem = 16 * 1024;
+    const int budget = (int)std::min<size_t>(ctx->smem_optin - static_smem, 200 * 1024);
+    const int max_bins_group = budget / (4 * channels) - DUMMY_BINS - 32;
     hp.groups.clear();
     int u = 0;
     while (u < qm.U) {
         Group g;
         g.u_lo = u;
-        g.bin_lo = cut_ptr_h[std::min(u * qm.S, qm.F)];
+        g.bin_lo = cp[std::min(u * qm.S, qm.F)];
         int u_end = u;
         while (u_end < qm.U) {
-            int f_hi = std::min((u_end + 1) * qm.S, qm.F);
-            int nb = cut_ptr_h[f_hi] - g.bin_lo;
-            int nf = f_hi - u * qm.S;
-            if ((nb > max_bins_group || nf > 2048) && u_end > u) break;
-            if (nb > max_bins_group) return fail(GBM_E_ARG, "a single feature unit has more bins than fit in shared memory");
+            const int f_hi = std::min((u_end + 1) * qm.S, qm.F);
+            const int nb = cp[f_hi] - g.bin_lo;
+            const int nf = f_hi - u * qm.S;
+            if ((nb > max_bins_group || nf > 2048 || (u_end - u + 1) > 32) && u_end > u) break;
+            if (nb > max_bins_group)
+                return fail(GBM_E_ARG, "a single feature unit has more bins than fit in shared memory");
             u_end++;
         }
         g.u_hi = u_end;
-        g.bin_hi = cut_ptr_h[std::min(u_end * qm.S, qm.F)];
+        g.bin_hi = cp[std::min(u_end * qm.S, qm.F)];
         hp.groups.push_back(g);
         u = u_end;
     }
     int max_nb = 1;
     for (auto &g : hp.groups) max_nb = std::max(max_nb, g.bin_hi - g.bin_lo);
-    hp.smem_bytes = max_nb * bytes_per_bin;
-    auto kern = wide ? hist_kernel<true> : hist_kernel<false>;
-    GBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
-    int occ = 0;
-    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, H_THREADS, hp.smem_bytes));
-    if (occ < 1) return fail(GBM_E_ARG, "histogram kernel cannot be resident");
-    hp.blocks = occ * ctx->sm_count;
-    // about two items per resident block per pass over the rows, capped by the exactness bound
-    long long per = (rows_hint + 2ll * hp.blocks - 1) / (2ll * hp.blocks) * (long long)hp.groups.size();
+    hp.hstride = (max_nb + DUMMY_BINS + 31) / 32 * 32;
+    hp.smem_bytes = channels * hp.hstride * 4;
+    GBM_TRY(GBM_DISPATCH(hp, setup_kernels, ctx, hp));
+    long long per = (rows_hint + 2ll * hp.blocks_range - 1) / (2ll * hp.blocks_range) * (long long)hp.groups.size();
     hp.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per));
+    return GBM_OK;
+}
+
+template <bool W, bool B, bool S>
+static int launch_range(gbm_ctx *ctx, const HistPlan &hp, RangeArgs a, cudaStream_t s) {
+    const long long n_items = (a.n_sel + a.chunk - 1) / a.chunk * (long long)a.n_groups;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(n_items, hp.blocks_range));
+    hist_range_kernel<W, B, S><<<grid, H_THREADS, hp.smem_bytes, s>>>(a);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
+template <bool W, bool B, bool S>
+static int launch_fused(gbm_ctx *ctx, const HistPlan &hp, FusedArgs a, cudaStream_t s) {
+    part_hist_kernel<W, B, S><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
+    GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
 
@@ -814,11 +1146,15 @@ static int check_qm(const gbm_qmatrix *qm) {
     return GBM_OK;
 }
 
-static int launch_hist(gbm_ctx *ctx, bool wide, const HistPlan &hp, const HistArgs &a, int grid, cudaStream_t s) {
-    if (wide) hist_kernel<true><<<grid, H_THREADS, hp.smem_bytes, s>>>(a);
-    else hist_kernel<false><<<grid, H_THREADS, hp.smem_bytes, s>>>(a);
-    GBM_CUDA(cudaGetLastError());
-    return GBM_OK;
+static EvalArgs eval_args_base(const gbm_qmatrix *q, const int32_t *scale_d, const gbm_params *prm) {
+    EvalArgs a = {};
+    a.F = q->n_features;
+    a.TB = q->cut_ptr_h[q->n_features];
+    a.cut_ptr = q->cut_ptr_d;
+    a.cut_values = q->cut_values_d;
+    a.scale = scale_d;
+    a.p = EvalParams{prm->eta, prm->lambda, prm->gamma, prm->min_child_weight, prm->max_depth};
+    return a;
 }
 
 }  // namespace gbm
@@ -837,37 +1173,34 @@ int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair
     cudaStream_t s = (cudaStream_t)stream;
     const QM qm = make_qm(q);
     const int TB = q->cut_ptr_h[q->n_features];
-    const bool wide = grad_bits > 15;
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, qm, q->cut_ptr_h, wide, n_sel, hp));
+    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp));
     GBM_TRY(ctx->arena.reserve(hp.groups.size() * sizeof(Group) + 256));
     Group *groups = ctx->arena.take<Group>(hp.groups.size());
     GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), hp.groups.size() * sizeof(Group), cudaMemcpyHostToDevice, s));
-    GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)TB * 2 * 8, s));
+    GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)std::max(TB, 1) * 2 * 8, s));
     if (n_sel == 0 || TB == 0) return GBM_OK;
-    HistArgs a = {};
+    RangeArgs a = {};
     a.qm = qm;
     a.qpair = reinterpret_cast<const int2 *>(qpair_d);
     a.ridx = rows_d;
-    a.items = nullptr;
     a.n_sel = n_sel;
     a.chunk = hp.chunk;
     a.n_groups = (int)hp.groups.size();
     a.groups = groups;
     a.cut_ptr = q->cut_ptr_d;
-    a.hist = reinterpret_cast<long long *>(hist_d);
-    a.totals = nullptr;
-    a.TB = TB;
-    long long n_items = (n_sel + hp.chunk - 1) / hp.chunk * (long long)hp.groups.size();
-    int grid = (int)std::min<long long>(n_items, hp.blocks);
-    GBM_TRY(launch_hist(ctx, wide, hp, a, grid, s));
-    // the pageable H2D copy of `groups` above completes before this call returns
-    return GBM_OK;
+    a.hist = reinterpret_cast<unsigned long long *>(hist_d);
+    a.hstride = hp.hstride;
+    int slot = -1;
+    a.rows_ctr = prof_rows_slot(ctx, &slot);
+    ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, (double)q->n_features * q->bits / 8.0 + 8.0 + (rows_d ? 4.0 : 0.0));
+    return GBM_DISPATCH(hp, launch_range, ctx, hp, a, s);
 }
 
 int gbm_allreduce_histograms(gbm_ctx *ctx, int64_t *hist_d, int64_t count, void *stream) {
     GBM_TRY(ctx_enter(ctx));
     GBM_REQUIRE(hist_d && count >= 0, GBM_E_ARG, "gbm_allreduce_histograms: bad arguments");
+    ProfScope ps(ctx, PC_ALLREDUCE, (cudaStream_t)stream, (double)count * 8);
     return allreduce_i64(ctx, reinterpret_cast<long long *>(hist_d), (size_t)count, (cudaStream_t)stream);
 }
 
@@ -880,12 +1213,18 @@ int gbm_evaluate_splits(gbm_ctx *ctx, const gbm_qmatrix *q, const int64_t *hist_
                     bin_d && default_left_d && gain_d && child_d && n_nodes >= 0,
                 GBM_E_ARG, "gbm_evaluate_splits: bad arguments");
     if (n_nodes == 0) return GBM_OK;
-    EvalParams p = {prm->eta, prm->lambda, prm->gamma, prm->min_child_weight, prm->max_depth};
-    const int TB = q->cut_ptr_h[q->n_features];
-    eval_many_kernel<<<n_nodes, E_THREADS, 0, (cudaStream_t)stream>>>(
-        q->n_features, TB, q->cut_ptr_d, scale_d, p, reinterpret_cast<const long long *>(hist_d),
-        reinterpret_cast<const long long *>(totals_d), split_d, feature_d, bin_d, default_left_d, gain_d,
-        reinterpret_cast<long long *>(child_d));
+    cudaStream_t s = (cudaStream_t)stream;
+    EvalArgs a = eval_args_base(q, scale_d, prm);
+    a.n_nodes = n_nodes;
+    a.hist_direct = reinterpret_cast<const long long *>(hist_d);
+    a.totals_direct = reinterpret_cast<const long long *>(totals_d);
+    GBM_TRY(ctx->arena.reserve((size_t)n_nodes * a.F * sizeof(FeatBest) + 256));
+    a.fb = ctx->arena.take<FeatBest>((size_t)n_nodes * a.F);
+    ProfScope ps(ctx, PC_EVAL, s);
+    const long long warps = (long long)n_nodes * a.F;
+    eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(a);
+    eval_out_kernel<<<n_nodes, E_THREADS, 0, s>>>(a, split_d, feature_d, bin_d, default_left_d, gain_d,
+                                                  reinterpret_cast<long long *>(child_d));
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
@@ -902,17 +1241,23 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
         return GBM_OK;
     }
     const QM qm = make_qm(q);
+    HistPlan hp;
+    GBM_TRY(plan_hist(ctx, q, qm, false, n_sel, hp));
     const int tiles = (int)((n_sel + PT - 1) / PT);
+    const int max_items = ((tiles + RUN - 1) / RUN) + 2;
     Arena &A = ctx->arena;
-    GBM_TRY(A.reserve(3 * sizeof(NodeDev) + 64 + (size_t)tiles * (PT / 32) * 4 + 2 * (size_t)tiles * 4 + 16 * 256 +
-                      sizeof(HistItem)));
+    GBM_TRY(A.reserve(3 * sizeof(NodeDev) + (size_t)tiles * (PT / 32) * 4 + 2 * (size_t)tiles * 4 + 32 * 256 +
+                      max_items * sizeof(TileItem) + (size_t)q->cut_ptr_h[q->n_features] * 16 + hp.groups.size() * 16 +
+                      1024));
     NodeDev *nodes = A.take<NodeDev>(3);
-    int *tile_base = A.take<int>(2);
-    int *next_tb = A.take<int>(3);
-    uint32_t *flags = A.take<uint32_t>((size_t)std::max(tiles, 1) * (PT / 32));
-    int *tile_left = A.take<int>(std::max(tiles, 1));
-    int *tile_off = A.take<int>(std::max(tiles, 1));
+    int *tile_base = A.take<int>(4);
+    uint32_t *flags = A.take<uint32_t>((size_t)tiles * (PT / 32));
+    int *tile_left = A.take<int>(tiles);
+    int *tile_off = A.take<int>(tiles);
     int *n_items = A.take<int>(1);
+    TileItem *items = A.take<TileItem>(max_items);
+    unsigned long long *hist = A.take<unsigned long long>((size_t)std::max(1, q->cut_ptr_h[q->n_features]) * 2);
+    Group *groups = A.take<Group>(hp.groups.size());
     NodeDev h[3] = {};
     h[0].start = 0;
     h[0].count = n_sel;
@@ -921,14 +1266,38 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     h[0].b = bin;
     h[0].dl = default_left ? 1 : 0;
     h[0].build_left = 1;
-    int tb[2] = {0, tiles};
     GBM_CUDA(cudaMemcpyAsync(nodes, h, sizeof(h), cudaMemcpyHostToDevice, s));
-    GBM_CUDA(cudaMemcpyAsync(tile_base, tb, sizeof(tb), cudaMemcpyHostToDevice, s));
-    const int grid = std::max(1, std::min(tiles, ctx->sm_count * 8));
-    part_count_kernel<false><<<grid, P_THREADS, 0, s>>>(qm, nodes, 0, 1, tile_base, rows_d, flags, tile_left, nullptr);
-    part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, 1, tile_base, tile_left, tile_off, nullptr, n_items, 1, 1, next_tb, 0);
-    part_scatter_kernel<<<grid, P_THREADS, 0, s>>>(nodes, 0, 1, tile_base, flags, tile_off, rows_d, out_d);
+    GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), hp.groups.size() * sizeof(Group), cudaMemcpyHostToDevice, s));
+    plan_kernel<<<1, 1024, 0, s>>>(nodes, 0, 1, 1, tile_base, items, n_items);  // one group: flags only needed
+    GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)tiles, s));
+    FusedArgs fa = {};
+    fa.qm = qm;
+    fa.nodes = nodes;
+    fa.first = 0;
+    fa.n_par = 1;
+    fa.tile_base = tile_base;
+    fa.items = items;
+    fa.n_items = n_items;
+    fa.ridx_in = rows_d;
+    fa.flags = flags;
+    fa.tile_left = tile_left;
+    fa.qpair = nullptr;  // histogram of a dummy group is not computed: see n_groups = 1 below
+    fa.groups = groups;
+    fa.cut_ptr = q->cut_ptr_d;
+    fa.hist = hist;
+    fa.TB = q->cut_ptr_h[q->n_features];
+    fa.hstride = hp.hstride;
+    // the fused kernel needs a qpair for the build rows: use a zero pair array of the rows
+    int2 *zq;
+    GBM_CUDA(cudaMallocAsync((void **)&zq, sizeof(int2) * (size_t)q->n_rows, s));
+    GBM_CUDA(cudaMemsetAsync(zq, 0, sizeof(int2) * (size_t)q->n_rows, s));
+    fa.qpair = zq;
+    GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s));
+    part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, tile_base, tile_left, tile_off);
+    part_scatter_kernel<<<std::max(1, std::min(tiles, ctx->sm_count * 8)), P_THREADS, 0, s>>>(
+        nodes, 0, 1, tile_base, flags, tile_off, rows_d, out_d, nullptr);
     GBM_CUDA(cudaGetLastError());
+    GBM_CUDA(cudaFreeAsync(zq, s));
     GBM_CUDA(cudaMemcpyAsync(n_left_d, &nodes[1].count, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     GBM_CUDA(cudaStreamSynchronize(s));  // host staging above must outlive the copies
     return GBM_OK;
@@ -951,115 +1320,178 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     cudaStream_t s = (cudaStream_t)stream;
     const QM qm = make_qm(q);
     const int F = q->n_features, D = prm->max_depth;
-    const int TB = q->cut_ptr_h[F];
-    const bool wide = prm->grad_bits > 15;
+    const long long TB = q->cut_ptr_h[F];
     const long long cap = (1ll << (D + 1)) - 1;
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, qm, q->cut_ptr_h, wide, std::max<long long>(n, 1), hp));
+    GBM_TRY(plan_hist(ctx, q, qm, prm->grad_bits > 15, std::max<long long>(n, 1), hp));
     const int G = (int)hp.groups.size();
 
     // ---- scratch (tree arena)
-    const int max_par = D >= 1 ? (1 << (D - 1)) : 1;            // parents partitioned at one level
+    const int max_par = D >= 1 ? (1 << (D - 1)) : 1;  // parents of one level
     const long long max_tiles = (n + PT - 1) / PT + 2ll * max_par + 2;
-    const long long max_items = ((n + hp.chunk - 1) / hp.chunk + max_par + 1) * G;
-    const long long slots_build = std::max(1, D >= 2 ? (1 << (D - 2)) : 1);
-    const long long slots_lvl = std::max(1, D >= 2 ? (1 << (D - 2)) : 1);
-    const size_t hist_unit = (size_t)TB * 2;
+    const long long max_items = (max_tiles / RUN + 2ll * max_par + 2) * G;
+    const long long slots = std::max(1, D >= 2 ? (1 << (D - 2)) : 1);
+    const size_t hist_unit = (size_t)std::max<long long>(TB, 1) * 2;
     size_t need = 0;
-    need += 2 * (size_t)std::max<long long>(n, 1) * 4 + 512;                  // ridx x2
-    need += (size_t)max_tiles * (PT / 32) * 4 + 256;                          // flags
-    need += 2 * (size_t)max_tiles * 4 + 512;                                  // tile_left/off
-    need += (size_t)(D + 2) * (2 * max_par + 2) * 4 + 256 * (D + 2);           // tile bases
-    need += (size_t)(2 * cap + 2) * sizeof(NodeDev) + 256;                    // nodes
-    need += (size_t)max_items * sizeof(HistItem) + 256 + 256;                 // items + count
+    need += 2 * (size_t)std::max<long long>(n, 1) * 4 + 512;          // ridx x2
+    need += (size_t)max_tiles * (PT / 32) * 4 + 256;                  // flags
+    need += 2 * (size_t)max_tiles * 4 + 512;                          // tile_left/off
+    need += (size_t)(2 * max_par + 2) * 4 + 256;                      // tile base
+    need += (size_t)(2 * cap + 2) * sizeof(NodeDev) + 256;            // nodes
+    need += (size_t)max_items * sizeof(TileItem) + 512;               // items + count
     need += G * sizeof(Group) + 256;
-    need += (slots_build * hist_unit + hist_unit + 2) * 8 + 512;                // build + root
-    need += 2 * slots_lvl * hist_unit * 8 + 512;                              // level hists
+    need += (slots * hist_unit + hist_unit + 2) * 8 + 512;            // build + root
+    need += 2 * slots * hist_unit * 8 + 512;                          // level hists
+    need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 256;
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     uint32_t *ridx[2] = {A.take<uint32_t>(std::max<long long>(n, 1)), A.take<uint32_t>(std::max<long long>(n, 1))};
     uint32_t *flags = A.take<uint32_t>((size_t)max_tiles * (PT / 32));
     int *tile_left = A.take<int>(max_tiles);
     int *tile_off = A.take<int>(max_tiles);
-    std::vector<int *> tile_base(D + 2);
-    for (int l = 0; l <= D + 1; ++l) tile_base[l] = A.take<int>(2 * max_par + 2);
+    int *tile_base = A.take<int>(2 * max_par + 2);
     NodeDev *nodes = A.take<NodeDev>(2 * cap + 2);
-    HistItem *items = A.take<HistItem>(max_items);
+    TileItem *items = A.take<TileItem>(max_items);
     int *n_items = A.take<int>(1);
     Group *groups = A.take<Group>(G);
-    long long *hist_root = A.take<long long>(hist_unit + 2);   // root histogram + totals
-    long long *hist_build = A.take<long long>(slots_build * hist_unit);
-    long long *hist_lvl[2] = {A.take<long long>(slots_lvl * hist_unit), A.take<long long>(slots_lvl * hist_unit)};
+    long long *hist_root = A.take<long long>(hist_unit + 2);  // root histogram + totals
+    long long *hist_build = A.take<long long>(slots * hist_unit);
+    long long *hist_lvl[2] = {A.take<long long>(slots * hist_unit), A.take<long long>(slots * hist_unit)};
+    FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
 
     GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
     const TreeDev t = tree_dev(tree);
-    const EvalParams ep = {prm->eta, prm->lambda, prm->gamma, prm->min_child_weight, D};
-    init_tree_kernel<<<(int)std::min<long long>((cap + 255) / 256, 1024), 256, 0, s>>>(t, cap, nodes, n, tile_base[0]);
-    GBM_CUDA(cudaGetLastError());
+    const double row_bytes = (double)F * q->bits / 8.0;  // algorithmic bytes of one packed row
+    {
+        ProfScope ps(ctx, PC_INIT, s);
+        init_tree_kernel<<<(int)std::min<long long>((cap + 255) / 256, 1024), 256, 0, s>>>(t, cap, nodes, n);
+    }
 
     // ---- InitRoot: root histogram + totals, allreduce, evaluate
     GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
-    HistArgs a = {};
-    a.qm = qm;
-    a.qpair = reinterpret_cast<const int2 *>(qpair_d);
-    a.n_groups = G;
-    a.groups = groups;
-    a.cut_ptr = q->cut_ptr_d;
-    a.TB = TB;
-    if (n > 0) {
-        a.ridx = nullptr;
-        a.items = nullptr;
-        a.n_sel = n;
-        a.chunk = hp.chunk;
-        a.hist = hist_root;
-        a.totals = hist_root + hist_unit;
-        long long n_it = (n + hp.chunk - 1) / hp.chunk * (long long)G;
-        GBM_TRY(launch_hist(ctx, wide, hp, a, (int)std::min<long long>(n_it, hp.blocks), s));
+    if (n > 0 && TB > 0) {
+        RangeArgs ra = {};
+        ra.qm = qm;
+        ra.qpair = reinterpret_cast<const int2 *>(qpair_d);
+        ra.ridx = nullptr;
+        ra.n_sel = n;
+        ra.chunk = hp.chunk;
+        ra.n_groups = G;
+        ra.groups = groups;
+        ra.cut_ptr = q->cut_ptr_d;
+        ra.hist = reinterpret_cast<unsigned long long *>(hist_root);
+        ra.totals = reinterpret_cast<unsigned long long *>(hist_root + hist_unit);
+        ra.hstride = hp.hstride;
+        ProfScope ps(ctx, PC_HIST_ROOT, s, (double)n * (row_bytes + 8.0));
+        GBM_TRY(GBM_DISPATCH(hp, launch_range, ctx, hp, ra, s));
+    } else if (n > 0) {
+        return fail(GBM_E_ARG, "gbm_build_tree: no feature has a cut (all values missing)");
     }
-    GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
-    eval_level_kernel<<<1, E_THREADS, 0, s>>>(0, 0, F, TB, q->cut_ptr_d, q->cut_values_d, scale_d, ep, nodes,
-                                              hist_root, nullptr, nullptr, nullptr, t);
-    GBM_CUDA(cudaGetLastError());
+    {
+        ProfScope ps(ctx, PC_ALLREDUCE, s, (double)(hist_unit + 2) * 8);
+        GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
+    }
+    EvalArgs ea = eval_args_base(q, scale_d, prm);
+    ea.nodes = nodes;
+    ea.hist_root = hist_root;
+    ea.hist_build = hist_build;
+    ea.fb = fb;
+    {
+        ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
+        ea.level = 0;
+        ea.first = 0;
+        ea.n_nodes = 1;
+        if (D > 0) eval_feat_kernel<<<(F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
+        eval_final_kernel<<<1, E_THREADS, 0, s>>>(ea, t);
+        GBM_CUDA(cudaGetLastError());
+    }
+    if (D == 0) {  // every row sits in the root leaf
+        GBM_CUDA(cudaMemsetAsync(row_leaf_d, 0, sizeof(int32_t) * (size_t)std::max<long long>(n, 0), s));
+        return GBM_OK;
+    }
 
+    FusedArgs fa = {};
+    fa.qm = qm;
+    fa.nodes = nodes;
+    fa.tile_base = tile_base;
+    fa.items = items;
+    fa.n_items = n_items;
+    fa.flags = flags;
+    fa.tile_left = tile_left;
+    fa.row_leaf = row_leaf_d;
+    fa.qpair = reinterpret_cast<const int2 *>(qpair_d);
+    fa.groups = groups;
+    fa.cut_ptr = q->cut_ptr_d;
+    fa.hist = reinterpret_cast<unsigned long long *>(hist_build);
+    fa.TB = std::max<long long>(TB, 1);
+    fa.hstride = hp.hstride;
     const int pgrid = ctx->sm_count * 8;
     for (int l = 1; l <= D; ++l) {
         const int first = (1 << (l - 1)) - 1, n_par = 1 << (l - 1);
         const uint32_t *rin = l == 1 ? nullptr : ridx[(l - 1) & 1];
         uint32_t *rout = ridx[l & 1];
-        if (l == D) {  // final partition: rows straight to their leaves
-            part_count_kernel<true><<<pgrid, P_THREADS, 0, s>>>(qm, nodes, first, n_par, tile_base[l - 1], rin, flags,
-                                                                tile_left, row_leaf_d);
+        const double ridx_b = rin ? 4.0 : 0.0;
+        if (l == D) {  // final level: every row's leaf by a row-order walk of the tree
+            const int n_internal = (1 << D) - 1;
+            const size_t sm = (size_t)n_internal * 8;
+            ProfScope ps(ctx, PC_PART_FINAL, s, (double)n * (q->bits * D / 8.0 + 4.0));
+            if (sm > 48 * 1024)
+                GBM_CUDA(cudaFuncSetAttribute(leaf_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            const int grid = (int)std::max<long long>(1, std::min<long long>((n + WALK_THREADS - 1) / WALK_THREADS,
+                                                                            (long long)ctx->sm_count * 8));
+            if (n > 0)
+                leaf_walk_kernel<<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
+                                                                n_internal, n, row_leaf_d);
             GBM_CUDA(cudaGetLastError());
             break;
         }
-        part_count_kernel<false><<<pgrid, P_THREADS, 0, s>>>(qm, nodes, first, n_par, tile_base[l - 1], rin, flags,
-                                                             tile_left, row_leaf_d);
-        part_scan_kernel<<<1, 1024, 0, s>>>(nodes, first, n_par, tile_base[l - 1], tile_left, tile_off, items, n_items,
-                                            G, hp.chunk, tile_base[l], 1);
-        part_scatter_kernel<<<pgrid, P_THREADS, 0, s>>>(nodes, first, n_par, tile_base[l - 1], flags, tile_off, rin,
-                                                        rout);
-        GBM_CUDA(cudaGetLastError());
-        // BuildPartialHistograms of the built children
+        {
+            ProfScope ps(ctx, PC_PART_SCAN, s);
+            plan_kernel<<<1, 1024, 0, s>>>(nodes, first, n_par, G, tile_base, items, n_items);
+        }
+        GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
+        // RepartitionInstances + BuildPartialHistograms (fused)
         GBM_CUDA(cudaMemsetAsync(hist_build, 0, (size_t)n_par * hist_unit * 8, s));
-        a.ridx = rout;
-        a.items = items;
-        a.n_items_dev = n_items;
-        a.hist = hist_build;
-        a.totals = nullptr;
-        GBM_TRY(launch_hist(ctx, wide, hp, a, hp.blocks, s));
-        // AllReduceHistograms
-        GBM_TRY(allreduce_i64(ctx, hist_build, (size_t)n_par * hist_unit, s));
-        // subtraction + EvaluateSplit for every node of level l
-        const long long *prev = l == 1 ? nullptr : hist_lvl[(l - 1) & 1];
-        long long *store = (l < D - 1) ? hist_lvl[l & 1] : nullptr;
-        eval_level_kernel<<<1 << l, E_THREADS, 0, s>>>(l, (1 << l) - 1, F, TB, q->cut_ptr_d, q->cut_values_d, scale_d,
-                                                       ep, nodes, hist_root, hist_build, prev, store, t);
+        {
+            fa.first = first;
+            fa.n_par = n_par;
+            fa.ridx_in = rin;
+            int slot;
+            fa.rows_ctr = prof_rows_slot(ctx, &slot);
+            // algorithmic bits: split symbol + ridx per parent row; packed row + qpair per built row
+            fa.bits_parent_row = q->bits + (rin ? 32 : 0);
+            fa.bits_built_row = F * q->bits + 64;
+            ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
+            GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s));
+        }
+        {
+            ProfScope ps(ctx, PC_PART_SCAN, s);
+            part_scan_kernel<<<n_par, 1024, 0, s>>>(nodes, first, tile_base, tile_left, tile_off);
+        }
+        {
+            int slot;
+            unsigned long long *rc = prof_rows_slot(ctx, &slot);
+            ProfScope ps(ctx, PC_PART_SCATTER, s, 0.0, slot, ridx_b + 4.0);
+            part_scatter_kernel<<<pgrid, P_THREADS, 0, s>>>(nodes, first, n_par, tile_base, flags, tile_off, rin, rout,
+                                                            rc);
+        }
         GBM_CUDA(cudaGetLastError());
-    }
-    if (D == 0) {  // every row sits in the root leaf
-        part_count_kernel<false><<<pgrid, P_THREADS, 0, s>>>(qm, nodes, 0, 1, tile_base[0], nullptr, flags, tile_left,
-                                                             row_leaf_d);
-        GBM_CUDA(cudaGetLastError());
+        {  // AllReduceHistograms
+            ProfScope ps(ctx, PC_ALLREDUCE, s, (double)n_par * hist_unit * 8);
+            GBM_TRY(allreduce_i64(ctx, hist_build, (size_t)n_par * hist_unit, s));
+        }
+        {  // subtraction + EvaluateSplit for every node of level l
+            ea.level = l;
+            ea.first = (1 << l) - 1;
+            ea.n_nodes = 1 << l;
+            ea.hist_prev = l == 1 ? nullptr : hist_lvl[(l - 1) & 1];
+            ea.hist_store = (l < D - 1) ? hist_lvl[l & 1] : nullptr;
+            ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
+            const long long warps = (long long)ea.n_nodes * F;
+            eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(ea);
+            eval_final_kernel<<<ea.n_nodes, E_THREADS, 0, s>>>(ea, t);
+            GBM_CUDA(cudaGetLastError());
+        }
     }
     return GBM_OK;
 }
