@@ -303,9 +303,9 @@ def run_reference(a):
     import oracle as O
     cfg = W.CONFIGS[a.config]
     n = a.rows or cfg.n_rows
-    budget_s = 150.0
+    budget_s = 90.0   # whole --steps K --warmup W run (plus ~10 s of preparation)
     per_row = 4.5e-6 * (cfg.n_features / 28.0) * (cfg.max_depth / 6.0)
-    rows = int(min(n, max(20_000, budget_s / (a.steps + a.warmup) / per_row)))
+    rows = int(min(n, 2_000_000, max(20_000, budget_s / (a.steps + a.warmup) / per_row)))
     X, y = W.generate(a.config, 0, rows, n_rows=max(rows, cfg.n_rows))
     beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
     b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective, max_depth=cfg.max_depth,

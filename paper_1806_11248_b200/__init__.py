@@ -239,15 +239,8 @@ class Context:
         rank 0 makes the id, torch broadcasts the 128 bytes (plumbing only)."""
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        buf = (C.c_uint8 * 128)()
-        if rank == 0:
-            _call("gbm_comm_unique_id", buf)
-        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
-        if dist.get_backend(group) == "nccl":
-            t = t.to(self.dev)
-        dist.broadcast(t, 0, group=group)
-        ids = (C.c_uint8 * 128)(*t.cpu().tolist())
-        _call("gbm_comm_init", self.h, ids, world, rank)
+        ids = share_unique_id(Context.comm_unique_id, group, device=self.dev)
+        _call("gbm_comm_init", self.h, (C.c_uint8 * 128)(*ids), world, rank)
 
     def comm_init(self, id_bytes: bytes, nranks: int, rank: int):
         ids = (C.c_uint8 * 128)(*id_bytes)
@@ -398,6 +391,22 @@ class Context:
               _p(cat["threshold"]), _p(cat["default_left"]), _p(cat["weight"]),
               float(base_margin), _p(X), n, F, _p(out), _stream())
         return out
+
+
+def share_unique_id(make_id, group=None, device=None) -> bytes:
+    """Rank 0 calls make_id() (128 bytes); torch.distributed broadcasts them to every rank of
+    `group` (gloo: CPU tensor, nccl: tensor on `device`).  Returns the bytes on every rank."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    raw = make_id() if rank == 0 else bytes(128)
+    if len(raw) != 128:
+        raise GbmError(-1, "share_unique_id", "the NCCL unique id must be 128 bytes")
+    t = torch.tensor(list(raw), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast(t, src, group=group)
+    return bytes(t.cpu().tolist())
 
 
 def _nz(t):
