@@ -85,6 +85,13 @@ GBM_API int gbm_profile_enable(gbm_ctx *ctx, int enable);
 GBM_API int gbm_profile_read(gbm_ctx *ctx, gbm_prof_entry *out, int32_t cap, int32_t *n_out);
 GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
 
+/* Tuning options (do not change results, only which kernels compute them).
+ * GBM_OPT_HIST_LAYOUT: shared-memory histogram layout of BuildPartialHistograms --
+ *   0 auto (= compact), 1 compact (random bins, bank conflicts), 2 bank-column (feature per
+ *   lane, conflict-free; falls back to compact when the bins do not fit). */
+enum { GBM_OPT_HIST_LAYOUT = 1 };
+GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
+
 /* ---------------------------------------------------------------- communicator
  * Rank 0 calls gbm_comm_unique_id and broadcasts the 128 bytes with its own process group
  * (the Python binding uses torch.distributed); then every rank calls gbm_comm_init
@@ -156,7 +163,17 @@ typedef struct {
     const float *cut_values_d; /* fp32 [TB]                                                */
     const int32_t *cut_ptr_d;  /* int32 [F+1]                                              */
     const int32_t *cut_ptr_h;  /* int32 [F+1], host copy                                   */
+    const uint8_t *colsym_d;   /* OPTIONAL feature-major copy of the symbols (bits <= 8):    */
+                               /* uint8 [n_features][n_rows], made by gbm_transpose_symbols; */
+                               /* NULL = split symbols are gathered from packed_d            */
 } gbm_qmatrix;
+
+/* gbm_transpose_symbols: fill colsym_d (uint8 [n_features][n_rows], caller-owned) with the
+ * symbols of qm->packed_d in feature-major order.  A time/space trade: RepartitionInstances
+ * then reads one byte per row of the split feature instead of a 32-byte sector of the packed
+ * row.  Requires qm->bits <= 8.  Asynchronous. */
+GBM_API int gbm_transpose_symbols(gbm_ctx *ctx, const gbm_qmatrix *qm, uint8_t *colsym_d,
+                                  void *stream);
 
 typedef struct {
     int32_t objective;         /* GBM_SQUARED_ERROR | GBM_LOGISTIC                          */

@@ -46,7 +46,7 @@ class _QM(C.Structure):
     _fields_ = [("packed_d", C.c_void_p), ("n_rows", C.c_int64), ("n_features", C.c_int32),
                 ("bits", C.c_int32), ("row_align_bits", C.c_int32), ("max_bins", C.c_int32),
                 ("cut_values_d", C.c_void_p), ("cut_ptr_d", C.c_void_p),
-                ("cut_ptr_h", C.POINTER(C.c_int32))]
+                ("cut_ptr_h", C.POINTER(C.c_int32)), ("colsym_d", C.c_void_p)]
 
 
 class _Tree(C.Structure):
@@ -70,6 +70,7 @@ EXPORTS = {
     "gbm_profile_read": (C.c_int, [C.c_void_p, C.POINTER(_ProfEntry), C.c_int32,
                                    C.POINTER(C.c_int32)]),
     "gbm_launch_count": (C.c_int64, [C.c_void_p]),
+    "gbm_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     "gbm_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "gbm_comm_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
     "gbm_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -84,6 +85,7 @@ EXPORTS = {
     "gbm_quantise_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                         C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                         C.c_int64, C.c_void_p]),
+    "gbm_transpose_symbols": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_void_p]),
     "gbm_gradients": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gbm_build_tree": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_void_p,
@@ -172,6 +174,7 @@ class QMatrix:
     cut_values: torch.Tensor      # fp32 [TB]
     cut_ptr: torch.Tensor         # int32 [F+1] (device)
     cut_ptr_h: np.ndarray         # int32 [F+1] (host)
+    colsym: torch.Tensor | None = None  # optional uint8 [F][n] feature-major symbol copy
 
     def c(self) -> _QM:
         self._cp = np.ascontiguousarray(self.cut_ptr_h, dtype=np.int32)
@@ -179,7 +182,8 @@ class QMatrix:
         self._cv = cv
         return _QM(self.packed.data_ptr(), self.n_rows, self.n_features, self.bits,
                    self.row_align_bits, self.max_bins, cv.data_ptr(), self.cut_ptr.data_ptr(),
-                   self._cp.ctypes.data_as(C.POINTER(C.c_int32)))
+                   self._cp.ctypes.data_as(C.POINTER(C.c_int32)),
+                   self.colsym.data_ptr() if self.colsym is not None else None)
 
     @property
     def n_bins_total(self) -> int:
@@ -268,6 +272,11 @@ class Context:
                                            bytes=arr[i].bytes, rows=arr[i].rows)
                 for i in range(n.value)}
 
+    HIST_LAYOUT = 1
+
+    def set_option(self, option: int, value: int):
+        _call("gbm_set_option", self.h, int(option), int(value))
+
     def launch_count(self) -> int:
         return int(lib().gbm_launch_count(self.h))
 
@@ -305,16 +314,27 @@ class Context:
         return out
 
     def make_qmatrix(self, X: torch.Tensor, max_bins: int, row_align_bits: int = 32,
-                     cuts=None) -> QMatrix:
-        """Fig. 1 preprocessing: global cuts (collective), then fused bin map + pack."""
+                     cuts=None, colsym: bool = True) -> QMatrix:
+        """Fig. 1 preprocessing: global cuts (collective), then fused bin map + pack, then
+        (bits <= 8, optional) the feature-major symbol copy used by RepartitionInstances."""
         if cuts is None:
             cv, cp, mx = self.cuts(X, max_bins)
         else:
             cv, cp, mx = cuts
         bits = symbol_bits(mx)
         packed = self.quantise_compress(X, max_bins, cv, cp, bits, row_align_bits)
-        return QMatrix(packed, X.shape[0], X.shape[1], bits, row_align_bits, max_bins, cv, cp,
-                       cp.cpu().numpy())
+        qm = QMatrix(packed, X.shape[0], X.shape[1], bits, row_align_bits, max_bins, cv, cp,
+                     cp.cpu().numpy())
+        if colsym and bits <= 8:
+            self.transpose_symbols(qm)
+        return qm
+
+    def transpose_symbols(self, qm: QMatrix) -> QMatrix:
+        qm.colsym = None
+        col = torch.empty((qm.n_features, max(qm.n_rows, 1)), dtype=torch.uint8, device=self.dev)
+        _call("gbm_transpose_symbols", self.h, C.byref(qm.c()), _p(col), _stream())
+        qm.colsym = col
+        return qm
 
     # ------------------------------------------------------------ §2.5
     def gradients(self, objective, margin, label, grad_bits=DEFAULT_GRAD_BITS, out=None,
@@ -421,12 +441,12 @@ class Booster:
     def __init__(self, ctx: Context, X: torch.Tensor, y: torch.Tensor, *, max_bins: int,
                  objective: str, max_depth: int, eta=0.3, reg_lambda=1.0, gamma=0.0,
                  min_child_weight=1.0, grad_bits=DEFAULT_GRAD_BITS, row_align_bits=32,
-                 base_margin=0.0, cuts=None):
+                 base_margin=0.0, cuts=None, colsym=True):
         self.ctx, self.y = ctx, y
         self.objective, self.max_depth, self.grad_bits = objective, max_depth, grad_bits
         self.kw = dict(eta=eta, reg_lambda=reg_lambda, gamma=gamma,
                        min_child_weight=min_child_weight)
-        self.qm = ctx.make_qmatrix(X, max_bins, row_align_bits, cuts=cuts)
+        self.qm = ctx.make_qmatrix(X, max_bins, row_align_bits, cuts=cuts, colsym=colsym)
         self.base_margin = float(base_margin)
         n = X.shape[0]
         self.margin = torch.full((n,), self.base_margin, dtype=torch.float64, device=ctx.dev)

@@ -235,6 +235,16 @@ int gbm_profile_read(gbm_ctx *ctx, gbm_prof_entry *out, int32_t cap, int32_t *n_
 
 int64_t gbm_launch_count(gbm_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
+int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
+    if (!ctx) return fail(GBM_E_ARG, "null context");
+    if (option == GBM_OPT_HIST_LAYOUT) {
+        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 column");
+        ctx->hist_layout = (int)value;
+        return GBM_OK;
+    }
+    return fail(GBM_E_ARG, "gbm_set_option: unknown option");
+}
+
 int gbm_symbol_bits(int32_t max_symbol) {
     if (max_symbol < 0) return fail(GBM_E_ARG, "gbm_symbol_bits: negative max_symbol");
     int b = 1;

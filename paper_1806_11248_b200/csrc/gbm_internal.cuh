@@ -103,6 +103,7 @@ struct gbm_ctx {
     gbm::Arena tree_arena;         // scratch owned by gbm_build_tree
     gbm::Prof prof;                // optional event timing (gbm_profile_*)
     long long launches = 0;        // kernel launches issued by this context
+    int hist_layout = 0;           // GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 bank-column
 };
 
 namespace gbm {
@@ -131,6 +132,8 @@ struct QM {
     int F, bits, B;    // features, symbol width, sentinel (max_bins)
     int S;             // symbols per unit (a unit spans <= 32 bits)
     int U;             // units per row = ceil(F / S)
+    const uint8_t *col;  // optional feature-major symbol copy [F][n]
+    long long n;         // rows (column stride of col)
 };
 
 inline long long row_stride_bits(int F, int bits, int row_align_bits) {
@@ -148,6 +151,8 @@ inline QM make_qm(const gbm_qmatrix *q) {
     m.stride = row_stride_bits(q->n_features, q->bits, q->row_align_bits);
     m.S = 32 / q->bits;
     m.U = (q->n_features + m.S - 1) / m.S;
+    m.col = q->colsym_d;
+    m.n = q->n_rows;
     return m;
 }
 
@@ -166,6 +171,11 @@ __device__ __forceinline__ uint32_t get_bits(const uint32_t *__restrict__ P, lon
 
 __device__ __forceinline__ uint32_t symbol_at(const QM &m, long long row, int f) {
     return get_bits(m.P, row * m.stride + (long long)f * m.bits, m.bits);
+}
+// symbol of (row, f), from the feature-major copy when present
+__device__ __forceinline__ uint32_t split_symbol(const QM &m, long long row, int f) {
+    if (m.col) return __ldg(m.col + (long long)f * m.n + row);
+    return symbol_at(m, row, f);
 }
 
 // exact floor(j / d) for j < 2^32 / d via a 32-bit multiply-high (magic = ceil(2^32 / d))

@@ -375,6 +375,23 @@ __global__ void tag_kernel(const uint32_t *__restrict__ run_off, const uint32_t 
     if ((long long)d > B) nbins[f] = -nb - 1;
 }
 
+// packed (row-major, bits <= 8) -> feature-major uint8 copy; 64 rows x all features per block
+constexpr int TR_ROWS = 64;
+__global__ void __launch_bounds__(256) transpose_kernel(QM qm, long long n, uint8_t *__restrict__ col) {
+    extern __shared__ uint8_t tr[];  // [TR_ROWS][F]
+    const long long r0 = (long long)blockIdx.x * TR_ROWS;
+    const int rows = (int)min((long long)TR_ROWS, n - r0);
+    for (int e = threadIdx.x; e < rows * qm.F; e += blockDim.x) {
+        const int r = e / qm.F, f = e - r * qm.F;
+        tr[r * qm.F + f] = (uint8_t)symbol_at(qm, r0 + r, f);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * qm.F; e += blockDim.x) {
+        const int f = e / rows, r = e - f * rows;
+        col[(long long)f * n + r0 + r] = tr[r * qm.F + f];
+    }
+}
+
 static int grid_for(long long work, int threads, int sm) {
     long long g = (work + threads - 1) / threads;
     long long cap = (long long)sm * 32;
@@ -539,6 +556,24 @@ int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t 
     *n_cuts_h = (int32_t)tb;
     bool any_missing = present_total < n_total * (long long)F;
     *max_symbol_h = any_missing ? max_bins : std::max(0, max_nb - 1);
+    return GBM_OK;
+}
+
+int gbm_transpose_symbols(gbm_ctx *ctx, const gbm_qmatrix *q, uint8_t *colsym_d, void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(q && q->packed_d && colsym_d && q->n_features > 0 && q->n_rows >= 0, GBM_E_ARG,
+                "gbm_transpose_symbols: bad arguments");
+    GBM_REQUIRE(q->bits >= 1 && q->bits <= 8, GBM_E_ARG, "gbm_transpose_symbols: needs bits <= 8");
+    if (q->n_rows == 0) return GBM_OK;
+    gbm_qmatrix qq = *q;
+    qq.colsym_d = nullptr;
+    const QM qm = make_qm(&qq);
+    const size_t sm = (size_t)TR_ROWS * q->n_features;
+    GBM_REQUIRE(sm <= 200 * 1024, GBM_E_ARG, "gbm_transpose_symbols: too many features");
+    if (sm > 48 * 1024) GBM_CUDA(cudaFuncSetAttribute(transpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ProfScope ps(ctx, PC_QUANT, (cudaStream_t)stream, (double)q->n_rows * q->n_features * (q->bits / 8.0 + 1.0));
+    transpose_kernel<<<(int)((q->n_rows + TR_ROWS - 1) / TR_ROWS), 256, sm, (cudaStream_t)stream>>>(qm, q->n_rows, colsym_d);
+    GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
 

@@ -48,10 +48,6 @@ struct RangeItem {  // rows [start, start+len) of a row source, one feature grou
     int len, pad;
 };
 
-struct TileItem {  // tiles [t0, t1) of parent j, one feature group
-    int j, group, t0, t1;
-};
-
 struct Group {
     int u_lo, u_hi;      // units [u_lo, u_hi) of a row (a unit = S consecutive features)
     int bin_lo, bin_hi;  // global bins of the group's features
@@ -63,13 +59,14 @@ struct FeatBest {  // best candidate of one (node, feature)
     long long Lg, Lh;
 };
 
-constexpr int PT = 1024;         // partition tile (rows)
+constexpr int PT = 2048;         // partition tile (rows): 16 warps x 128 rows
+constexpr int WROWS = PT / 16;   // rows per warp per tile
 constexpr int P_THREADS = 256;   // partition kernels: 8 warps x 4 ballot words
 constexpr int H_THREADS = 512;   // histogram / fused kernels
-constexpr int RUN = 16;          // tiles per fused work item (flush amortisation)
+constexpr int RUN = 8;           // tiles per fused work item (flush amortisation)
 constexpr int E_THREADS = 256;   // evaluation kernels
 constexpr int MAX_CHUNK = 65535; // rows per flush (exactness bound above)
-constexpr int DUMMY_BINS = 256;  // scratch bins for padding features of the byte path
+constexpr int DUMMY_BINS = 32;   // scratch bins: padding features of the byte path (symbol 0)
 
 struct EvalParams {
     double eta, lambda, gamma, mcw;
@@ -156,22 +153,30 @@ __device__ __forceinline__ void accumulate(const QM &qm, const Group &grp, const
         totals = totals && L.w == grp.u_lo;   // each row's pair counted once
         const long long sw = qm.stride >> 5;  // words per row
         int r = L.r0;
-        for (; r + L.rstep < nrows; r += 2 * L.rstep) {  // two rows in flight
-            const uint32_t ra = rowf(r), rb2 = rowf(r + L.rstep);
-            const uint32_t wa = __ldg(qm.P + ra * sw + L.w), wb = __ldg(qm.P + rb2 * sw + L.w);
-            const int2 qa = __ldg(qpair + ra), qb = __ldg(qpair + rb2);
-            if (totals) {
-                *tg += (long long)qa.x + qb.x;
-                *th += (long long)qa.y + qb.y;
+        for (; r + 3 * L.rstep < nrows; r += 4 * L.rstep) {  // four rows in flight
+            uint32_t rw[4], wd[4];
+            int2 qq[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rw[i] = rowf(r + i * L.rstep);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                wd[i] = __ldg(qm.P + rw[i] * sw + L.w);
+                qq[i] = __ldg(qpair + rw[i]);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int sa = (wa >> (8 * j)) & 255, sb = (wb >> (8 * j)) & 255;
-                if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sa, qa);
-                if (!SENT || sb != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sb, qb);
+            for (int i = 0; i < 4; ++i) {
+                if (totals) {
+                    *tg += qq[i].x;
+                    *th += qq[i].y;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int sy = (wd[i] >> (8 * j)) & 255;
+                    if (!SENT || sy != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sy, qq[i]);
+                }
             }
         }
-        if (r < nrows) {
+        for (; r < nrows; r += L.rstep) {
             const uint32_t ra = rowf(r);
             const uint32_t wa = __ldg(qm.P + ra * sw + L.w);
             const int2 qa = __ldg(qpair + ra);
@@ -303,79 +308,87 @@ __device__ __forceinline__ int find_parent(const int *__restrict__ tile_base, in
     return lo;
 }
 
+// Row-index entries of the level buffers.  CARRY (grad_bits <= 15): the row's fixed-point
+// gradient pair travels with its index through every partition, so no level pass gathers qpair
+// (a 64-byte DRAM access per 8-byte pair).  q_g in [-2^15, 2^15] needs 17 bits, q_h in
+// [0, 2^15] 16: x = row | (bit 16 of q_g) << 31 (rows < 2^31), y = q_g[15:0] | q_h << 16.
+template <bool CARRY> struct EntryOf { using T = uint32_t; };
+template <> struct EntryOf<true> { using T = uint2; };
+__device__ __forceinline__ uint32_t row_of(uint32_t e) { return e; }
+__device__ __forceinline__ uint32_t row_of(uint2 e) { return e.x & 0x7fffffffu; }
+template <bool CARRY>
+__device__ __forceinline__ typename EntryOf<CARRY>::T make_entry(uint32_t row, const int2 *__restrict__ qpair) {
+    if constexpr (CARRY) {
+        const int2 q = __ldg(qpair + row);
+        const uint32_t g17 = (uint32_t)q.x & 0x1ffffu;
+        return make_uint2(row | ((g17 >> 16) << 31), (g17 & 0xffffu) | ((uint32_t)q.y << 16));
+    } else {
+        return row;
+    }
+}
+__device__ __forceinline__ int2 entry_q(uint2 e, const int2 *) {
+    const uint32_t g17 = ((e.x >> 31) << 16) | (e.y & 0xffffu);
+    return make_int2(((int)(g17 << 15)) >> 15, (int)(e.y >> 16));
+}
+__device__ __forceinline__ int2 entry_q(uint32_t e, const int2 *__restrict__ qpair) { return __ldg(qpair + e); }
+
 __device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint32_t row) {
-    const uint32_t sym = symbol_at(qm, row, nd.f);
+    const uint32_t sym = split_symbol(qm, row, nd.f);
     return (int)sym == qm.B ? (nd.dl != 0) : ((int)sym <= nd.b);
 }
 
 // ============================================================== plan (1 block)
-// Tile plan of the parents of a level and the fused kernel's work items.  Split parents get
-// RUN-tile items for every feature group; leaf parents one group-0 item per run (row_leaf).
+// Tile plan of the parents of a level: tile_base[j] (first 2048-row tile of parent j) and
+// run_base[j] (first RUN-tile run); n_items = runs x feature groups.  Work item i of the fused
+// kernel is run i / G, group i % G, resolved on the fly (find_parent over run_base).
 __global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
                                                     int n_groups, int *__restrict__ tile_base,
-                                                    TileItem *__restrict__ items, int *__restrict__ n_items) {
+                                                    int *__restrict__ run_base, int *__restrict__ n_items) {
     __shared__ long long sm32[32];
-    __shared__ int carry_t, carry_i;
-    if (threadIdx.x == 0) {
-        carry_t = 0;
-        carry_i = 0;
-    }
+    __shared__ long long carry;
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int c = 0; c < n_par; c += 1024) {
         const int j = c + threadIdx.x;
-        int nt = 0, ni = 0;
+        long long nt = 0, nr = 0;
         if (j < n_par) {
             const NodeDev nd = nodes[first + j];
             if (nd.state != GBM_NODE_ABSENT && nd.count > 0) {
-                nt = (int)((nd.count + PT - 1) / PT);
-                ni = ((nt + RUN - 1) / RUN) * (nd.state == GBM_NODE_SPLIT ? n_groups : 1);
+                nt = (nd.count + PT - 1) / PT;
+                nr = (nt + RUN - 1) / RUN;
             }
         }
-        // block exclusive scan of (nt, ni) packed in one 64-bit value
-        long long v = ((long long)nt << 32) | (unsigned)ni, x = v;
+        const long long v = (nt << 32) | nr;
+        long long x = v;
         for (int o = 1; o < 32; o <<= 1) {
-            long long y = __shfl_up_sync(0xffffffffu, x, o);
+            const long long y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
         if (lane == 31) sm32[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            long long s = sm32[lane];
+            long long t = sm32[lane];
             for (int o = 1; o < 32; o <<= 1) {
-                long long y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
+                const long long y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
             }
-            sm32[lane] = s;
+            sm32[lane] = t;
         }
         __syncthreads();
-        const long long ex = (wid ? sm32[wid - 1] : 0) + x - v;
-        const int tb = carry_t + (int)(ex >> 32), ib = carry_i + (int)(ex & 0xffffffff);
+        const long long ex = carry + (wid ? sm32[wid - 1] : 0) + x - v;
         if (j < n_par) {
-            tile_base[j] = tb;
-            const NodeDev nd = nodes[first + j];
-            const int G = nd.state == GBM_NODE_SPLIT ? n_groups : 1;
-            for (int q = 0; q < ni; ++q) {
-                const int run = q / G, g = q - run * G;
-                TileItem it;
-                it.j = j;
-                it.group = g;
-                it.t0 = tb + run * RUN;
-                it.t1 = min(tb + nt, it.t0 + RUN);
-                items[ib + q] = it;
-            }
+            tile_base[j] = (int)(ex >> 32);
+            run_base[j] = (int)(ex & 0xffffffff);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const long long tot = sm32[31];
-            carry_t += (int)(tot >> 32);
-            carry_i += (int)(tot & 0xffffffff);
-        }
+        if (threadIdx.x == 0) carry += sm32[31];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        tile_base[n_par] = carry_t;
-        *n_items = carry_i;
+        tile_base[n_par] = (int)(carry >> 32);
+        run_base[n_par] = (int)(carry & 0xffffffff);
+        *n_items = (int)(carry & 0xffffffff) * n_groups;
     }
 }
 
@@ -385,9 +398,10 @@ struct FusedArgs {
     const NodeDev *nodes;
     int first, n_par;
     const int *tile_base;
-    const TileItem *items;
+    const int *run_base;
+    int n_groups;
     const int *n_items;
-    const uint32_t *ridx_in;  // null = identity (level 1)
+    const void *ridx_in;      // entries (EntryOf<CARRY>), null = identity (level 1)
     uint32_t *flags;          // [tiles][PT/32]
     int *tile_left;           // [tiles]
     int32_t *row_leaf;
@@ -406,31 +420,36 @@ struct FusedArgs {
 // inside an item).  Per 64-row batch: (A) split symbol of each row -> left flags (ballot), the
 // warp's left count into tile_left, the rows of the built child compacted into a warp-private
 // list; (B) the listed rows' words accumulated by the warp (lane -> fixed word of the row).
-template <bool WIDE, bool BYTE, bool SENT>
+template <bool WIDE, bool BYTE, bool SENT, bool CARRY>
 __global__ void __launch_bounds__(H_THREADS) part_hist_kernel(FusedArgs a) {
+    using E = typename EntryOf<CARRY>::T;
     extern __shared__ int smem[];
     __shared__ int s_off[2049];
-    __shared__ uint32_t s_rows[H_THREADS / 32][64];
+    __shared__ E s_rows[H_THREADS / 32][WROWS];
+    const E *rin = static_cast<const E *>(a.ridx_in);
     const QM &qm = a.qm;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int n_items = *a.n_items;
-    uint32_t *wrows = s_rows[wid];
+    E *wrows = s_rows[wid];
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const TileItem item = a.items[it];
-        const int k = a.first + item.j;
+        const int run = it / a.n_groups, g = it - run * a.n_groups;
+        const int j = find_parent(a.run_base, a.n_par, run);
+        const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
+        const int tb = a.tile_base[j];
+        const int t0 = tb + (run - a.run_base[j]) * RUN, t1 = min(a.tile_base[j + 1], t0 + RUN);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
-            for (int t = item.t0; t < item.t1; ++t) {
-                const long long base = nd.start + (long long)(t - a.tile_base[item.j]) * PT;
+            if (g != 0) continue;
+            for (int t = t0; t < t1; ++t) {
+                const long long base = nd.start + (long long)(t - tb) * PT;
                 for (int i = threadIdx.x; i < PT; i += H_THREADS) {
                     const long long pos = base + i;
-                    if (pos < seg_end) a.row_leaf[a.ridx_in ? __ldg(a.ridx_in + pos) : (uint32_t)pos] = k;
+                    if (pos < seg_end) a.row_leaf[rin ? row_of(rin[pos]) : (uint32_t)pos] = k;
                 }
             }
             continue;
         }
-        const int g = item.group;
         const Group grp = a.groups[g];
         SmemHist h{smem, grp.bin_hi - grp.bin_lo, a.hstride};
         smem_zero<WIDE>(h);
@@ -445,81 +464,95 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_kernel(FusedArgs a) {
         int off[4] = {h.nb, h.nb, h.nb, h.nb};
         if (BYTE && my_r >= 0) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int f = my_u * 4 + j;
-                if (f < qm.F) off[j] = s_off[f - f_lo];
+            for (int jj = 0; jj < 4; ++jj) {
+                const int f = my_u * 4 + jj;
+                if (f < qm.F) off[jj] = s_off[f - f_lo];
             }
         }
         const bool build_left = nd.build_left != 0;
         const long long sw = qm.stride >> 5;
         const uint32_t mask = (1u << qm.bits) - 1u;
         unsigned long long bits_acc = 0;
-        for (int t = item.t0; t < item.t1; ++t) {
-            const long long base = nd.start + (long long)(t - a.tile_base[item.j]) * PT + wid * 64;
-            // (A) partition flags for the warp's 64 rows
-            uint32_t row[2], bw[2];
+        for (int t = t0; t < t1; ++t) {
+            const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
+            // (A) partition flags for the warp's 128 rows (4 per lane)
+            E row[4];
+            uint32_t bw[4];
             int nleft = 0;
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
+            for (int s2 = 0; s2 < 4; ++s2) {
                 const long long pos = base + s2 * 32 + lane;
-                const bool valid = pos < seg_end;
-                uint32_t r = 0;
-                bool left = false;
-                if (valid) {
-                    r = a.ridx_in ? __ldg(a.ridx_in + pos) : (uint32_t)pos;
-                    left = goes_left(qm, nd, r);
-                }
-                const uint32_t lw = __ballot_sync(0xffffffffu, valid && left);
-                bw[s2] = __ballot_sync(0xffffffffu, valid && (left == build_left));
-                if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 2 + s2] = lw;
+                if (pos < seg_end) row[s2] = rin ? rin[pos] : make_entry<CARRY>((uint32_t)pos, a.qpair);
+                else row[s2] = E{};
+            }
+            bool left[4];
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+                left[s2] = base + s2 * 32 + lane < seg_end && goes_left(qm, nd, row_of(row[s2]));
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const bool valid = base + s2 * 32 + lane < seg_end;
+                const uint32_t lw = __ballot_sync(0xffffffffu, valid && left[s2]);
+                bw[s2] = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
+                if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 4 + s2] = lw;
                 nleft += __popc(lw);
-                row[s2] = r;
+            }
+            int nbuild = 0;
+            const uint32_t ltm = (1u << lane) - 1u;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                if ((bw[s2] >> lane) & 1u) wrows[nbuild + __popc(bw[s2] & ltm)] = row[s2];
+                nbuild += __popc(bw[s2]);
             }
             if (g == 0 && lane == 0) {
                 if (nleft) atomicAdd(a.tile_left + t, nleft);
                 if (a.rows_ctr) {
-                    const long long nv = max(0ll, min(64ll, seg_end - base));
+                    const long long nv = max(0ll, min((long long)WROWS, seg_end - base));
                     bits_acc += (unsigned long long)nv * a.bits_parent_row +
-                                (unsigned long long)(__popc(bw[0]) + __popc(bw[1])) * a.bits_built_row;
+                                (unsigned long long)nbuild * a.bits_built_row;
                 }
             }
-            const uint32_t ltm = (1u << lane) - 1u;
-            const int n0 = __popc(bw[0]);
-            if ((bw[0] >> lane) & 1u) wrows[__popc(bw[0] & ltm)] = row[0];
-            if ((bw[1] >> lane) & 1u) wrows[n0 + __popc(bw[1] & ltm)] = row[1];
             __syncwarp();
-            const int nbuild = n0 + __popc(bw[1]);
             // (B) histogram of the listed rows
             if (my_r >= 0) {
                 if (BYTE) {
                     int rr = my_r;
-                    for (; rr + rpp < nbuild; rr += 2 * rpp) {
-                        const uint32_t ra = wrows[rr], rb = wrows[rr + rpp];
-                        const uint32_t wa = __ldg(qm.P + ra * sw + my_u), wb = __ldg(qm.P + rb * sw + my_u);
-                        const int2 qa = __ldg(a.qpair + ra), qb = __ldg(a.qpair + rb);
+                    for (; rr + 3 * rpp < nbuild; rr += 4 * rpp) {
+                        E ew[4];
+                        uint32_t wd[4];
+                        int2 qq[4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int sa = (wa >> (8 * j)) & 255, sb = (wb >> (8 * j)) & 255;
-                            if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[j] + sa, qa);
-                            if (!SENT || sb != qm.B) hist_add<WIDE>(h.base, h.hstride, off[j] + sb, qb);
+                        for (int i = 0; i < 4; ++i) ew[i] = wrows[rr + i * rpp];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            wd[i] = __ldg(qm.P + row_of(ew[i]) * sw + my_u);
+                            qq[i] = entry_q(ew[i], a.qpair);
                         }
-                    }
-                    if (rr < nbuild) {
-                        const uint32_t ra = wrows[rr];
-                        const uint32_t wa = __ldg(qm.P + ra * sw + my_u);
-                        const int2 qa = __ldg(a.qpair + ra);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int sa = (wa >> (8 * j)) & 255;
-                            if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[j] + sa, qa);
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj) {
+                                const int sy = (wd[i] >> (8 * jj)) & 255;
+                                if (!SENT || sy != qm.B) hist_add<WIDE>(h.base, h.hstride, off[jj] + sy, qq[i]);
+                            }
+                    }
+                    for (; rr < nbuild; rr += rpp) {
+                        const E ea = wrows[rr];
+                        const uint32_t wa = __ldg(qm.P + row_of(ea) * sw + my_u);
+                        const int2 qa = entry_q(ea, a.qpair);
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int sa = (wa >> (8 * jj)) & 255;
+                            if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[jj] + sa, qa);
                         }
                     }
                 } else {
                     const int f0 = my_u * qm.S;
                     const int ns = min(qm.S, qm.F - f0);
                     for (int rr = my_r; rr < nbuild; rr += rpp) {
-                        const uint32_t ra = wrows[rr];
-                        const int2 q = __ldg(a.qpair + ra);
+                        const E ea = wrows[rr];
+                        const uint32_t ra = row_of(ea);
+                        const int2 q = entry_q(ea, a.qpair);
                         const uint32_t win =
                             get_bits(qm.P, (long long)ra * qm.stride + (long long)f0 * qm.bits, ns * qm.bits);
                         for (int jj = 0; jj < ns; ++jj) {
@@ -534,7 +567,260 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_kernel(FusedArgs a) {
         }
         if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
         __syncthreads();
-        smem_flush<WIDE>(h, a.hist + ((long long)item.j * a.TB + grp.bin_lo) * 2);
+        smem_flush<WIDE>(h, a.hist + ((long long)j * a.TB + grp.bin_lo) * 2);
+        __syncthreads();
+    }
+}
+
+// ============================================================== bank-column histograms
+// Feature-per-lane layout (GBM_OPT_HIST_LAYOUT = 2, when every feature's bins fit a column): the
+// shared-memory word of (bin b, column c) is b*32 + c, so every update a lane makes falls into
+// bank c and no ATOMS can conflict -- with random bins the compact layout costs ~3.7 bank
+// wavefronts per 32-lane atomic (ncu: 74.9M wavefronts vs 20.1M ideal on the Higgs root pass).
+// Measured: conflict-free, but one row per warp instruction costs ~63 instructions per row
+// (696M vs 111M on the Higgs root pass, 1.19 ms vs 0.33 ms), so it is not the default; it needs
+// a feature-major source staged by TMA to pay off.
+// A group holds Fg <= 32 features; a warp processes R = 32/Fg rows per step: lane = copy*Fg +
+// feature, the R copies of a feature live in different columns and are merged by the flush.
+struct ColGroup {
+    int f_lo, f_hi;  // features [f_lo, f_hi), Fg <= 32
+};
+
+template <bool WIDE>
+__device__ __forceinline__ void col_add(int *hs, int cstride, int word, int2 q) {
+    if (WIDE) {
+        atomicAdd(hs + word, q.x & 0x7fff);
+        atomicAdd(hs + cstride + word, q.y & 0x7fff);
+        atomicAdd(hs + 2 * cstride + word, q.x >> 15);
+        atomicAdd(hs + 3 * cstride + word, q.y >> 15);
+    } else {
+        atomicAdd(hs + word, q.x);
+        atomicAdd(hs + cstride + word, q.y);
+    }
+}
+
+template <bool WIDE>
+__device__ void col_flush(const int *hs, int cstride, const ColGroup &cg, const int32_t *__restrict__ cut_ptr,
+                          unsigned long long *dst /* slot base */) {
+    const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
+    for (int w = threadIdx.x; w < cstride; w += blockDim.x) {
+        const int b = w >> 5, col = w & 31;
+        if (col >= R * Fg) continue;
+        const int f = cg.f_lo + col % Fg;
+        const int c0 = __ldg(cut_ptr + f);
+        if (b >= __ldg(cut_ptr + f + 1) - c0) continue;
+        long long G, H;
+        if (WIDE) {
+            G = (long long)hs[2 * cstride + w] * 32768 + (long long)(unsigned)hs[w];
+            H = (long long)hs[3 * cstride + w] * 32768 + (long long)(unsigned)hs[cstride + w];
+        } else {
+            G = hs[w];
+            H = hs[cstride + w];
+        }
+        if (G) atomicAdd(dst + 2ll * (c0 + b), (unsigned long long)G);
+        if (H) atomicAdd(dst + 2ll * (c0 + b) + 1, (unsigned long long)H);
+    }
+}
+
+struct ColLane {
+    int copy, R, Fg;
+    bool active;
+    long long bitoff;  // f * bits
+};
+
+__device__ __forceinline__ ColLane col_lane(const QM &qm, const ColGroup &cg) {
+    ColLane L;
+    const int lane = threadIdx.x & 31;
+    L.Fg = cg.f_hi - cg.f_lo;
+    L.R = 32 / L.Fg;
+    L.copy = lane / L.Fg;
+    L.active = lane < L.R * L.Fg;
+    L.bitoff = (long long)(cg.f_lo + (L.active ? lane % L.Fg : 0)) * qm.bits;
+    return L;
+}
+
+struct ColRangeArgs {
+    QM qm;
+    const int2 *qpair;
+    const uint32_t *ridx;        // null = identity rows
+    long long n_sel;
+    int chunk, n_groups;
+    const ColGroup *groups;
+    const int32_t *cut_ptr;
+    unsigned long long *hist;    // [TB][2]
+    unsigned long long *totals;  // [2] or null
+    unsigned long long *rows_ctr;
+    int cstride;                 // words per channel = rows * 32
+};
+
+template <bool WIDE>
+__global__ void __launch_bounds__(H_THREADS) hist_col_range_kernel(ColRangeArgs a) {
+    extern __shared__ int smem[];
+    __shared__ long long s_red[2 * H_THREADS / 32];
+    const QM &qm = a.qm;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = H_THREADS / 32;
+    const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int g = it % a.n_groups;
+        const long long start = (long long)(it / a.n_groups) * a.chunk;
+        const long long end = min(a.n_sel, start + a.chunk);
+        const ColGroup cg = a.groups[g];
+        for (int i = threadIdx.x; i < (WIDE ? 4 : 2) * a.cstride; i += H_THREADS) smem[i] = 0;
+        if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)(end - start));
+        __syncthreads();
+        const ColLane L = col_lane(qm, cg);
+        const bool tot = a.totals && g == 0 && L.active && (lane % L.Fg) == 0;
+        long long tg = 0, th = 0;
+        const long long step = (long long)NW * L.R;
+        for (long long r0 = start + (long long)wid * L.R + L.copy; r0 < end; r0 += 4 * step) {
+            uint32_t sym[4];
+            int2 q[4];
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long r = r0 + u * step;
+                ok[u] = L.active && r < end;
+                const uint32_t row = ok[u] ? (a.ridx ? __ldg(a.ridx + r) : (uint32_t)r) : 0u;
+                sym[u] = ok[u] ? get_bits(qm.P, (long long)row * qm.stride + L.bitoff, qm.bits) : 0u;
+                q[u] = ok[u] ? __ldg(a.qpair + row) : make_int2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (ok[u] && (int)sym[u] != qm.B) col_add<WIDE>(smem, a.cstride, (int)sym[u] * 32 + lane, q[u]);
+                if (tot && ok[u]) {
+                    tg += q[u].x;
+                    th += q[u].y;
+                }
+            }
+        }
+        if (a.totals && g == 0) block_totals(tg, th, s_red, a.totals);
+        __syncthreads();
+        col_flush<WIDE>(smem, a.cstride, cg, a.cut_ptr, a.hist);
+        __syncthreads();
+    }
+}
+
+struct ColFusedArgs {
+    QM qm;
+    const NodeDev *nodes;
+    int first, n_par;
+    const int *tile_base;
+    const int *run_base;
+    int n_groups;
+    const int *n_items;
+    const void *ridx_in;  // entries, null = identity (level 1)
+    uint32_t *flags;
+    int *tile_left;
+    int32_t *row_leaf;
+    const int2 *qpair;
+    const ColGroup *groups;
+    const int32_t *cut_ptr;
+    unsigned long long *hist;  // [n_par][TB][2]
+    long long TB;
+    int cstride;
+    unsigned long long *rows_ctr;
+    int bits_parent_row, bits_built_row;
+};
+
+template <bool WIDE, bool CARRY>
+__global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a) {
+    using E = typename EntryOf<CARRY>::T;
+    extern __shared__ int smem[];
+    __shared__ E s_rows[H_THREADS / 32][WROWS];
+    const QM &qm = a.qm;
+    const E *rin = static_cast<const E *>(a.ridx_in);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n_items = *a.n_items;
+    E *wrows = s_rows[wid];
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int run = it / a.n_groups, g = it - run * a.n_groups;
+        const int j = find_parent(a.run_base, a.n_par, run);
+        const int k = a.first + j;
+        const NodeDev nd = a.nodes[k];
+        const int tb = a.tile_base[j];
+        const int t0 = tb + (run - a.run_base[j]) * RUN, t1 = min(a.tile_base[j + 1], t0 + RUN);
+        const long long seg_end = nd.start + nd.count;
+        if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
+            if (g != 0) continue;
+            for (int t = t0; t < t1; ++t) {
+                const long long base = nd.start + (long long)(t - tb) * PT;
+                for (int i = threadIdx.x; i < PT; i += H_THREADS) {
+                    const long long pos = base + i;
+                    if (pos < seg_end) a.row_leaf[rin ? row_of(rin[pos]) : (uint32_t)pos] = k;
+                }
+            }
+            continue;
+        }
+        const ColGroup cg = a.groups[g];
+        for (int i = threadIdx.x; i < (WIDE ? 4 : 2) * a.cstride; i += H_THREADS) smem[i] = 0;
+        __syncthreads();
+        const ColLane L = col_lane(qm, cg);
+        const bool build_left = nd.build_left != 0;
+        unsigned long long bits_acc = 0;
+        for (int t = t0; t < t1; ++t) {
+            const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
+            // (A) partition flags for the warp's 128 rows (lane = row)
+            E row[4];
+            uint32_t bw[4];
+            int nleft = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const long long pos = base + s2 * 32 + lane;
+                if (pos < seg_end) row[s2] = rin ? rin[pos] : make_entry<CARRY>((uint32_t)pos, a.qpair);
+                else row[s2] = E{};
+            }
+            bool left[4];
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+                left[s2] = base + s2 * 32 + lane < seg_end && goes_left(qm, nd, row_of(row[s2]));
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const bool valid = base + s2 * 32 + lane < seg_end;
+                const uint32_t lw = __ballot_sync(0xffffffffu, valid && left[s2]);
+                bw[s2] = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
+                if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 4 + s2] = lw;
+                nleft += __popc(lw);
+            }
+            int nbuild = 0;
+            const uint32_t ltm = (1u << lane) - 1u;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                if ((bw[s2] >> lane) & 1u) wrows[nbuild + __popc(bw[s2] & ltm)] = row[s2];
+                nbuild += __popc(bw[s2]);
+            }
+            if (g == 0 && lane == 0) {
+                if (nleft) atomicAdd(a.tile_left + t, nleft);
+                if (a.rows_ctr) {
+                    const long long nv = max(0ll, min((long long)WROWS, seg_end - base));
+                    bits_acc += (unsigned long long)nv * a.bits_parent_row +
+                                (unsigned long long)nbuild * a.bits_built_row;
+                }
+            }
+            __syncwarp();
+            // (B) histogram of the listed rows, lane = (copy, feature column)
+            for (int i0 = L.copy; i0 < nbuild; i0 += 4 * L.R) {
+                uint32_t sym[4];
+                int2 q[4];
+                bool ok[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * L.R;
+                    ok[u] = L.active && i < nbuild;
+                    const E e = ok[u] ? wrows[i] : E{};
+                    const uint32_t r = row_of(e);
+                    sym[u] = ok[u] ? get_bits(qm.P, (long long)r * qm.stride + L.bitoff, qm.bits) : 0u;
+                    q[u] = ok[u] ? entry_q(e, a.qpair) : make_int2(0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (ok[u] && (int)sym[u] != qm.B) col_add<WIDE>(smem, a.cstride, (int)sym[u] * 32 + lane, q[u]);
+            }
+            __syncwarp();
+        }
+        if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
+        __syncthreads();
+        col_flush<WIDE>(smem, a.cstride, cg, a.cut_ptr, a.hist + (long long)j * a.TB * 2);
         __syncthreads();
     }
 }
@@ -561,7 +847,7 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const in
         while (k < n_internal) {
             const int fk = s_f[k];
             if (!(fk & (1 << 21))) break;
-            const uint32_t sym = symbol_at(qm, i, fk & 0xfffff);
+            const uint32_t sym = split_symbol(qm, i, fk & 0xfffff);
             const bool left = (int)sym == qm.B ? ((fk >> 20) & 1) : ((int)sym <= s_b[k]);
             k = left ? 2 * k + 1 : 2 * k + 2;
         }
@@ -639,10 +925,14 @@ __global__ void __launch_bounds__(1024) part_scan_kernel(NodeDev *__restrict__ n
     }
 }
 
+template <bool CARRY>
 __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
     const NodeDev *__restrict__ nodes, int first, int n_par, const int *__restrict__ tile_base,
-    const uint32_t *__restrict__ flags, const int *__restrict__ tile_off, const uint32_t *__restrict__ ridx_in,
-    uint32_t *__restrict__ ridx_out, unsigned long long *__restrict__ rows_ctr) {
+    const uint32_t *__restrict__ flags, const int *__restrict__ tile_off,
+    const typename EntryOf<CARRY>::T *__restrict__ ridx_in, typename EntryOf<CARRY>::T *__restrict__ ridx_out,
+    const int2 *__restrict__ qpair, unsigned long long *__restrict__ rows_ctr) {
+    using E = typename EntryOf<CARRY>::T;
+    constexpr int WPW = PT / 32 / (P_THREADS / 32);  // flag words per warp (8)
     __shared__ int wpre[PT / 32];
     const int n_tiles = tile_base[n_par];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -655,32 +945,40 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
         const int lt = t - tile_base[j];
         if (rows_ctr && threadIdx.x == 0)
             atomicAdd(rows_ctr, (unsigned long long)min((long long)PT, nd.count - (long long)lt * PT));
-        uint32_t w[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) w[s] = __ldg(flags + (long long)t * (PT / 32) + wid * 4 + s);
-        if (lane < 4) wpre[wid * 4 + lane] = __popc(lane == 0 ? w[0] : lane == 1 ? w[1] : lane == 2 ? w[2] : w[3]);
+        // one flag word per lane (lanes >= WPW idle), warp-scan of the popcounts
+        const uint32_t myw = lane < WPW ? __ldg(flags + (long long)t * (PT / 32) + wid * WPW + lane) : 0u;
+        if (lane < WPW) wpre[wid * WPW + lane] = __popc(myw);
         __syncthreads();
-        if (threadIdx.x < 32) {
-            int v = wpre[threadIdx.x], x = v;
+        static_assert(PT / 32 == 64, "two flag words per lane below");
+        if (threadIdx.x < 32) {  // exclusive scan of the 64 word popcounts, two per lane
+            const int v0 = wpre[2 * lane], v1 = wpre[2 * lane + 1];
+            const int v = v0 + v1;
+            int x = v;
             for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, x, o);
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            wpre[threadIdx.x] = x - v;
+            wpre[2 * lane] = x - v;
+            wpre[2 * lane + 1] = x - v + v0;
         }
         __syncthreads();
         const long long off = tile_off[t];
         const uint32_t ltm = (1u << lane) - 1u;
+        E rows[WPW];
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const int i = wid * 128 + s * 32 + lane;
-            const long long pin = (long long)lt * PT + i;  // position within the node
+        for (int s = 0; s < WPW; ++s) {
+            const long long pin = (long long)lt * PT + wid * (WPW * 32) + s * 32 + lane;
+            if (pin < nd.count) rows[s] = ridx_in ? ridx_in[nd.start + pin] : make_entry<CARRY>((uint32_t)(nd.start + pin), qpair);
+            else rows[s] = E{};
+        }
+#pragma unroll
+        for (int s = 0; s < WPW; ++s) {
+            const uint32_t w = __shfl_sync(0xffffffffu, myw, s);
+            const long long pin = (long long)lt * PT + wid * (WPW * 32) + s * 32 + lane;  // position within the node
             if (pin >= nd.count) continue;
-            const long long pos = nd.start + pin;
-            const uint32_t row = ridx_in ? __ldg(ridx_in + pos) : (uint32_t)pos;
-            const long long lb = off + wpre[wid * 4 + s] + __popc(w[s] & ltm);  // lefts before
-            const bool left = (w[s] >> lane) & 1u;
-            ridx_out[left ? nd.start + lb : nd.start + n_left + (pin - lb)] = row;
+            const long long lb = off + wpre[wid * WPW + s] + __popc(w & ltm);  // lefts before
+            const bool left = (w >> lane) & 1u;
+            ridx_out[left ? nd.start + lb : nd.start + n_left + (pin - lb)] = rows[s];
         }
         __syncthreads();
     }
@@ -1039,6 +1337,10 @@ __global__ void init_tree_kernel(TreeDev t, long long cap, NodeDev *nodes, long 
 struct HistPlan {
     std::vector<Group> groups;
     bool wide = false, byte_path = false, sent = false;
+    bool carry = false;   // level entries carry the gradient pairs (grad_bits <= 15)
+    bool col = false;     // bank-column kernels (every feature has <= rows bins)
+    std::vector<ColGroup> cgroups;
+    int cstride = 0;      // col: words per channel (rows * 32)
     int hstride = 0;      // words per smem channel
     int smem_bytes = 0;   // dynamic smem per block
     int blocks_range = 0, blocks_fused = 0;
@@ -1048,10 +1350,19 @@ struct HistPlan {
 template <bool W, bool B, bool S>
 static int setup_kernels(gbm_ctx *ctx, HistPlan &hp) {
     GBM_CUDA(cudaFuncSetAttribute(hist_range_kernel<W, B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
-    GBM_CUDA(cudaFuncSetAttribute(part_hist_kernel<W, B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+    GBM_CUDA(cudaFuncSetAttribute(part_hist_kernel<W, B, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  hp.smem_bytes));
+    if constexpr (!W)
+        GBM_CUDA(cudaFuncSetAttribute(part_hist_kernel<W, B, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      hp.smem_bytes));
     int o1 = 0, o2 = 0;
     GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_range_kernel<W, B, S>, H_THREADS, hp.smem_bytes));
-    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_kernel<W, B, S>, H_THREADS, hp.smem_bytes));
+    if constexpr (!W)
+        GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_kernel<W, B, S, true>, H_THREADS,
+                                                               hp.smem_bytes));
+    else
+        GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_kernel<W, B, S, false>, H_THREADS,
+                                                               hp.smem_bytes));
     if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "histogram kernels cannot be resident (shared memory)");
     hp.blocks_range = o1 * ctx->sm_count;
     hp.blocks_fused = o2 * ctx->sm_count;
@@ -1064,14 +1375,58 @@ static int setup_kernels(gbm_ctx *ctx, HistPlan &hp) {
              : (hp.byte_path ? (hp.sent ? F<false, true, true>(__VA_ARGS__) : F<false, true, false>(__VA_ARGS__)) \
                              : F<false, false, false>(__VA_ARGS__)))
 
+template <bool W>
+static int setup_col(gbm_ctx *ctx, HistPlan &hp) {
+    GBM_CUDA(cudaFuncSetAttribute(hist_col_range_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+    GBM_CUDA(cudaFuncSetAttribute(part_hist_col_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  hp.smem_bytes));
+    if constexpr (!W)
+        GBM_CUDA(cudaFuncSetAttribute(part_hist_col_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      hp.smem_bytes));
+    int o1 = 0, o2 = 0;
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_col_range_kernel<W>, H_THREADS, hp.smem_bytes));
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_col_kernel<W, !W>, H_THREADS, hp.smem_bytes));
+    if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "column histogram kernels cannot be resident");
+    hp.blocks_range = o1 * ctx->sm_count;
+    hp.blocks_fused = o2 * ctx->sm_count;
+    return GBM_OK;
+}
+
 static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide, long long rows_hint,
-                     HistPlan &hp) {
+                     HistPlan &hp, int grad_bits = 30, bool allow_col = true) {
     const int *cp = q->cut_ptr_h;
     hp.wide = wide;
+    hp.carry = !wide && grad_bits <= 15;
+    // ---- bank-column plan: every feature's bins fit one column of the smem histogram
+    {
+        const int channels = wide ? 4 : 2;
+        const int budget = (int)std::min<size_t>(ctx->smem_optin - 20 * 1024, 200 * 1024);
+        int max_nb = 1;
+        for (int f = 0; f < qm.F; ++f) max_nb = std::max(max_nb, cp[f + 1] - cp[f]);
+        const int rows = (max_nb + 7) / 8 * 8;
+        if (allow_col && channels * rows * 32 * 4 <= budget) {
+            hp.col = true;
+            hp.cstride = rows * 32;
+            hp.smem_bytes = channels * hp.cstride * 4;
+            hp.cgroups.clear();
+            const int ng = (qm.F + 31) / 32;
+            for (int g = 0; g < ng; ++g) {  // balanced groups of <= 32 features
+                ColGroup c;
+                c.f_lo = (int)((long long)qm.F * g / ng);
+                c.f_hi = (int)((long long)qm.F * (g + 1) / ng);
+                hp.cgroups.push_back(c);
+            }
+            GBM_TRY(wide ? setup_col<true>(ctx, hp) : setup_col<false>(ctx, hp));
+            const long long G = (long long)hp.cgroups.size();
+            long long per = (rows_hint + 2ll * hp.blocks_range - 1) / (2ll * hp.blocks_range) * G;
+            hp.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per));
+            return GBM_OK;
+        }
+    }
     hp.byte_path = q->bits == 8 && (qm.stride % 32) == 0;
     hp.sent = q->max_bins < 256;  // the sentinel symbol fits in 8 bits
     const int channels = wide ? 4 : 2;
-    const int static_smem = 16 * 1024;
+    const int static_smem = 26 * 1024;
     const int budget = (int)std::min<size_t>(ctx->smem_optin - static_smem, 200 * 1024);
     const int max_bins_group = budget / (4 * channels) - DUMMY_BINS - 32;
     hp.groups.clear();
@@ -1115,8 +1470,13 @@ static int launch_range(gbm_ctx *ctx, const HistPlan &hp, RangeArgs a, cudaStrea
 }
 
 template <bool W, bool B, bool S>
-static int launch_fused(gbm_ctx *ctx, const HistPlan &hp, FusedArgs a, cudaStream_t s) {
-    part_hist_kernel<W, B, S><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
+static int launch_fused(gbm_ctx *ctx, const HistPlan &hp, FusedArgs a, cudaStream_t s, bool carry) {
+    if constexpr (!W) {
+        if (carry) part_hist_kernel<W, B, S, true><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
+        else part_hist_kernel<W, B, S, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
+    } else {
+        part_hist_kernel<W, B, S, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
+    }
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
@@ -1174,12 +1534,37 @@ int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair
     const QM qm = make_qm(q);
     const int TB = q->cut_ptr_h[q->n_features];
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp));
+    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp, grad_bits, ctx->hist_layout == 2));
+    GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)std::max(TB, 1) * 2 * 8, s));
+    if (n_sel == 0 || TB == 0) return GBM_OK;
+    if (hp.col) {
+        GBM_TRY(ctx->arena.reserve(hp.cgroups.size() * sizeof(ColGroup) + 256));
+        ColGroup *cgs = ctx->arena.take<ColGroup>(hp.cgroups.size());
+        GBM_CUDA(cudaMemcpyAsync(cgs, hp.cgroups.data(), hp.cgroups.size() * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
+        ColRangeArgs ca = {};
+        ca.qm = qm;
+        ca.qpair = reinterpret_cast<const int2 *>(qpair_d);
+        ca.ridx = rows_d;
+        ca.n_sel = n_sel;
+        ca.chunk = hp.chunk;
+        ca.n_groups = (int)hp.cgroups.size();
+        ca.groups = cgs;
+        ca.cut_ptr = q->cut_ptr_d;
+        ca.hist = reinterpret_cast<unsigned long long *>(hist_d);
+        ca.cstride = hp.cstride;
+        int slot = -1;
+        ca.rows_ctr = prof_rows_slot(ctx, &slot);
+        ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, (double)q->n_features * q->bits / 8.0 + 8.0 + (rows_d ? 4.0 : 0.0));
+        const long long n_items = (n_sel + hp.chunk - 1) / hp.chunk * (long long)hp.cgroups.size();
+        const int grid = (int)std::max<long long>(1, std::min<long long>(n_items, hp.blocks_range));
+        if (hp.wide) hist_col_range_kernel<true><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
+        else hist_col_range_kernel<false><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
+        GBM_CUDA(cudaGetLastError());
+        return GBM_OK;
+    }
     GBM_TRY(ctx->arena.reserve(hp.groups.size() * sizeof(Group) + 256));
     Group *groups = ctx->arena.take<Group>(hp.groups.size());
     GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), hp.groups.size() * sizeof(Group), cudaMemcpyHostToDevice, s));
-    GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)std::max(TB, 1) * 2 * 8, s));
-    if (n_sel == 0 || TB == 0) return GBM_OK;
     RangeArgs a = {};
     a.qm = qm;
     a.qpair = reinterpret_cast<const int2 *>(qpair_d);
@@ -1242,12 +1627,12 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     }
     const QM qm = make_qm(q);
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, q, qm, false, n_sel, hp));
+    GBM_TRY(plan_hist(ctx, q, qm, false, n_sel, hp, 30, false));
     const int tiles = (int)((n_sel + PT - 1) / PT);
-    const int max_items = ((tiles + RUN - 1) / RUN) + 2;
+
     Arena &A = ctx->arena;
     GBM_TRY(A.reserve(3 * sizeof(NodeDev) + (size_t)tiles * (PT / 32) * 4 + 2 * (size_t)tiles * 4 + 32 * 256 +
-                      max_items * sizeof(TileItem) + (size_t)q->cut_ptr_h[q->n_features] * 16 + hp.groups.size() * 16 +
+                      64 + (size_t)q->cut_ptr_h[q->n_features] * 16 + hp.groups.size() * 16 +
                       1024));
     NodeDev *nodes = A.take<NodeDev>(3);
     int *tile_base = A.take<int>(4);
@@ -1255,7 +1640,7 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     int *tile_left = A.take<int>(tiles);
     int *tile_off = A.take<int>(tiles);
     int *n_items = A.take<int>(1);
-    TileItem *items = A.take<TileItem>(max_items);
+    int *run_base = A.take<int>(4);
     unsigned long long *hist = A.take<unsigned long long>((size_t)std::max(1, q->cut_ptr_h[q->n_features]) * 2);
     Group *groups = A.take<Group>(hp.groups.size());
     NodeDev h[3] = {};
@@ -1268,7 +1653,7 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     h[0].build_left = 1;
     GBM_CUDA(cudaMemcpyAsync(nodes, h, sizeof(h), cudaMemcpyHostToDevice, s));
     GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), hp.groups.size() * sizeof(Group), cudaMemcpyHostToDevice, s));
-    plan_kernel<<<1, 1024, 0, s>>>(nodes, 0, 1, 1, tile_base, items, n_items);  // one group: flags only needed
+    plan_kernel<<<1, 1024, 0, s>>>(nodes, 0, 1, 1, tile_base, run_base, n_items);  // group 0 only: flags
     GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)tiles, s));
     FusedArgs fa = {};
     fa.qm = qm;
@@ -1276,7 +1661,8 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     fa.first = 0;
     fa.n_par = 1;
     fa.tile_base = tile_base;
-    fa.items = items;
+    fa.run_base = run_base;
+    fa.n_groups = 1;
     fa.n_items = n_items;
     fa.ridx_in = rows_d;
     fa.flags = flags;
@@ -1292,10 +1678,10 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     GBM_CUDA(cudaMallocAsync((void **)&zq, sizeof(int2) * (size_t)q->n_rows, s));
     GBM_CUDA(cudaMemsetAsync(zq, 0, sizeof(int2) * (size_t)q->n_rows, s));
     fa.qpair = zq;
-    GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s));
+    GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, false));
     part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, tile_base, tile_left, tile_off);
-    part_scatter_kernel<<<std::max(1, std::min(tiles, ctx->sm_count * 8)), P_THREADS, 0, s>>>(
-        nodes, 0, 1, tile_base, flags, tile_off, rows_d, out_d, nullptr);
+    part_scatter_kernel<false><<<std::max(1, std::min(tiles, ctx->sm_count * 8)), P_THREADS, 0, s>>>(
+        nodes, 0, 1, tile_base, flags, tile_off, rows_d, out_d, nullptr, nullptr);
     GBM_CUDA(cudaGetLastError());
     GBM_CUDA(cudaFreeAsync(zq, s));
     GBM_CUDA(cudaMemcpyAsync(n_left_d, &nodes[1].count, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -1323,43 +1709,46 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     const long long TB = q->cut_ptr_h[F];
     const long long cap = (1ll << (D + 1)) - 1;
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, q, qm, prm->grad_bits > 15, std::max<long long>(n, 1), hp));
-    const int G = (int)hp.groups.size();
+    GBM_TRY(plan_hist(ctx, q, qm, prm->grad_bits > 15, std::max<long long>(n, 1), hp, prm->grad_bits,
+                      ctx->hist_layout == 2));
+    const int G = hp.col ? (int)hp.cgroups.size() : (int)hp.groups.size();
+    const size_t esz = hp.carry ? 8 : 4;  // bytes per level entry
 
     // ---- scratch (tree arena)
     const int max_par = D >= 1 ? (1 << (D - 1)) : 1;  // parents of one level
     const long long max_tiles = (n + PT - 1) / PT + 2ll * max_par + 2;
-    const long long max_items = (max_tiles / RUN + 2ll * max_par + 2) * G;
     const long long slots = std::max(1, D >= 2 ? (1 << (D - 2)) : 1);
     const size_t hist_unit = (size_t)std::max<long long>(TB, 1) * 2;
     size_t need = 0;
-    need += 2 * (size_t)std::max<long long>(n, 1) * 4 + 512;          // ridx x2
+    need += 2 * (size_t)std::max<long long>(n, 1) * 8 + 512;          // ridx entries x2
     need += (size_t)max_tiles * (PT / 32) * 4 + 256;                  // flags
     need += 2 * (size_t)max_tiles * 4 + 512;                          // tile_left/off
     need += (size_t)(2 * max_par + 2) * 4 + 256;                      // tile base
     need += (size_t)(2 * cap + 2) * sizeof(NodeDev) + 256;            // nodes
-    need += (size_t)max_items * sizeof(TileItem) + 512;               // items + count
-    need += G * sizeof(Group) + 256;
+    need += (size_t)(2 * max_par + 2) * 4 + 512;                      // run base + count
+    need += G * std::max(sizeof(Group), sizeof(ColGroup)) + 256;
     need += (slots * hist_unit + hist_unit + 2) * 8 + 512;            // build + root
     need += 2 * slots * hist_unit * 8 + 512;                          // level hists
     need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 256;
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
-    uint32_t *ridx[2] = {A.take<uint32_t>(std::max<long long>(n, 1)), A.take<uint32_t>(std::max<long long>(n, 1))};
+    char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
     uint32_t *flags = A.take<uint32_t>((size_t)max_tiles * (PT / 32));
     int *tile_left = A.take<int>(max_tiles);
     int *tile_off = A.take<int>(max_tiles);
     int *tile_base = A.take<int>(2 * max_par + 2);
     NodeDev *nodes = A.take<NodeDev>(2 * cap + 2);
-    TileItem *items = A.take<TileItem>(max_items);
+    int *run_base = A.take<int>(2 * max_par + 2);
     int *n_items = A.take<int>(1);
-    Group *groups = A.take<Group>(G);
+    Group *groups = A.take<Group>(hp.col ? 1 : G);
+    ColGroup *cgroups = A.take<ColGroup>(hp.col ? G : 1);
     long long *hist_root = A.take<long long>(hist_unit + 2);  // root histogram + totals
     long long *hist_build = A.take<long long>(slots * hist_unit);
     long long *hist_lvl[2] = {A.take<long long>(slots * hist_unit), A.take<long long>(slots * hist_unit)};
     FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
 
-    GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
+    if (hp.col) GBM_CUDA(cudaMemcpyAsync(cgroups, hp.cgroups.data(), G * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
+    else GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
     const TreeDev t = tree_dev(tree);
     const double row_bytes = (double)F * q->bits / 8.0;  // algorithmic bytes of one packed row
     {
@@ -1369,7 +1758,26 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
 
     // ---- InitRoot: root histogram + totals, allreduce, evaluate
     GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
-    if (n > 0 && TB > 0) {
+    if (n > 0 && TB > 0 && hp.col) {
+        ColRangeArgs ca = {};
+        ca.qm = qm;
+        ca.qpair = reinterpret_cast<const int2 *>(qpair_d);
+        ca.ridx = nullptr;
+        ca.n_sel = n;
+        ca.chunk = hp.chunk;
+        ca.n_groups = G;
+        ca.groups = cgroups;
+        ca.cut_ptr = q->cut_ptr_d;
+        ca.hist = reinterpret_cast<unsigned long long *>(hist_root);
+        ca.totals = reinterpret_cast<unsigned long long *>(hist_root + hist_unit);
+        ca.cstride = hp.cstride;
+        ProfScope ps(ctx, PC_HIST_ROOT, s, (double)n * (row_bytes + 8.0));
+        const long long n_it = (n + hp.chunk - 1) / hp.chunk * (long long)G;
+        const int grid = (int)std::max<long long>(1, std::min<long long>(n_it, hp.blocks_range));
+        if (hp.wide) hist_col_range_kernel<true><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
+        else hist_col_range_kernel<false><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
+        GBM_CUDA(cudaGetLastError());
+    } else if (n > 0 && TB > 0) {
         RangeArgs ra = {};
         ra.qm = qm;
         ra.qpair = reinterpret_cast<const int2 *>(qpair_d);
@@ -1414,7 +1822,8 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     fa.qm = qm;
     fa.nodes = nodes;
     fa.tile_base = tile_base;
-    fa.items = items;
+    fa.run_base = run_base;
+    fa.n_groups = G;
     fa.n_items = n_items;
     fa.flags = flags;
     fa.tile_left = tile_left;
@@ -1428,8 +1837,8 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     const int pgrid = ctx->sm_count * 8;
     for (int l = 1; l <= D; ++l) {
         const int first = (1 << (l - 1)) - 1, n_par = 1 << (l - 1);
-        const uint32_t *rin = l == 1 ? nullptr : ridx[(l - 1) & 1];
-        uint32_t *rout = ridx[l & 1];
+        const char *rin = l == 1 ? nullptr : ridx[(l - 1) & 1];
+        char *rout = ridx[l & 1];
         const double ridx_b = rin ? 4.0 : 0.0;
         if (l == D) {  // final level: every row's leaf by a row-order walk of the tree
             const int n_internal = (1 << D) - 1;
@@ -1447,7 +1856,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         }
         {
             ProfScope ps(ctx, PC_PART_SCAN, s);
-            plan_kernel<<<1, 1024, 0, s>>>(nodes, first, n_par, G, tile_base, items, n_items);
+            plan_kernel<<<1, 1024, 0, s>>>(nodes, first, n_par, G, tile_base, run_base, n_items);
         }
         GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
         // RepartitionInstances + BuildPartialHistograms (fused)
@@ -1462,7 +1871,36 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             fa.bits_parent_row = q->bits + (rin ? 32 : 0);
             fa.bits_built_row = F * q->bits + 64;
             ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
-            GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s));
+            if (hp.col) {
+                ColFusedArgs ca = {};
+                ca.qm = qm;
+                ca.nodes = nodes;
+                ca.first = first;
+                ca.n_par = n_par;
+                ca.tile_base = tile_base;
+                ca.run_base = run_base;
+                ca.n_groups = G;
+                ca.n_items = n_items;
+                ca.ridx_in = rin;
+                ca.flags = flags;
+                ca.tile_left = tile_left;
+                ca.row_leaf = row_leaf_d;
+                ca.qpair = reinterpret_cast<const int2 *>(qpair_d);
+                ca.groups = cgroups;
+                ca.cut_ptr = q->cut_ptr_d;
+                ca.hist = reinterpret_cast<unsigned long long *>(hist_build);
+                ca.TB = std::max<long long>(TB, 1);
+                ca.cstride = hp.cstride;
+                ca.rows_ctr = fa.rows_ctr;
+                ca.bits_parent_row = fa.bits_parent_row;
+                ca.bits_built_row = fa.bits_built_row;
+                if (hp.wide) part_hist_col_kernel<true, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(ca);
+                else if (hp.carry) part_hist_col_kernel<false, true><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(ca);
+                else part_hist_col_kernel<false, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(ca);
+                GBM_CUDA(cudaGetLastError());
+            } else {
+                GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));
+            }
         }
         {
             ProfScope ps(ctx, PC_PART_SCAN, s);
@@ -1472,8 +1910,14 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             int slot;
             unsigned long long *rc = prof_rows_slot(ctx, &slot);
             ProfScope ps(ctx, PC_PART_SCATTER, s, 0.0, slot, ridx_b + 4.0);
-            part_scatter_kernel<<<pgrid, P_THREADS, 0, s>>>(nodes, first, n_par, tile_base, flags, tile_off, rin, rout,
-                                                            rc);
+            if (hp.carry)
+                part_scatter_kernel<true><<<pgrid, P_THREADS, 0, s>>>(
+                    nodes, first, n_par, tile_base, flags, tile_off, reinterpret_cast<const uint2 *>(rin),
+                    reinterpret_cast<uint2 *>(rout), reinterpret_cast<const int2 *>(qpair_d), rc);
+            else
+                part_scatter_kernel<false><<<pgrid, P_THREADS, 0, s>>>(
+                    nodes, first, n_par, tile_base, flags, tile_off, reinterpret_cast<const uint32_t *>(rin),
+                    reinterpret_cast<uint32_t *>(rout), nullptr, rc);
         }
         GBM_CUDA(cudaGetLastError());
         {  // AllReduceHistograms

@@ -124,6 +124,14 @@ def test_compress_overflow_latched(ctx, G):
     assert e.value.code == -3
 
 
+@pytest.mark.parametrize("cfg,align", [("higgs", 32), ("airline", 0), ("tiny", 128)])
+def test_transpose_symbols_parity(ctx, G, cfg, align):
+    X, _ = W.generate(cfg, 0, 2000 if cfg == "tiny" else 30_001)
+    qm, v, p, s, bits, words = _qm_from_oracle(G, X, W.CONFIGS[cfg].max_bins, align)
+    ctx.transpose_symbols(qm)
+    np.testing.assert_array_equal(qm.colsym.cpu().numpy(), s.T.astype(np.uint8))
+
+
 # ------------------------------------------------------------------ a3: gradients
 @pytest.mark.parametrize("obj", ["reg:squarederror", "binary:logistic"])
 @pytest.mark.parametrize("P", [15, 30, 7])
@@ -149,10 +157,12 @@ def test_gradients_label_error(ctx, G):
 
 
 # ------------------------------------------------------------------ a4/a6: histograms
+@pytest.mark.parametrize("layout", [1, 2])
 @pytest.mark.parametrize("P", [15, 30])
 @pytest.mark.parametrize("cfg,align,missing", [("higgs", 32, 0.0), ("tiny", 0, 0.05),
                                                ("airline", 128, 0.0), ("yearmsd", 32, 0.01)])
-def test_histogram_parity(ctx, G, P, cfg, align, missing):
+def test_histogram_parity(ctx, G, P, cfg, align, missing, layout):
+    ctx.set_option(ctx.HIST_LAYOUT, layout)
     n = 2000 if cfg == "tiny" else 150_000
     X, y = W.generate(cfg, 0, n, missing=missing)
     qm, v, p, s, bits, words = _qm_from_oracle(G, X, W.CONFIGS[cfg].max_bins, align)
@@ -167,6 +177,7 @@ def test_histogram_parity(ctx, G, P, cfg, align, missing):
         ref = O.node_histogram(words, X.shape[1], bits, align, p, qm.max_bins, q, sel)
         got = ctx.build_histogram(qm, qd, P, None if rows is None else dev(rows.view(np.int32)))
         np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    ctx.set_option(ctx.HIST_LAYOUT, 0)
 
 
 # ------------------------------------------------------------------ a9: EvaluateSplit
@@ -229,15 +240,20 @@ TREE_CASES = [
     # cfg, rows, missing, align, P, rounds, depth override
     ("tiny", 2000, 0.0, 32, 15, 3, None),
     ("tiny", 2000, 0.05, 0, 30, 3, 5),
+    ("tiny", 2000, 0.05, 32, 15, 2, 4),
     ("yearmsd", 30_000, 0.0, 32, 15, 3, None),
     ("higgs", 100_000, 0.0, 32, 15, 3, None),
+    ("higgs", 100_000, 0.0, 32, 16, 2, None),
     ("higgs", 50_000, 0.02, 128, 30, 2, None),
     ("airline", 120_000, 0.0, 32, 15, 2, None),
+    ("airline", 60_000, 0.03, 0, 12, 2, None),
 ]
 
 
+@pytest.mark.parametrize("layout,colsym", [(0, True), (2, True), (0, False)])
 @pytest.mark.parametrize("cfg,n,missing,align,P,rounds,depth", TREE_CASES)
-def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth):
+def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth, colsym, layout):
+    ctx.set_option(ctx.HIST_LAYOUT, layout)
     c = W.CONFIGS[cfg]
     X, y = W.generate(cfg, 0, n, missing=missing)
     D = c.max_depth if depth is None else depth
@@ -246,7 +262,7 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
                    row_align_bits=align, **kw)
     gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=D,
                    grad_bits=P, row_align_bits=align, base_margin=ob.base_margin, eta=0.3,
-                   reg_lambda=1.0, gamma=0.0, min_child_weight=1.0)
+                   reg_lambda=1.0, gamma=0.0, min_child_weight=1.0, colsym=colsym)
     np.testing.assert_array_equal(u32(gb.qm.packed), ob.words)
     for r in range(rounds):
         ot = ob.round()
@@ -259,6 +275,7 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
     Xt, _ = W.generate(cfg, n, n + 5000, n_rows=max(n + 5000, c.n_rows))
     np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
     np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy(), ob.predict(Xt))
+    ctx.set_option(ctx.HIST_LAYOUT, 0)
 
 
 def test_max_depth_zero_and_one(ctx, G):
