@@ -88,8 +88,10 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
 /* Tuning options (do not change results, only which kernels compute them).
  * GBM_OPT_HIST_LAYOUT: shared-memory histogram layout of BuildPartialHistograms --
  *   0 auto (= compact), 1 compact (random bins, bank conflicts), 2 bank-column (feature per
- *   lane, conflict-free; falls back to compact when the bins do not fit). */
-enum { GBM_OPT_HIST_LAYOUT = 1 };
+ *   lane, conflict-free; falls back to compact when the bins do not fit).
+ * GBM_OPT_CARRY_GRADIENTS: 0 (default) level passes gather qpair by row; 1 the row-index
+ *   entries of every level carry the row's gradient pair (grad_bits <= 15; 8-byte entries). */
+enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

@@ -273,6 +273,7 @@ class Context:
                 for i in range(n.value)}
 
     HIST_LAYOUT = 1
+    CARRY_GRADIENTS = 2
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

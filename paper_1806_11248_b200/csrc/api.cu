@@ -89,7 +89,7 @@ int ctx_enter(gbm_ctx *ctx) {
 }
 
 int allreduce_i64(gbm_ctx *ctx, long long *buf, size_t count, cudaStream_t s) {
-    if (!ctx->comm || ctx->nranks == 1 || count == 0) return GBM_OK;
+    if (!ctx->comm || count == 0) return GBM_OK;
     GBM_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, ctx->comm, s));
     return GBM_OK;
 }
@@ -240,6 +240,10 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
     if (option == GBM_OPT_HIST_LAYOUT) {
         if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 column");
         ctx->hist_layout = (int)value;
+        return GBM_OK;
+    }
+    if (option == GBM_OPT_CARRY_GRADIENTS) {
+        ctx->carry_gradients = value != 0;
         return GBM_OK;
     }
     return fail(GBM_E_ARG, "gbm_set_option: unknown option");

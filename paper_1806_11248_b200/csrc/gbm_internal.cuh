@@ -104,6 +104,7 @@ struct gbm_ctx {
     gbm::Prof prof;                // optional event timing (gbm_profile_*)
     long long launches = 0;        // kernel launches issued by this context
     int hist_layout = 0;           // GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 bank-column
+    int carry_gradients = 0;       // GBM_OPT_CARRY_GRADIENTS
 };
 
 namespace gbm {
@@ -189,9 +190,16 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
-// (double)int64 rounded to nearest even, then an exact power-of-two scale (2^-s)
+// exact 2^e as a double, -1022 <= e <= 1023
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+// x * 2^e with one correct rounding (== ldexp): a multiply by an exact power of two when 2^e is
+// a normal double (the product is then exact or rounded once), scalbn otherwise
+__device__ __forceinline__ double ldexp_exact(double x, int e) {
+    return (e >= -1022 && e <= 1023) ? __dmul_rn(x, pow2i(e)) : scalbn(x, e);
+}
+// (double)int64 rounded to nearest even, then the power-of-two scale 2^-s
 __device__ __forceinline__ double fixed_to_double(long long v, int s) {
-    return scalbn(__ll2double_rn(v), -s);
+    return ldexp_exact(__ll2double_rn(v), -s);
 }
 
 __host__ __device__ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }

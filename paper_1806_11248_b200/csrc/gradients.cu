@@ -4,6 +4,8 @@
 // Bit-exactness (R19-R21): the sigmoid goes through det_exp, which uses only correctly rounded
 // IEEE +,-,*,/, fma and an exact power-of-two scale, and every fp64 op is an explicitly rounded
 // intrinsic (no contraction).  All three kernels are plain streaming kernels: HBM-bound.
+#include <algorithm>
+
 #include "gbm_internal.cuh"
 
 namespace gbm {
@@ -23,7 +25,7 @@ __device__ __forceinline__ double det_exp(double t) {
     double p = DE_C[13];
 #pragma unroll
     for (int i = 12; i >= 0; --i) p = fma(p, r, DE_C[i]);
-    return scalbn(p, (int)k);
+    return ldexp_exact(p, (int)k);
 }
 
 __device__ __forceinline__ double sigmoid(double x) {
@@ -35,32 +37,40 @@ __device__ __forceinline__ double sigmoid(double x) {
     return ddiv(e, dadd(1.0, e));
 }
 
-// Eq. 1-2 (logistic) / squared error; returns false on a label-domain violation
-__device__ __forceinline__ bool grad_hess(int obj, double m, float yl, double &g, double &h) {
-    double y = (double)yl;
+// Eq. 1-2 (logistic, from s = sigmoid(margin)) / squared error
+__device__ __forceinline__ void grad_hess_s(int obj, double m_or_s, float yl, double &g, double &h) {
+    const double y = (double)yl;
     if (obj == GBM_SQUARED_ERROR) {
-        g = dsub(m, y);
+        g = dsub(m_or_s, y);
         h = 1.0;
-        return true;
+        return;
     }
-    double s = sigmoid(m);
+    const double s = m_or_s;
     g = dsub(s, y);
     h = dmul(s, dsub(1.0, s));
-    return yl == 0.0f || yl == 1.0f;
 }
 
 constexpr int G_THREADS = 256;
 
+// pass 1: per-row (g, h), the block maxima of |g|, |h|; for the logistic objective the
+// sigmoid of each row is kept (sig) so that pass 2 does not evaluate det_exp again
 __global__ void __launch_bounds__(G_THREADS) grad_max_kernel(int obj, const double *__restrict__ margin,
                                                              const float *__restrict__ label, long long n,
                                                              unsigned long long *__restrict__ maxbits,
-                                                             uint32_t *dev_err) {
+                                                             double *__restrict__ sig, uint32_t *dev_err) {
     double mg = 0.0, mh = 0.0;
     bool bad = false;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
+        const float yl = __ldg(label + i);
+        double v = __ldg(margin + i);
+        if (obj == GBM_LOGISTIC) {
+            v = sigmoid(v);
+            sig[i] = v;
+            bad |= !(yl == 0.0f || yl == 1.0f);
+        }
         double g, h;
-        bad |= !grad_hess(obj, __ldg(margin + i), __ldg(label + i), g, h);
+        grad_hess_s(obj, v, yl, g, h);
         mg = fmax(mg, fabs(g));
         mh = fmax(mh, fabs(h));
     }
@@ -96,6 +106,7 @@ __device__ __forceinline__ int scale_of(unsigned long long bits, int P) {
 __global__ void __launch_bounds__(G_THREADS) grad_quant_kernel(int obj, int P, const double *__restrict__ margin,
                                                                const float *__restrict__ label, long long n,
                                                                const unsigned long long *__restrict__ maxbits,
+                                                               const double *__restrict__ sig,
                                                                int2 *__restrict__ qpair, int32_t *__restrict__ scale) {
     const int sg = scale_of(maxbits[0], P), sh = scale_of(maxbits[1], P);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -105,8 +116,8 @@ __global__ void __launch_bounds__(G_THREADS) grad_quant_kernel(int obj, int P, c
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         double g, h;
-        grad_hess(obj, __ldg(margin + i), __ldg(label + i), g, h);
-        qpair[i] = make_int2(__double2int_rn(scalbn(g, sg)), __double2int_rn(scalbn(h, sh)));
+        grad_hess_s(obj, obj == GBM_LOGISTIC ? __ldg(sig + i) : __ldg(margin + i), __ldg(label + i), g, h);
+        qpair[i] = make_int2(__double2int_rn(ldexp_exact(g, sg)), __double2int_rn(ldexp_exact(h, sh)));
     }
 }
 
@@ -163,21 +174,23 @@ int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const doub
     GBM_REQUIRE((margin_d && label_d && qpair_d) || n_rows == 0, GBM_E_ARG, "gbm_gradients: null pointer");
     GBM_REQUIRE(scale_d, GBM_E_ARG, "gbm_gradients: null scale");
     cudaStream_t s = (cudaStream_t)stream;
-    GBM_TRY(ctx->arena.reserve(64));
+    const bool lg = objective == GBM_LOGISTIC;
+    GBM_TRY(ctx->arena.reserve(512 + (lg ? (size_t)n_rows * 8 : 0)));
     unsigned long long *maxbits = ctx->arena.take<unsigned long long>(2);
+    double *sig = lg ? ctx->arena.take<double>((size_t)std::max<int64_t>(n_rows, 1)) : nullptr;
     GBM_CUDA(cudaMemsetAsync(maxbits, 0, 16, s));
     int grid = grid_for(n_rows, G_THREADS, ctx->sm_count);
     if (n_rows > 0) {
         ProfScope ps(ctx, PC_GRAD_MAX, s, (double)n_rows * 12);
-        grad_max_kernel<<<grid, G_THREADS, 0, s>>>(objective, margin_d, label_d, n_rows, maxbits, ctx->dev_err);
+        grad_max_kernel<<<grid, G_THREADS, 0, s>>>(objective, margin_d, label_d, n_rows, maxbits, sig, ctx->dev_err);
     }
-    if (ctx->comm && ctx->nranks > 1) {  // C1: global max of |g|, |h| (exact, order-free)
+    if (ctx->comm) {  // C1: global max of |g|, |h| (exact, order-free)
         ProfScope ps(ctx, PC_ALLREDUCE, s, 16.0);
         GBM_NCCL(ncclAllReduce(maxbits, maxbits, 2, ncclUint64, ncclMax, ctx->comm, s));
     }
     {
         ProfScope ps(ctx, PC_GRAD_QUANT, s, (double)n_rows * 20);
-        grad_quant_kernel<<<grid, G_THREADS, 0, s>>>(objective, grad_bits, margin_d, label_d, n_rows, maxbits,
+        grad_quant_kernel<<<grid, G_THREADS, 0, s>>>(objective, grad_bits, margin_d, label_d, n_rows, maxbits, sig,
                                                      reinterpret_cast<int2 *>(qpair_d), scale_d);
     }
     GBM_CUDA(cudaGetLastError());

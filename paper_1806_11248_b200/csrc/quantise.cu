@@ -467,7 +467,7 @@ int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t 
     long long n_total = n_rows, n_max = n_rows;
     const float *Xg = X_d;
     float *gathered = nullptr;
-    if (ctx->comm && ctx->nranks > 1) {
+    if (ctx->comm) {
         long long *tmp;
         GBM_CUDA(cudaMallocAsync((void **)&tmp, 2 * sizeof(long long), s));
         long long h2[2] = {n_rows, n_rows};

@@ -586,6 +586,22 @@ struct ColGroup {
     int f_lo, f_hi;  // features [f_lo, f_hi), Fg <= 32
 };
 
+// byte symbols: every feature has <= 256 bins, the channel stride is the constant 256*32 words
+constexpr int COLB_STRIDE = 256 * 32;
+constexpr int COLB_UR = 4;   // rows in flight per lane in the byte column kernels (16 measured slower)
+template <bool WIDE>
+__device__ __forceinline__ void col_add_b(int *hs, int word, int2 q) {
+    if (WIDE) {
+        atomicAdd(hs + word, q.x & 0x7fff);
+        atomicAdd(hs + COLB_STRIDE + word, q.y & 0x7fff);
+        atomicAdd(hs + 2 * COLB_STRIDE + word, q.x >> 15);
+        atomicAdd(hs + 3 * COLB_STRIDE + word, q.y >> 15);
+    } else {
+        atomicAdd(hs + word, q.x);
+        atomicAdd(hs + COLB_STRIDE + word, q.y);
+    }
+}
+
 template <bool WIDE>
 __device__ __forceinline__ void col_add(int *hs, int cstride, int word, int2 q) {
     if (WIDE) {
@@ -653,7 +669,7 @@ struct ColRangeArgs {
     int cstride;                 // words per channel = rows * 32
 };
 
-template <bool WIDE>
+template <bool WIDE, bool BYTE>
 __global__ void __launch_bounds__(H_THREADS) hist_col_range_kernel(ColRangeArgs a) {
     extern __shared__ int smem[];
     __shared__ long long s_red[2 * H_THREADS / 32];
@@ -673,6 +689,9 @@ __global__ void __launch_bounds__(H_THREADS) hist_col_range_kernel(ColRangeArgs 
         const bool tot = a.totals && g == 0 && L.active && (lane % L.Fg) == 0;
         long long tg = 0, th = 0;
         const long long step = (long long)NW * L.R;
+        const uint8_t *Pb = reinterpret_cast<const uint8_t *>(qm.P) + (L.bitoff >> 3);
+        const unsigned sb = (unsigned)(qm.stride >> 3);  // bytes per row (BYTE)
+        const bool chk = qm.B < 256;
         for (long long r0 = start + (long long)wid * L.R + L.copy; r0 < end; r0 += 4 * step) {
             uint32_t sym[4];
             int2 q[4];
@@ -682,12 +701,17 @@ __global__ void __launch_bounds__(H_THREADS) hist_col_range_kernel(ColRangeArgs 
                 const long long r = r0 + u * step;
                 ok[u] = L.active && r < end;
                 const uint32_t row = ok[u] ? (a.ridx ? __ldg(a.ridx + r) : (uint32_t)r) : 0u;
-                sym[u] = ok[u] ? get_bits(qm.P, (long long)row * qm.stride + L.bitoff, qm.bits) : 0u;
+                if (BYTE) sym[u] = ok[u] ? __ldg(Pb + (size_t)row * sb) : 0u;
+                else sym[u] = ok[u] ? get_bits(qm.P, (long long)row * qm.stride + L.bitoff, qm.bits) : 0u;
                 q[u] = ok[u] ? __ldg(a.qpair + row) : make_int2(0, 0);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                if (ok[u] && (int)sym[u] != qm.B) col_add<WIDE>(smem, a.cstride, (int)sym[u] * 32 + lane, q[u]);
+                if (BYTE) {
+                    if (ok[u] && (!chk || (int)sym[u] != qm.B)) col_add_b<WIDE>(smem, (int)(sym[u] << 5) + lane, q[u]);
+                } else if (ok[u] && (int)sym[u] != qm.B) {
+                    col_add<WIDE>(smem, a.cstride, (int)sym[u] * 32 + lane, q[u]);
+                }
                 if (tot && ok[u]) {
                     tg += q[u].x;
                     th += q[u].y;
@@ -699,6 +723,75 @@ __global__ void __launch_bounds__(H_THREADS) hist_col_range_kernel(ColRangeArgs 
         col_flush<WIDE>(smem, a.cstride, cg, a.cut_ptr, a.hist);
         __syncthreads();
     }
+}
+
+// Lean byte-symbol column kernel (bits == 8): branch-free inner loop.  Lanes beyond R*Fg write
+// into columns the flush never reads, the sentinel symbol (B < 256) lands in a bin >= n_bins(f)
+// of its own column (never flushed), and the ragged tail is masked by a zero gradient pair, so
+// every ATOMS is unconditional and conflict-free.  Root totals come from sum_qpair_kernel.
+template <bool WIDE, bool IDENT>
+__global__ void __launch_bounds__(H_THREADS) hist_colb_range_kernel(ColRangeArgs a) {
+    extern __shared__ int smem[];
+    const QM &qm = a.qm;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = H_THREADS / 32;
+    const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
+    const unsigned sb = (unsigned)(qm.stride >> 3);  // bytes per row
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int g = it % a.n_groups;
+        const long long start = (long long)(it / a.n_groups) * a.chunk;
+        const long long end = min(a.n_sel, start + a.chunk);
+        const ColGroup cg = a.groups[g];
+        for (int i = threadIdx.x; i < (WIDE ? 4 : 2) * COLB_STRIDE; i += H_THREADS) smem[i] = 0;
+        if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)(end - start));
+        __syncthreads();
+        const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
+        const int copy = min(lane / Fg, R - 1);
+        const uint8_t *Pf = reinterpret_cast<const uint8_t *>(qm.P) + (cg.f_lo + lane % Fg);
+        const int step = NW * R;
+        const long long last = end - 1;
+        // COLB_UR rows in flight per lane: each load moves one row's byte, so memory-level
+        // parallelism must come from many independent rows (Little's law)
+        for (long long r0 = start + (long long)wid * R + copy; r0 < end; r0 += COLB_UR * step) {
+            uint32_t row[COLB_UR];
+            bool ok[COLB_UR];
+#pragma unroll
+            for (int u = 0; u < COLB_UR; ++u) {
+                const long long r = r0 + u * step;
+                ok[u] = r < end;
+                const long long rc = ok[u] ? r : last;
+                row[u] = IDENT ? (uint32_t)rc : __ldg(a.ridx + rc);
+            }
+            uint32_t sym[COLB_UR];
+            int2 q[COLB_UR];
+#pragma unroll
+            for (int u = 0; u < COLB_UR; ++u) {
+                sym[u] = __ldg(Pf + (size_t)row[u] * sb);
+                q[u] = __ldg(a.qpair + row[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < COLB_UR; ++u) {
+                const int2 qq = ok[u] ? q[u] : make_int2(0, 0);
+                col_add_b<WIDE>(smem, (int)(sym[u] << 5) + lane, qq);
+            }
+        }
+        __syncthreads();
+        col_flush<WIDE>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist);
+        __syncthreads();
+    }
+}
+
+// root totals T = sum over rows of (q_g, q_h) (InitRoot), for the lean byte kernel
+__global__ void __launch_bounds__(256) sum_qpair_kernel(const int2 *__restrict__ q, long long n,
+                                                        unsigned long long *__restrict__ out) {
+    __shared__ long long red[2 * 256 / 32];
+    long long tg = 0, th = 0;
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+        const int2 v = __ldg(q + i);
+        tg += v.x;
+        th += v.y;
+    }
+    block_totals(tg, th, red, out);
 }
 
 struct ColFusedArgs {
@@ -723,7 +816,7 @@ struct ColFusedArgs {
     int bits_parent_row, bits_built_row;
 };
 
-template <bool WIDE, bool CARRY>
+template <bool WIDE, bool CARRY, bool BYTE>
 __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a) {
     using E = typename EntryOf<CARRY>::T;
     extern __shared__ int smem[];
@@ -758,6 +851,9 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
         const ColLane L = col_lane(qm, cg);
         const bool build_left = nd.build_left != 0;
         unsigned long long bits_acc = 0;
+        const uint8_t *Pb = reinterpret_cast<const uint8_t *>(qm.P) + (L.bitoff >> 3);
+        const unsigned sb = (unsigned)(qm.stride >> 3);
+        const bool chk = qm.B < 256;
         for (int t = t0; t < t1; ++t) {
             const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
             // (A) partition flags for the warp's 128 rows (lane = row)
@@ -799,6 +895,26 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
             }
             __syncwarp();
             // (B) histogram of the listed rows, lane = (copy, feature column)
+            if (BYTE) {  // branch-free (see hist_colb_range_kernel)
+                const uint8_t *Pf = reinterpret_cast<const uint8_t *>(qm.P) + (cg.f_lo + lane % L.Fg);
+                const int cp2 = min(L.copy, L.R - 1);
+                for (int i0 = cp2; i0 < nbuild; i0 += COLB_UR * L.R) {
+                    uint32_t sym[COLB_UR];
+                    int2 q[COLB_UR];
+                    bool ok[COLB_UR];
+#pragma unroll
+                    for (int u = 0; u < COLB_UR; ++u) {
+                        const int i = i0 + u * L.R;
+                        ok[u] = i < nbuild;
+                        const E e = wrows[ok[u] ? i : nbuild - 1];
+                        sym[u] = __ldg(Pf + (size_t)row_of(e) * sb);
+                        q[u] = entry_q(e, a.qpair);
+                    }
+#pragma unroll
+                    for (int u = 0; u < COLB_UR; ++u)
+                        col_add_b<WIDE>(smem, (int)(sym[u] << 5) + lane, ok[u] ? q[u] : make_int2(0, 0));
+                }
+            } else
             for (int i0 = L.copy; i0 < nbuild; i0 += 4 * L.R) {
                 uint32_t sym[4];
                 int2 q[4];
@@ -809,12 +925,19 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
                     ok[u] = L.active && i < nbuild;
                     const E e = ok[u] ? wrows[i] : E{};
                     const uint32_t r = row_of(e);
-                    sym[u] = ok[u] ? get_bits(qm.P, (long long)r * qm.stride + L.bitoff, qm.bits) : 0u;
+                    if (BYTE) sym[u] = ok[u] ? __ldg(Pb + (size_t)r * sb) : 0u;
+                    else sym[u] = ok[u] ? get_bits(qm.P, (long long)r * qm.stride + L.bitoff, qm.bits) : 0u;
                     q[u] = ok[u] ? entry_q(e, a.qpair) : make_int2(0, 0);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (ok[u] && (int)sym[u] != qm.B) col_add<WIDE>(smem, a.cstride, (int)sym[u] * 32 + lane, q[u]);
+                for (int u = 0; u < 4; ++u) {
+                    if (BYTE) {
+                        if (ok[u] && (!chk || (int)sym[u] != qm.B))
+                            col_add_b<WIDE>(smem, (int)(sym[u] << 5) + lane, q[u]);
+                    } else if (ok[u] && (int)sym[u] != qm.B) {
+                        col_add<WIDE>(smem, a.cstride, (int)sym[u] * 32 + lane, q[u]);
+                    }
+                }
             }
             __syncwarp();
         }
@@ -833,7 +956,8 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const in
                                                                  const int32_t *__restrict__ feature,
                                                                  const int32_t *__restrict__ bin,
                                                                  const int8_t *__restrict__ dl, int n_internal,
-                                                                 long long n, int32_t *__restrict__ row_leaf) {
+                                                                 int depth, long long n,
+                                                                 int32_t *__restrict__ row_leaf) {
     extern __shared__ int s_tree[];  // [n_internal] packed: feature | dl << 20 | split << 21, bin
     int *s_f = s_tree, *s_b = s_tree + n_internal;
     for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
@@ -841,17 +965,32 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const in
         s_b[k] = bin[k];
     }
     __syncthreads();
-    for (long long i = blockIdx.x * (long long)WALK_THREADS + threadIdx.x; i < n;
-         i += (long long)gridDim.x * WALK_THREADS) {
-        int k = 0;
-        while (k < n_internal) {
-            const int fk = s_f[k];
-            if (!(fk & (1 << 21))) break;
-            const uint32_t sym = split_symbol(qm, i, fk & 0xfffff);
-            const bool left = (int)sym == qm.B ? ((fk >> 20) & 1) : ((int)sym <= s_b[k]);
-            k = left ? 2 * k + 1 : 2 * k + 2;
+    const long long stride = (long long)gridDim.x * WALK_THREADS;
+    for (long long i0 = blockIdx.x * (long long)WALK_THREADS + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        int k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k[u] = 0;
+        for (int d = 0; d < depth; ++d) {  // four independent walks in lockstep
+            uint32_t sym[4];
+            int fk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long i = i0 + u * stride;
+                fk[u] = (i < n && k[u] < n_internal) ? s_f[k[u]] : 0;
+                sym[u] = (fk[u] & (1 << 21)) ? split_symbol(qm, i, fk[u] & 0xfffff) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!(fk[u] & (1 << 21))) continue;
+                const bool left = (int)sym[u] == qm.B ? ((fk[u] >> 20) & 1) : ((int)sym[u] <= s_b[k[u]]);
+                k[u] = left ? 2 * k[u] + 1 : 2 * k[u] + 2;
+            }
         }
-        row_leaf[i] = k;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n) row_leaf[i] = k[u];
+        }
     }
 }
 
@@ -1008,70 +1147,112 @@ struct NodeHist {
 
 // Best candidate of feature f of one node, computed by one warp (valid in every lane).
 // Op order of every fp64 step = R8 (oracle_evaluate_split).
+// One candidate (R8 op order); updates best.
+__device__ __forceinline__ void eval_candidate(long long Pg, long long Ph, long long Mg, long long Mh, long long Tg,
+                                               long long Th, int sg, int sh, double e, const EvalParams &p,
+                                               long long bin_global, FeatBest &best) {
+#pragma unroll
+    for (int dli = 0; dli < 2; ++dli) {
+        const bool dl = dli == 0;  // true first (R9)
+        const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
+        const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
+        const double GR = fixed_to_double(Tg - Lg, sg), HR = fixed_to_double(Th - Lh, sh);
+        if (!(HL >= p.mcw && HR >= p.mcw && dadd(HL, p.lambda) > 0.0 && dadd(HR, p.lambda) > 0.0)) continue;
+        double aa = dmul(GL, GL);
+        aa = ddiv(aa, dadd(HL, p.lambda));
+        double cc = dmul(GR, GR);
+        cc = ddiv(cc, dadd(HR, p.lambda));
+        double d = dadd(aa, cc);
+        d = dsub(d, e);
+        d = dmul(0.5, d);
+        const double gain = dsub(d, p.gamma);
+        const long long idx = bin_global * 2 + dli;
+        if (better(gain, idx, best.gain, best.idx)) {
+            best.gain = gain;
+            best.idx = idx;
+            best.Lg = Lg;
+            best.Lh = Lh;
+        }
+    }
+}
+
+// Best candidate of feature f of one node, computed by one warp (valid in every lane).
+// Register-blocked: lane owns KB consecutive bins of each 32*KB-bin chunk, so all histogram
+// loads of a chunk are in flight together; the prefix is a per-lane serial scan plus one warp
+// scan of the lane totals.
+constexpr int KB = 8;
 __device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long Tg, long long Th, int sg, int sh,
                                  double e, const EvalParams &p) {
     const int lane = threadIdx.x & 31;
-    long long sgs = 0, shs = 0;
-    for (int b = lane; b < nbf; b += 32) {
-        long long g, h;
-        src.get(b0 + b, g, h);
-        if (src.store) {
-            src.store[2 * (b0 + b)] = g;
-            src.store[2 * (b0 + b) + 1] = h;
+    constexpr int CH = 32 * KB;
+    long long Mg, Mh;
+    long long vg[KB], vh[KB];
+    auto load_chunk = [&](int c) {
+#pragma unroll
+        for (int i = 0; i < KB; ++i) {
+            const int b = c + lane * KB + i;
+            vg[i] = vh[i] = 0;
+            if (b < nbf) {
+                src.get(b0 + b, vg[i], vh[i]);
+                if (src.store) {
+                    src.store[2 * (b0 + b)] = vg[i];
+                    src.store[2 * (b0 + b) + 1] = vh[i];
+                }
+            }
         }
-        sgs += g;
-        shs += h;
+    };
+    auto warp_sum = [&](long long x) {
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        return x;
+    };
+    if (nbf <= CH) {
+        load_chunk(0);
+    } else {  // wide features: totals first
+        long long sg2 = 0, sh2 = 0;
+        for (int b = lane; b < nbf; b += 32) {
+            long long g, h;
+            src.get(b0 + b, g, h);
+            sg2 += g;
+            sh2 += h;
+        }
+        Mg = Tg - warp_sum(sg2);
+        Mh = Th - warp_sum(sh2);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        sgs += __shfl_xor_sync(0xffffffffu, sgs, o);
-        shs += __shfl_xor_sync(0xffffffffu, shs, o);
-    }
-    const long long Mg = Tg - sgs, Mh = Th - shs;  // missing mass (R7)
     FeatBest best;
     best.gain = 0.0;
     best.idx = LLONG_MAX;
     best.Lg = best.Lh = 0;
-    long long cg = 0, ch = 0;
-    for (int c = 0; c < nbf; c += 32) {
-        const int b = c + lane;
-        long long g = 0, h = 0;
-        if (b < nbf) src.get(b0 + b, g, h);
-        long long pg = g, ph = h;
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long yg = __shfl_up_sync(0xffffffffu, pg, o), yh = __shfl_up_sync(0xffffffffu, ph, o);
-            if (lane >= o) {
-                pg += yg;
-                ph += yh;
-            }
-        }
-        const long long Pg = cg + pg, Ph = ch + ph;
-        cg += __shfl_sync(0xffffffffu, pg, 31);
-        ch += __shfl_sync(0xffffffffu, ph, 31);
-        if (b < nbf) {
+    long long cg = 0, ch = 0;  // prefix of earlier chunks
+    for (int c = 0; c < nbf; c += CH) {
+        if (c > 0 || nbf > CH) load_chunk(c);
+        long long lg = 0, lh = 0;
 #pragma unroll
-            for (int dli = 0; dli < 2; ++dli) {
-                const bool dl = dli == 0;  // true first (R9)
-                const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
-                const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
-                const double GR = fixed_to_double(Tg - Lg, sg), HR = fixed_to_double(Th - Lh, sh);
-                if (!(HL >= p.mcw && HR >= p.mcw && dadd(HL, p.lambda) > 0.0 && dadd(HR, p.lambda) > 0.0)) continue;
-                double aa = dmul(GL, GL);
-                aa = ddiv(aa, dadd(HL, p.lambda));
-                double cc = dmul(GR, GR);
-                cc = ddiv(cc, dadd(HR, p.lambda));
-                double d = dadd(aa, cc);
-                d = dsub(d, e);
-                d = dmul(0.5, d);
-                const double gain = dsub(d, p.gamma);
-                const long long idx = (long long)(b0 + b) * 2 + dli;
-                if (better(gain, idx, best.gain, best.idx)) {
-                    best.gain = gain;
-                    best.idx = idx;
-                    best.Lg = Lg;
-                    best.Lh = Lh;
-                }
+        for (int i = 0; i < KB; ++i) {
+            lg += vg[i];
+            lh += vh[i];
+        }
+        long long xg = lg, xh = lh;  // inclusive warp scan of lane totals
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long yg = __shfl_up_sync(0xffffffffu, xg, o), yh = __shfl_up_sync(0xffffffffu, xh, o);
+            if (lane >= o) {
+                xg += yg;
+                xh += yh;
             }
         }
+        if (nbf <= CH) {  // single chunk: the feature sum is the scan's total
+            Mg = Tg - __shfl_sync(0xffffffffu, xg, 31);
+            Mh = Th - __shfl_sync(0xffffffffu, xh, 31);
+        }
+        long long Pg = cg + xg - lg, Ph = ch + xh - lh;
+#pragma unroll
+        for (int i = 0; i < KB; ++i) {
+            const int b = c + lane * KB + i;
+            Pg += vg[i];
+            Ph += vh[i];
+            if (b < nbf) eval_candidate(Pg, Ph, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), best);
+        }
+        cg += __shfl_sync(0xffffffffu, xg, 31);
+        ch += __shfl_sync(0xffffffffu, xh, 31);
     }
     for (int o = 16; o > 0; o >>= 1) {
         const double og = __shfl_xor_sync(0xffffffffu, best.gain, o);
@@ -1375,17 +1556,23 @@ static int setup_kernels(gbm_ctx *ctx, HistPlan &hp) {
              : (hp.byte_path ? (hp.sent ? F<false, true, true>(__VA_ARGS__) : F<false, true, false>(__VA_ARGS__)) \
                              : F<false, false, false>(__VA_ARGS__)))
 
-template <bool W>
+template <bool W, bool B>
 static int setup_col(gbm_ctx *ctx, HistPlan &hp) {
-    GBM_CUDA(cudaFuncSetAttribute(hist_col_range_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
-    GBM_CUDA(cudaFuncSetAttribute(part_hist_col_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GBM_CUDA(cudaFuncSetAttribute(hist_col_range_kernel<W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+    if constexpr (B) {
+        GBM_CUDA(cudaFuncSetAttribute(hist_colb_range_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      hp.smem_bytes));
+        GBM_CUDA(cudaFuncSetAttribute(hist_colb_range_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      hp.smem_bytes));
+    }
+    GBM_CUDA(cudaFuncSetAttribute(part_hist_col_kernel<W, false, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   hp.smem_bytes));
     if constexpr (!W)
-        GBM_CUDA(cudaFuncSetAttribute(part_hist_col_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GBM_CUDA(cudaFuncSetAttribute(part_hist_col_kernel<W, true, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       hp.smem_bytes));
     int o1 = 0, o2 = 0;
-    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_col_range_kernel<W>, H_THREADS, hp.smem_bytes));
-    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_col_kernel<W, !W>, H_THREADS, hp.smem_bytes));
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_col_range_kernel<W, B>, H_THREADS, hp.smem_bytes));
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_col_kernel<W, !W, B>, H_THREADS, hp.smem_bytes));
     if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "column histogram kernels cannot be resident");
     hp.blocks_range = o1 * ctx->sm_count;
     hp.blocks_fused = o2 * ctx->sm_count;
@@ -1396,16 +1583,18 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
                      HistPlan &hp, int grad_bits = 30, bool allow_col = true) {
     const int *cp = q->cut_ptr_h;
     hp.wide = wide;
-    hp.carry = !wide && grad_bits <= 15;
+    hp.carry = !wide && grad_bits <= 15 && ctx->carry_gradients;
     // ---- bank-column plan: every feature's bins fit one column of the smem histogram
     {
         const int channels = wide ? 4 : 2;
         const int budget = (int)std::min<size_t>(ctx->smem_optin - 20 * 1024, 200 * 1024);
         int max_nb = 1;
         for (int f = 0; f < qm.F; ++f) max_nb = std::max(max_nb, cp[f + 1] - cp[f]);
-        const int rows = (max_nb + 7) / 8 * 8;
+        const bool byte_sym = q->bits == 8;
+        const int rows = byte_sym ? 256 : (max_nb + 7) / 8 * 8;
         if (allow_col && channels * rows * 32 * 4 <= budget) {
             hp.col = true;
+            hp.byte_path = byte_sym;
             hp.cstride = rows * 32;
             hp.smem_bytes = channels * hp.cstride * 4;
             hp.cgroups.clear();
@@ -1416,7 +1605,9 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
                 c.f_hi = (int)((long long)qm.F * (g + 1) / ng);
                 hp.cgroups.push_back(c);
             }
-            GBM_TRY(wide ? setup_col<true>(ctx, hp) : setup_col<false>(ctx, hp));
+            int rc = wide ? (byte_sym ? setup_col<true, true>(ctx, hp) : setup_col<true, false>(ctx, hp))
+                          : (byte_sym ? setup_col<false, true>(ctx, hp) : setup_col<false, false>(ctx, hp));
+            GBM_TRY(rc);
             const long long G = (long long)hp.cgroups.size();
             long long per = (rows_hint + 2ll * hp.blocks_range - 1) / (2ll * hp.blocks_range) * G;
             hp.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per));
@@ -1479,6 +1670,43 @@ static int launch_fused(gbm_ctx *ctx, const HistPlan &hp, FusedArgs a, cudaStrea
     }
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
+}
+
+static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int grid, cudaStream_t s) {
+    const int sm = hp.smem_bytes;
+    if (hp.byte_path) {
+        if (ca.totals) sum_qpair_kernel<<<std::min<long long>((ca.n_sel + 255) / 256, 148 * 8), 256, 0, s>>>(
+            ca.qpair, ca.n_sel, ca.totals);
+        if (hp.wide) {
+            if (ca.ridx) hist_colb_range_kernel<true, false><<<grid, H_THREADS, sm, s>>>(ca);
+            else hist_colb_range_kernel<true, true><<<grid, H_THREADS, sm, s>>>(ca);
+        } else {
+            if (ca.ridx) hist_colb_range_kernel<false, false><<<grid, H_THREADS, sm, s>>>(ca);
+            else hist_colb_range_kernel<false, true><<<grid, H_THREADS, sm, s>>>(ca);
+        }
+        return;
+    }
+    if (hp.wide) {
+        if (hp.byte_path) hist_col_range_kernel<true, true><<<grid, H_THREADS, sm, s>>>(ca);
+        else hist_col_range_kernel<true, false><<<grid, H_THREADS, sm, s>>>(ca);
+    } else {
+        if (hp.byte_path) hist_col_range_kernel<false, true><<<grid, H_THREADS, sm, s>>>(ca);
+        else hist_col_range_kernel<false, false><<<grid, H_THREADS, sm, s>>>(ca);
+    }
+}
+
+static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStream_t s) {
+    const int g = hp.blocks_fused, sm = hp.smem_bytes;
+    if (hp.wide) {
+        if (hp.byte_path) part_hist_col_kernel<true, false, true><<<g, H_THREADS, sm, s>>>(ca);
+        else part_hist_col_kernel<true, false, false><<<g, H_THREADS, sm, s>>>(ca);
+    } else if (hp.carry) {
+        if (hp.byte_path) part_hist_col_kernel<false, true, true><<<g, H_THREADS, sm, s>>>(ca);
+        else part_hist_col_kernel<false, true, false><<<g, H_THREADS, sm, s>>>(ca);
+    } else {
+        if (hp.byte_path) part_hist_col_kernel<false, false, true><<<g, H_THREADS, sm, s>>>(ca);
+        else part_hist_col_kernel<false, false, false><<<g, H_THREADS, sm, s>>>(ca);
+    }
 }
 
 static TreeDev tree_dev(const gbm_tree *t) {
@@ -1557,8 +1785,7 @@ int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair
         ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, (double)q->n_features * q->bits / 8.0 + 8.0 + (rows_d ? 4.0 : 0.0));
         const long long n_items = (n_sel + hp.chunk - 1) / hp.chunk * (long long)hp.cgroups.size();
         const int grid = (int)std::max<long long>(1, std::min<long long>(n_items, hp.blocks_range));
-        if (hp.wide) hist_col_range_kernel<true><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
-        else hist_col_range_kernel<false><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
+        launch_col_range(hp, ca, grid, s);
         GBM_CUDA(cudaGetLastError());
         return GBM_OK;
     }
@@ -1774,8 +2001,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         ProfScope ps(ctx, PC_HIST_ROOT, s, (double)n * (row_bytes + 8.0));
         const long long n_it = (n + hp.chunk - 1) / hp.chunk * (long long)G;
         const int grid = (int)std::max<long long>(1, std::min<long long>(n_it, hp.blocks_range));
-        if (hp.wide) hist_col_range_kernel<true><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
-        else hist_col_range_kernel<false><<<grid, H_THREADS, hp.smem_bytes, s>>>(ca);
+        launch_col_range(hp, ca, grid, s);
         GBM_CUDA(cudaGetLastError());
     } else if (n > 0 && TB > 0) {
         RangeArgs ra = {};
@@ -1850,7 +2076,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
                                                                             (long long)ctx->sm_count * 8));
             if (n > 0)
                 leaf_walk_kernel<<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
-                                                                n_internal, n, row_leaf_d);
+                                                                n_internal, D, n, row_leaf_d);
             GBM_CUDA(cudaGetLastError());
             break;
         }
@@ -1894,9 +2120,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
                 ca.rows_ctr = fa.rows_ctr;
                 ca.bits_parent_row = fa.bits_parent_row;
                 ca.bits_built_row = fa.bits_built_row;
-                if (hp.wide) part_hist_col_kernel<true, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(ca);
-                else if (hp.carry) part_hist_col_kernel<false, true><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(ca);
-                else part_hist_col_kernel<false, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(ca);
+                launch_col_fused(hp, ca, s);
                 GBM_CUDA(cudaGetLastError());
             } else {
                 GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));

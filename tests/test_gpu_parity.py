@@ -250,10 +250,12 @@ TREE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("layout,colsym", [(0, True), (2, True), (0, False)])
+@pytest.mark.parametrize("layout,colsym,carry", [(0, True, 0), (2, True, 0), (0, False, 1), (2, False, 1)])
 @pytest.mark.parametrize("cfg,n,missing,align,P,rounds,depth", TREE_CASES)
-def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth, colsym, layout):
+def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth, colsym, layout,
+                                carry):
     ctx.set_option(ctx.HIST_LAYOUT, layout)
+    ctx.set_option(ctx.CARRY_GRADIENTS, carry)
     c = W.CONFIGS[cfg]
     X, y = W.generate(cfg, 0, n, missing=missing)
     D = c.max_depth if depth is None else depth
@@ -276,6 +278,7 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
     np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
     np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy(), ob.predict(Xt))
     ctx.set_option(ctx.HIST_LAYOUT, 0)
+    ctx.set_option(ctx.CARRY_GRADIENTS, 0)
 
 
 def test_max_depth_zero_and_one(ctx, G):
@@ -330,3 +333,24 @@ def test_full_size_round_properties(ctx, G, cfg):
     tid["weight"] = np.arange(cap, dtype=np.float64)
     leaf = O.predict([tid], c.max_depth, 0.0, X[idx]).astype(np.int64)
     np.testing.assert_array_equal(leaf, rl[idx])
+
+
+def test_single_rank_communicator_paths(G):
+    """A 1-rank NCCL communicator: every collective of the path (C3 all-gather in gbm_cuts, C1
+    max in gbm_gradients, C2 histogram sums in gbm_build_tree) runs through NCCL and the model
+    is unchanged (integer sums, exact maxima)."""
+    X, y = W.generate("tiny", missing=0.05)
+    c = G.Context(0)
+    c.comm_init(G.Context.comm_unique_id(), 1, 0)
+    assert G.lib().gbm_comm_info(c.h, None, None) == 0
+    ob = O.Booster(X, y, max_bins=16, objective="reg:squarederror", max_depth=4, eta=0.3)
+    gb = G.Booster(c, dev(X), dev(y), max_bins=16, objective="reg:squarederror", max_depth=4,
+                   eta=0.3, base_margin=ob.base_margin)
+    np.testing.assert_array_equal(u32(gb.qm.packed), ob.words)
+    for _ in range(3):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    h = torch.arange(10, dtype=torch.int64, device="cuda")
+    c.allreduce_histograms(h)
+    assert h.cpu().tolist() == list(range(10))
+    c.close()
