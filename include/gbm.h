@@ -71,7 +71,7 @@ GBM_API int gbm_check(gbm_ctx *ctx, void *stream);
  * Optional CUDA-event timing of every kernel launch the context issues, grouped by kernel
  * (bench.py's per-kernel roofline).  gbm_profile_enable(1) resets and starts recording (it
  * synchronises the device); gbm_profile_read synchronises, fills one entry per kernel
- * category (cap >= 16) and starts a new window.  bytes = the launches' ALGORITHMIC bytes
+ * category (cap >= 32) and starts a new window.  bytes = the launches' ALGORITHMIC bytes
  * (DESIGN.md "Algorithmic bytes"), rows = rows they processed, counted on the device.
  * gbm_launch_count: kernel launches issued by the context since creation. */
 typedef struct {

@@ -48,7 +48,7 @@ int Arena::reserve(size_t bytes) {
 const char *const PROF_NAMES[PC_N] = {
     "grad_max", "grad_quant", "hist_root", "hist_level", "part_count", "part_scan",
     "part_scatter", "part_final", "evaluate", "allreduce", "update_margins", "init_tree",
-    "predict", "cuts", "quantise_compress"};
+    "predict", "cuts", "quantise_compress", "eval_final", "plan"};
 
 static cudaEvent_t pool_event(Prof &p) {
     if (p.pool_used == p.pool.size()) {

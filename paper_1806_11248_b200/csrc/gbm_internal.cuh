@@ -70,7 +70,7 @@ struct Arena {
 enum ProfCat {
     PC_GRAD_MAX = 0, PC_GRAD_QUANT, PC_HIST_ROOT, PC_HIST_LEVEL, PC_PART_COUNT, PC_PART_SCAN,
     PC_PART_SCATTER, PC_PART_FINAL, PC_EVAL, PC_ALLREDUCE, PC_MARGINS, PC_INIT, PC_PREDICT,
-    PC_CUTS, PC_QUANT, PC_N
+    PC_CUTS, PC_QUANT, PC_EVAL_FINAL, PC_PLAN, PC_N
 };
 extern const char *const PROF_NAMES[PC_N];
 

@@ -341,15 +341,15 @@ __device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint3
 // Tile plan of the parents of a level: tile_base[j] (first 2048-row tile of parent j) and
 // run_base[j] (first RUN-tile run); n_items = runs x feature groups.  Work item i of the fused
 // kernel is run i / G, group i % G, resolved on the fly (find_parent over run_base).
-__global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
-                                                    int n_groups, int *__restrict__ tile_base,
-                                                    int *__restrict__ run_base, int *__restrict__ n_items) {
+// Works for any block size that is a multiple of 32 (<= 1024).
+__device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_par, int n_groups,
+                           int *__restrict__ tile_base, int *__restrict__ run_base, int *__restrict__ n_items) {
     __shared__ long long sm32[32];
     __shared__ long long carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int c = 0; c < n_par; c += 1024) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = 0; c < n_par; c += blockDim.x) {
         const int j = c + threadIdx.x;
         long long nt = 0, nr = 0;
         if (j < n_par) {
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ 
         if (lane == 31) sm32[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            long long t = sm32[lane];
+            long long t = lane < nw ? sm32[lane] : 0;
             for (int o = 1; o < 32; o <<= 1) {
                 const long long y = __shfl_up_sync(0xffffffffu, t, o);
                 if (lane >= o) t += y;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ 
             run_base[j] = (int)(ex & 0xffffffff);
         }
         __syncthreads();
-        if (threadIdx.x == 0) carry += sm32[31];
+        if (threadIdx.x == 0) carry += sm32[nw - 1];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
@@ -390,6 +390,12 @@ __global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ 
         run_base[n_par] = (int)(carry & 0xffffffff);
         *n_items = (int)(carry & 0xffffffff) * n_groups;
     }
+}
+
+__global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
+                                                    int n_groups, int *__restrict__ tile_base,
+                                                    int *__restrict__ run_base, int *__restrict__ n_items) {
+    plan_block(nodes, first, n_par, n_groups, tile_base, run_base, n_items);
 }
 
 // ============================================================== fused partition + histogram
@@ -421,7 +427,7 @@ struct FusedArgs {
 // warp's left count into tile_left, the rows of the built child compacted into a warp-private
 // list; (B) the listed rows' words accumulated by the warp (lane -> fixed word of the row).
 template <bool WIDE, bool BYTE, bool SENT, bool CARRY>
-__global__ void __launch_bounds__(H_THREADS) part_hist_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
     using E = typename EntryOf<CARRY>::T;
     extern __shared__ int smem[];
     __shared__ int s_off[2049];
@@ -994,6 +1000,55 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const in
     }
 }
 
+// Row-register variant (rows of W <= 16 whole words, i.e. row_align 32/128 or F*bits % 32 == 0):
+// each thread loads its row's W words once (one memory round trip) and walks the tree on
+// register-resident symbols.
+template <int W>
+__device__ __forceinline__ uint32_t reg_symbol(const uint32_t (&r)[W], int bitpos, int bits) {
+    const int wi = bitpos >> 5, off = bitpos & 31;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        lo = (i == wi) ? r[i] : lo;
+        hi = (i == wi + 1) ? r[i] : hi;
+    }
+    const uint64_t v = ((uint64_t)hi << 32 | lo) >> off;
+    return (uint32_t)v & ((1u << bits) - 1u);
+}
+
+template <int W>
+__global__ void __launch_bounds__(WALK_THREADS) leaf_walk_reg_kernel(QM qm, const int8_t *__restrict__ kind,
+                                                                     const int32_t *__restrict__ feature,
+                                                                     const int32_t *__restrict__ bin,
+                                                                     const int8_t *__restrict__ dl, int n_internal,
+                                                                     int depth, long long n,
+                                                                     int32_t *__restrict__ row_leaf) {
+    extern __shared__ int s_tree[];
+    int *s_f = s_tree, *s_b = s_tree + n_internal;
+    for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
+        s_f[k] = kind[k] == GBM_NODE_SPLIT ? (feature[k] | ((int)dl[k] << 20) | (1 << 21)) : 0;
+        s_b[k] = bin[k];
+    }
+    __syncthreads();
+    const long long sw = qm.stride >> 5;
+    for (long long i = blockIdx.x * (long long)WALK_THREADS + threadIdx.x; i < n;
+         i += (long long)gridDim.x * WALK_THREADS) {
+        uint32_t r[W];
+        const uint32_t *p = qm.P + i * sw;
+#pragma unroll
+        for (int w = 0; w < W; ++w) r[w] = __ldg(p + w);
+        int k = 0;
+        for (int d = 0; d < depth; ++d) {
+            const int fk = s_f[k];
+            if (!(fk & (1 << 21))) break;
+            const uint32_t sym = reg_symbol<W>(r, (fk & 0xfffff) * qm.bits, qm.bits);
+            const bool left = (int)sym == qm.B ? ((fk >> 20) & 1) : ((int)sym <= s_b[k]);
+            k = left ? 2 * k + 1 : 2 * k + 2;
+        }
+        row_leaf[i] = k;
+    }
+}
+
 // ============================================================== scan + scatter
 __device__ __forceinline__ long long block_exscan(long long v, long long *total, long long *sm32) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1151,8 +1206,11 @@ struct NodeHist {
 __device__ __forceinline__ void eval_candidate(long long Pg, long long Ph, long long Mg, long long Mh, long long Tg,
                                                long long Th, int sg, int sh, double e, const EvalParams &p,
                                                long long bin_global, FeatBest &best) {
-#pragma unroll
-    for (int dli = 0; dli < 2; ++dli) {
+    // No missing mass: both default directions give the same (L, R), hence the same gain, and
+    // the dl = true candidate comes first in the canonical order -- evaluating it alone picks
+    // the identical best (R9).
+    const int n_dl = (Mg == 0 && Mh == 0) ? 1 : 2;
+    for (int dli = 0; dli < n_dl; ++dli) {
         const bool dl = dli == 0;  // true first (R9)
         const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
         const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
@@ -1270,6 +1328,10 @@ __device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long
 
 struct EvalArgs {
     int level, first, F, n_nodes;
+    // tree mode: the last eval_final block plans the next level's partition (plan_block)
+    unsigned *done;                 // block counter (reset by the last block), null = no plan
+    int plan_groups;
+    int *tile_base, *run_base, *n_items;
     long long TB;
     const int32_t *cut_ptr;
     const float *cut_values;
@@ -1406,8 +1468,27 @@ __device__ FeatBest reduce_node(const EvalArgs &a, int j) {
     return r;
 }
 
-// tree mode: one block per node of the level
+__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t);
+
+// tree mode: one block per node of the level; the last block to finish plans the next level
 __global__ void __launch_bounds__(E_THREADS) eval_final_kernel(EvalArgs a, TreeDev t) {
+    eval_final_body(a, t);
+    if (!a.done) return;
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // the children of this level are the next level's parents
+    plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.tile_base, a.run_base, a.n_items);
+    if (threadIdx.x == 0) *a.done = 0;
+}
+
+__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t) {
     const int j = blockIdx.x, k = a.first + j;
     NodeHist src;
     long long Tg, Th;
@@ -1709,6 +1790,13 @@ static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStr
     }
 }
 
+template <int W>
+static void launch_walk_reg(int grid, size_t sm, cudaStream_t s, const QM &qm, const TreeDev &t, int n_int, int D,
+                            long long n, int32_t *rl) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(leaf_walk_reg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    leaf_walk_reg_kernel<W><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl);
+}
+
 static TreeDev tree_dev(const gbm_tree *t) {
     TreeDev d;
     d.kind = t->kind;
@@ -1956,7 +2044,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     need += G * std::max(sizeof(Group), sizeof(ColGroup)) + 256;
     need += (slots * hist_unit + hist_unit + 2) * 8 + 512;            // build + root
     need += 2 * slots * hist_unit * 8 + 512;                          // level hists
-    need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 256;
+    need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 512;
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
@@ -1973,6 +2061,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     long long *hist_build = A.take<long long>(slots * hist_unit);
     long long *hist_lvl[2] = {A.take<long long>(slots * hist_unit), A.take<long long>(slots * hist_unit)};
     FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
+    unsigned *done = A.take<unsigned>(1);
 
     if (hp.col) GBM_CUDA(cudaMemcpyAsync(cgroups, hp.cgroups.data(), G * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
     else GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
@@ -2025,17 +2114,26 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         ProfScope ps(ctx, PC_ALLREDUCE, s, (double)(hist_unit + 2) * 8);
         GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
     }
+    GBM_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
     EvalArgs ea = eval_args_base(q, scale_d, prm);
     ea.nodes = nodes;
     ea.hist_root = hist_root;
     ea.hist_build = hist_build;
     ea.fb = fb;
-    {
+    ea.plan_groups = G;
+    ea.tile_base = tile_base;
+    ea.run_base = run_base;
+    ea.n_items = n_items;
+    ea.level = 0;
+    ea.first = 0;
+    ea.n_nodes = 1;
+    ea.done = (1 < D) ? done : nullptr;  // the root's eval plans level 1
+    if (D > 0) {
         ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
-        ea.level = 0;
-        ea.first = 0;
-        ea.n_nodes = 1;
-        if (D > 0) eval_feat_kernel<<<(F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
+        eval_feat_kernel<<<(F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
+    }
+    {
+        ProfScope ps(ctx, PC_EVAL_FINAL, s);
         eval_final_kernel<<<1, E_THREADS, 0, s>>>(ea, t);
         GBM_CUDA(cudaGetLastError());
     }
@@ -2070,19 +2168,27 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             const int n_internal = (1 << D) - 1;
             const size_t sm = (size_t)n_internal * 8;
             ProfScope ps(ctx, PC_PART_FINAL, s, (double)n * (q->bits * D / 8.0 + 4.0));
-            if (sm > 48 * 1024)
-                GBM_CUDA(cudaFuncSetAttribute(leaf_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             const int grid = (int)std::max<long long>(1, std::min<long long>((n + WALK_THREADS - 1) / WALK_THREADS,
                                                                             (long long)ctx->sm_count * 8));
-            if (n > 0)
+            // with the feature-major copy the walk reads one byte per level (coalesced at the top
+            // levels); without it the row's words are loaded once into registers
+            const int W = (qm.stride % 32 == 0) ? (int)(qm.stride / 32) : 0;
+            if (n > 0 && !qm.col && W >= 1 && W <= 16) {
+                switch (W) {
+#define GBM_WALK(w) case w: launch_walk_reg<w>(grid, sm, s, qm, t, n_internal, D, n, row_leaf_d); break;
+                    GBM_WALK(1) GBM_WALK(2) GBM_WALK(3) GBM_WALK(4) GBM_WALK(5) GBM_WALK(6) GBM_WALK(7) GBM_WALK(8)
+                    GBM_WALK(9) GBM_WALK(10) GBM_WALK(11) GBM_WALK(12) GBM_WALK(13) GBM_WALK(14) GBM_WALK(15)
+                    GBM_WALK(16)
+#undef GBM_WALK
+                }
+            } else if (n > 0) {
+                if (sm > 48 * 1024)
+                    GBM_CUDA(cudaFuncSetAttribute(leaf_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 leaf_walk_kernel<<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
                                                                 n_internal, D, n, row_leaf_d);
+            }
             GBM_CUDA(cudaGetLastError());
             break;
-        }
-        {
-            ProfScope ps(ctx, PC_PART_SCAN, s);
-            plan_kernel<<<1, 1024, 0, s>>>(nodes, first, n_par, G, tile_base, run_base, n_items);
         }
         GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
         // RepartitionInstances + BuildPartialHistograms (fused)
@@ -2154,9 +2260,13 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             ea.n_nodes = 1 << l;
             ea.hist_prev = l == 1 ? nullptr : hist_lvl[(l - 1) & 1];
             ea.hist_store = (l < D - 1) ? hist_lvl[l & 1] : nullptr;
-            ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
-            const long long warps = (long long)ea.n_nodes * F;
-            eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(ea);
+            ea.done = (l + 1 < D) ? done : nullptr;  // this level's eval plans level l + 1
+            {
+                ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
+                const long long warps = (long long)ea.n_nodes * F;
+                eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(ea);
+            }
+            ProfScope ps(ctx, PC_EVAL_FINAL, s);
             eval_final_kernel<<<ea.n_nodes, E_THREADS, 0, s>>>(ea, t);
             GBM_CUDA(cudaGetLastError());
         }
