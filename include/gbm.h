@@ -69,8 +69,12 @@ GBM_API int gbm_check(gbm_ctx *ctx, void *stream);
 
 /* ---------------------------------------------------------------- instrumentation
  * Optional CUDA-event timing of every kernel launch the context issues, grouped by kernel
- * (bench.py's per-kernel roofline).  gbm_profile_enable(1) resets and starts recording (it
- * synchronises the device); gbm_profile_read synchronises, fills one entry per kernel
+ * (bench.py's per-kernel roofline).  gbm_profile_enable(1) resets and starts recording every
+ * category; any other non-zero value is a bitmask of the categories to record (bit i = entry i
+ * of gbm_profile_read); 0 stops.  It synchronises the device.  Launches captured into a CUDA
+ * graph record their events as graph nodes: after replays, ms are those of the last replay while
+ * the device row counters (hence bytes, rows) accumulate over every replay.
+ * gbm_profile_read synchronises, fills one entry per kernel
  * category (cap >= 32) and starts a new window.  bytes = the launches' ALGORITHMIC bytes
  * (DESIGN.md "Algorithmic bytes"), rows = rows they processed, counted on the device.
  * gbm_launch_count: kernel launches issued by the context since creation. */
@@ -90,8 +94,9 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   0 auto (= compact), 1 compact (random bins, bank conflicts), 2 bank-column (feature per
  *   lane, conflict-free; falls back to compact when the bins do not fit).
  * GBM_OPT_CARRY_GRADIENTS: 0 (default) level passes gather qpair by row; 1 the row-index
- *   entries of every level carry the row's gradient pair (grad_bits <= 15; 8-byte entries). */
-enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2 };
+ *   entries of every level carry the row's gradient pair (grad_bits <= 15; 8-byte entries).
+ * GBM_OPT_RUN_TILES: 2048-row tiles per work item of the fused level kernel (0 = auto). */
+enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

@@ -260,8 +260,19 @@ class Context:
         _call("gbm_check", self.h, _stream())
 
     # ------------------------------------------------------------ instrumentation
-    def profile(self, enable: bool = True):
-        _call("gbm_profile_enable", self.h, int(bool(enable)))
+    PROFILE_CATEGORIES = ("grad_max", "grad_quant", "hist_root", "hist_level", "part_count", "part_scan",
+                          "part_scatter", "part_final", "evaluate", "allreduce", "update_margins",
+                          "init_tree", "predict", "cuts", "quantise_compress", "eval_final", "plan")
+
+    def profile(self, enable: bool = True, only=None):
+        """Start (reset) / stop in-library event timing; `only` = category names to record."""
+        v = int(bool(enable))
+        if enable and only:
+            v = 0
+            for name in only:
+                v |= 1 << self.PROFILE_CATEGORIES.index(name)
+            assert v > 1, "pick at least one category other than grad_max alone"
+        _call("gbm_profile_enable", self.h, v)
 
     def profile_read(self) -> dict:
         """Per-kernel {launches, ms, bytes, rows} since the last read (synchronises)."""
@@ -274,6 +285,7 @@ class Context:
 
     HIST_LAYOUT = 1
     CARRY_GRADIENTS = 2
+    RUN_TILES = 3
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

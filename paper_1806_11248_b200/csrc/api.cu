@@ -42,6 +42,7 @@ int Arena::reserve(size_t bytes) {
     }
     cap = want;
     used = 0;
+    generation++;
     return GBM_OK;
 }
 
@@ -49,6 +50,14 @@ const char *const PROF_NAMES[PC_N] = {
     "grad_max", "grad_quant", "hist_root", "hist_level", "part_count", "part_scan",
     "part_scatter", "part_final", "evaluate", "allreduce", "update_margins", "init_tree",
     "predict", "cuts", "quantise_compress", "eval_final", "plan"};
+
+// Under stream capture an event record must be an EXTERNAL event node to be timed after replays.
+static void record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+}
 
 static cudaEvent_t pool_event(Prof &p) {
     if (p.pool_used == p.pool.size()) {
@@ -69,16 +78,16 @@ unsigned long long *prof_rows_slot(gbm_ctx *ctx, int *slot) {
 ProfScope::ProfScope(gbm_ctx *c_, int cat_, cudaStream_t s_, double fixed_, int slot_, double bpr_)
     : c(c_), cat(cat_), slot(slot_), s(s_), bpr(bpr_), fixed(fixed_) {
     c->launches += (cat_ == PC_ALLREDUCE) ? 0 : 1;
-    if (!c->prof.on) return;
+    if (!c->prof.on || !((c->prof.mask >> cat_) & 1u)) return;
     a = pool_event(c->prof);
-    if (a) cudaEventRecord(a, s);
+    if (a) record(a, s);
 }
 
 ProfScope::~ProfScope() {
-    if (!c->prof.on || !a) return;
+    if (!a) return;
     cudaEvent_t b = pool_event(c->prof);
     if (!b) return;
-    cudaEventRecord(b, s);
+    record(b, s);
     c->prof.recs.push_back(ProfRec{cat, a, b, slot, bpr, fixed});
 }
 
@@ -199,6 +208,7 @@ int gbm_profile_enable(gbm_ctx *ctx, int enable) {
     }
     if (p.rows_dev) GBM_CUDA(cudaMemset(p.rows_dev, 0, sizeof(unsigned long long) * p.rows_cap));
     p.on = enable != 0;
+    p.mask = enable == 1 ? 0xffffffffu : (unsigned)enable;
     return GBM_OK;
 }
 
@@ -240,6 +250,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
     if (option == GBM_OPT_HIST_LAYOUT) {
         if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 column");
         ctx->hist_layout = (int)value;
+        return GBM_OK;
+    }
+    if (option == GBM_OPT_RUN_TILES) {
+        if (value < 0 || value > 64) return fail(GBM_E_ARG, "GBM_OPT_RUN_TILES: 0 (auto) .. 64");
+        ctx->run_tiles = (int)value;
         return GBM_OK;
     }
     if (option == GBM_OPT_CARRY_GRADIENTS) {

@@ -53,6 +53,7 @@ enum : uint32_t { DERR_LABEL = 1u, DERR_OVERFLOW = 2u, DERR_NONFINITE = 4u };
 struct Arena {
     char *base = nullptr;
     size_t cap = 0, used = 0;
+    unsigned generation = 0;  // bumped on every reallocation
     int reserve(size_t bytes);
     void reset() { used = 0; }
     template <class T> T *take(size_t count) {
@@ -83,6 +84,7 @@ struct ProfRec {
 
 struct Prof {
     bool on = false;
+    unsigned mask = 0xffffffffu;  // categories recorded (bit = ProfCat)
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> pool;
     size_t pool_used = 0;
@@ -105,6 +107,8 @@ struct gbm_ctx {
     long long launches = 0;        // kernel launches issued by this context
     int hist_layout = 0;           // GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 bank-column
     int carry_gradients = 0;       // GBM_OPT_CARRY_GRADIENTS
+    int run_tiles = 0;             // GBM_OPT_RUN_TILES (0 = auto)
+    std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
 };
 
 namespace gbm {

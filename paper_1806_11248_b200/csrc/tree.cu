@@ -63,7 +63,8 @@ constexpr int PT = 2048;         // partition tile (rows): 16 warps x 128 rows
 constexpr int WROWS = PT / 16;   // rows per warp per tile
 constexpr int P_THREADS = 256;   // partition kernels: 8 warps x 4 ballot words
 constexpr int H_THREADS = 512;   // histogram / fused kernels
-constexpr int RUN = 8;           // tiles per fused work item (flush amortisation)
+constexpr int RUN_MAX = 16;      // tiles per fused work item: chosen per tree (flush amortisation
+                                 // vs. enough items for every resident block)
 constexpr int E_THREADS = 256;   // evaluation kernels
 constexpr int MAX_CHUNK = 65535; // rows per flush (exactness bound above)
 constexpr int DUMMY_BINS = 32;   // scratch bins: padding features of the byte path (symbol 0)
@@ -122,7 +123,40 @@ __device__ void smem_flush(const SmemHist &h, unsigned long long *dst /* slot + 
 struct ByteLane {
     int r0, rstep, w;  // r0 < 0: thread idle
     int off[4];
+    unsigned agg;      // symbol slots (bit j) warp-aggregated: some lane's feature has few bins
 };
+
+// Features with at most this many bins are warp-aggregated.  0 = off: measured on B200,
+// __match_any_sync costs far more than the same-address ATOMS replays it removes (Higgs root
+// 0.33 -> 2.14 ms, Airline root 0.65 -> 7.6 ms with 64), so the path is kept but disabled.
+constexpr int AGG_MAX_BINS = 0;
+
+// Adds the 4 byte symbols of word wd with pair q.  Slots flagged in agg go through
+// __match_any_sync + __reduce_add_sync first, so the lanes that hit the same bin of a
+// low-cardinality feature (same-address ATOMS serialise) issue a single atomic (north star:
+// "warp-aggregated updates").  Called by all 32 lanes (warp-uniform control flow).
+template <bool WIDE, bool SENT>
+__device__ __forceinline__ void byte_word_add(const SmemHist &h, const int (&off)[4], unsigned agg, uint32_t wd,
+                                              int2 q, bool valid, int B) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int sy = (wd >> (8 * j)) & 255;
+        const bool ok = valid && (!SENT || sy != B);
+        const int bin = off[j] + sy;
+        if (!WIDE && ((agg >> j) & 1u)) {
+            const unsigned peers = __match_any_sync(0xffffffffu, ok ? bin : -1 - lane);
+            const int gs = __reduce_add_sync(peers, ok ? q.x : 0);
+            const int hs = __reduce_add_sync(peers, ok ? q.y : 0);
+            if (ok && lane == __ffs(peers) - 1) {
+                atomicAdd(h.base + bin, gs);
+                atomicAdd(h.base + h.hstride + bin, hs);
+            }
+        } else if (ok) {
+            hist_add<WIDE>(h.base, h.hstride, bin, q);
+        }
+    }
+}
 
 __device__ __forceinline__ ByteLane byte_lane(const QM &qm, const Group &grp, const int *s_off, int nb) {
     ByteLane L;
@@ -130,14 +164,21 @@ __device__ __forceinline__ ByteLane byte_lane(const QM &qm, const Group &grp, co
     const int rb = H_THREADS / Ug;
     L.rstep = rb;
     L.r0 = (int)threadIdx.x < rb * Ug ? (int)threadIdx.x / Ug : -1;
-    const int wr = (int)threadIdx.x - (L.r0 < 0 ? 0 : L.r0) * Ug;
+    const int wr = L.r0 < 0 ? 0 : (int)threadIdx.x - L.r0 * Ug;
     L.w = grp.u_lo + wr;
     const int f_lo = grp.u_lo * 4;
+    unsigned lc = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         int f = L.w * 4 + j;
-        L.off[j] = (L.r0 >= 0 && f < qm.F) ? s_off[f - f_lo] : nb;  // nb = first scratch bin
+        const bool real = L.r0 >= 0 && f < qm.F;
+        L.off[j] = real ? s_off[f - f_lo] : nb;  // nb = first scratch bin
+        if (real && s_off[f - f_lo + 1] - s_off[f - f_lo] <= AGG_MAX_BINS) lc |= 1u << j;
     }
+    L.agg = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (__any_sync(0xffffffffu, (lc >> j) & 1u)) L.agg |= 1u << j;
     return L;
 }
 
@@ -149,45 +190,27 @@ __device__ __forceinline__ void accumulate(const QM &qm, const Group &grp, const
                                            int nrows, const ByteLane &L, long long *tg, long long *th,
                                            bool totals) {
     if (BYTE) {
-        if (L.r0 < 0) return;
-        totals = totals && L.w == grp.u_lo;   // each row's pair counted once
-        const long long sw = qm.stride >> 5;  // words per row
-        int r = L.r0;
-        for (; r + 3 * L.rstep < nrows; r += 4 * L.rstep) {  // four rows in flight
-            uint32_t rw[4], wd[4];
+        totals = totals && L.r0 >= 0 && L.w == grp.u_lo;  // each row's pair counted once
+        const long long sw = qm.stride >> 5;                // words per row
+        for (int rb = 0; rb < nrows; rb += 4 * L.rstep) {   // warp-uniform; four rows in flight
+            uint32_t wd[4];
             int2 qq[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) rw[i] = rowf(r + i * L.rstep);
+            bool ok[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                wd[i] = __ldg(qm.P + rw[i] * sw + L.w);
-                qq[i] = __ldg(qpair + rw[i]);
+                const int r = rb + L.r0 + i * L.rstep;
+                ok[i] = L.r0 >= 0 && r < nrows;
+                const uint32_t ra = rowf(ok[i] ? r : 0);
+                wd[i] = __ldg(qm.P + ra * sw + L.w);
+                qq[i] = __ldg(qpair + ra);
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                if (totals) {
+                if (totals && ok[i]) {
                     *tg += qq[i].x;
                     *th += qq[i].y;
                 }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int sy = (wd[i] >> (8 * j)) & 255;
-                    if (!SENT || sy != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sy, qq[i]);
-                }
-            }
-        }
-        for (; r < nrows; r += L.rstep) {
-            const uint32_t ra = rowf(r);
-            const uint32_t wa = __ldg(qm.P + ra * sw + L.w);
-            const int2 qa = __ldg(qpair + ra);
-            if (totals) {
-                *tg += qa.x;
-                *th += qa.y;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int sa = (wa >> (8 * j)) & 255;
-                if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, L.off[j] + sa, qa);
+                byte_word_add<WIDE, SENT>(h, L.off, L.agg, wd[i], qq[i], ok[i], qm.B);
             }
         }
     } else {
@@ -342,7 +365,7 @@ __device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint3
 // run_base[j] (first RUN-tile run); n_items = runs x feature groups.  Work item i of the fused
 // kernel is run i / G, group i % G, resolved on the fly (find_parent over run_base).
 // Works for any block size that is a multiple of 32 (<= 1024).
-__device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_par, int n_groups,
+__device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_par, int n_groups, int run_tiles,
                            int *__restrict__ tile_base, int *__restrict__ run_base, int *__restrict__ n_items) {
     __shared__ long long sm32[32];
     __shared__ long long carry;
@@ -356,7 +379,7 @@ __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_p
             const NodeDev nd = nodes[first + j];
             if (nd.state != GBM_NODE_ABSENT && nd.count > 0) {
                 nt = (nd.count + PT - 1) / PT;
-                nr = (nt + RUN - 1) / RUN;
+                nr = (nt + run_tiles - 1) / run_tiles;
             }
         }
         const long long v = (nt << 32) | nr;
@@ -388,14 +411,24 @@ __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_p
     if (threadIdx.x == 0) {
         tile_base[n_par] = (int)(carry >> 32);
         run_base[n_par] = (int)(carry & 0xffffffff);
-        *n_items = (int)(carry & 0xffffffff) * n_groups;
+        n_items[0] = (int)(carry & 0xffffffff) * n_groups;
+        n_items[1] = 0;  // dynamic work counter of the fused kernel
     }
+}
+
+// Dynamic work distribution: the block claims the next item from counter[0]; n_items[0] items.
+__device__ __forceinline__ int claim_item(int *counter) {
+    __shared__ int s_item;
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    return s_item;
 }
 
 __global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
                                                     int n_groups, int *__restrict__ tile_base,
                                                     int *__restrict__ run_base, int *__restrict__ n_items) {
-    plan_block(nodes, first, n_par, n_groups, tile_base, run_base, n_items);
+    plan_block(nodes, first, n_par, n_groups, 1, tile_base, run_base, n_items);
 }
 
 // ============================================================== fused partition + histogram
@@ -405,7 +438,7 @@ struct FusedArgs {
     int first, n_par;
     const int *tile_base;
     const int *run_base;
-    int n_groups;
+    int n_groups, run_tiles;
     const int *n_items;
     const void *ridx_in;      // entries (EntryOf<CARRY>), null = identity (level 1)
     uint32_t *flags;          // [tiles][PT/32]
@@ -437,13 +470,14 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int n_items = *a.n_items;
     E *wrows = s_rows[wid];
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_items;
+         it = claim_item(const_cast<int *>(a.n_items) + 1)) {
         const int run = it / a.n_groups, g = it - run * a.n_groups;
         const int j = find_parent(a.run_base, a.n_par, run);
         const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * RUN, t1 = min(a.tile_base[j + 1], t0 + RUN);
+        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             if (g != 0) continue;
@@ -468,12 +502,22 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
         const int my_u = grp.u_lo + (lane - (my_r < 0 ? 0 : my_r) * Ug);
         const int f_lo = grp.u_lo * qm.S;
         int off[4] = {h.nb, h.nb, h.nb, h.nb};
-        if (BYTE && my_r >= 0) {
+        unsigned agg = 0;
+        if (BYTE) {
+            unsigned lc = 0;
+            if (my_r >= 0) {
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int f = my_u * 4 + jj;
-                if (f < qm.F) off[jj] = s_off[f - f_lo];
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int f = my_u * 4 + jj;
+                    if (f < qm.F) {
+                        off[jj] = s_off[f - f_lo];
+                        if (s_off[f - f_lo + 1] - s_off[f - f_lo] <= AGG_MAX_BINS) lc |= 1u << jj;
+                    }
+                }
             }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+                if (__any_sync(0xffffffffu, (lc >> jj) & 1u)) agg |= 1u << jj;
         }
         const bool build_left = nd.build_left != 0;
         const long long sw = qm.stride >> 5;
@@ -520,8 +564,24 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
             }
             __syncwarp();
             // (B) histogram of the listed rows
-            if (my_r >= 0) {
-                if (BYTE) {
+            if (BYTE && agg) {  // warp-uniform loop (aggregated slots use warp intrinsics)
+                for (int rb = 0; rb < nbuild; rb += 4 * rpp) {
+                    uint32_t wd[4];
+                    int2 qq[4];
+                    bool ok[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int rr = rb + my_r + i * rpp;
+                        ok[i] = my_r >= 0 && rr < nbuild;
+                        const E ew = wrows[ok[i] ? rr : 0];
+                        wd[i] = __ldg(qm.P + row_of(ew) * sw + (ok[i] ? my_u : grp.u_lo));
+                        qq[i] = entry_q(ew, a.qpair);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) byte_word_add<WIDE, SENT>(h, off, agg, wd[i], qq[i], ok[i], qm.B);
+                }
+            } else if (BYTE) {
+                if (my_r >= 0) {
                     int rr = my_r;
                     for (; rr + 3 * rpp < nbuild; rr += 4 * rpp) {
                         E ew[4];
@@ -552,7 +612,9 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
                             if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[jj] + sa, qa);
                         }
                     }
-                } else {
+                }
+            } else if (my_r >= 0) {
+                {
                     const int f0 = my_u * qm.S;
                     const int ns = min(qm.S, qm.F - f0);
                     for (int rr = my_r; rr < nbuild; rr += rpp) {
@@ -806,7 +868,7 @@ struct ColFusedArgs {
     int first, n_par;
     const int *tile_base;
     const int *run_base;
-    int n_groups;
+    int n_groups, run_tiles;
     const int *n_items;
     const void *ridx_in;  // entries, null = identity (level 1)
     uint32_t *flags;
@@ -832,13 +894,14 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int n_items = *a.n_items;
     E *wrows = s_rows[wid];
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_items;
+         it = claim_item(const_cast<int *>(a.n_items) + 1)) {
         const int run = it / a.n_groups, g = it - run * a.n_groups;
         const int j = find_parent(a.run_base, a.n_par, run);
         const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * RUN, t1 = min(a.tile_base[j + 1], t0 + RUN);
+        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             if (g != 0) continue;
@@ -1330,7 +1393,7 @@ struct EvalArgs {
     int level, first, F, n_nodes;
     // tree mode: the last eval_final block plans the next level's partition (plan_block)
     unsigned *done;                 // block counter (reset by the last block), null = no plan
-    int plan_groups;
+    int plan_groups, plan_run;
     int *tile_base, *run_base, *n_items;
     long long TB;
     const int32_t *cut_ptr;
@@ -1484,7 +1547,7 @@ __global__ void __launch_bounds__(E_THREADS) eval_final_kernel(EvalArgs a, TreeD
     if (!last) return;
     __threadfence();
     // the children of this level are the next level's parents
-    plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.tile_base, a.run_base, a.n_items);
+    plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.plan_run, a.tile_base, a.run_base, a.n_items);
     if (threadIdx.x == 0) *a.done = 0;
 }
 
@@ -1954,7 +2017,7 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     uint32_t *flags = A.take<uint32_t>((size_t)tiles * (PT / 32));
     int *tile_left = A.take<int>(tiles);
     int *tile_off = A.take<int>(tiles);
-    int *n_items = A.take<int>(1);
+    int *n_items = A.take<int>(2);  // [0] items, [1] work counter
     int *run_base = A.take<int>(4);
     unsigned long long *hist = A.take<unsigned long long>((size_t)std::max(1, q->cut_ptr_h[q->n_features]) * 2);
     Group *groups = A.take<Group>(hp.groups.size());
@@ -1978,6 +2041,7 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     fa.tile_base = tile_base;
     fa.run_base = run_base;
     fa.n_groups = 1;
+    fa.run_tiles = 1;
     fa.n_items = n_items;
     fa.ridx_in = rows_d;
     fa.flags = flags;
@@ -2031,7 +2095,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
 
     // ---- scratch (tree arena)
     const int max_par = D >= 1 ? (1 << (D - 1)) : 1;  // parents of one level
-    const long long max_tiles = (n + PT - 1) / PT + 2ll * max_par + 2;
+    const long long max_tiles = (n + PT - 1) / PT + 2ll * max_par + 2;  // (runs <= tiles)
     const long long slots = std::max(1, D >= 2 ? (1 << (D - 2)) : 1);
     const size_t hist_unit = (size_t)std::max<long long>(TB, 1) * 2;
     size_t need = 0;
@@ -2054,7 +2118,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     int *tile_base = A.take<int>(2 * max_par + 2);
     NodeDev *nodes = A.take<NodeDev>(2 * cap + 2);
     int *run_base = A.take<int>(2 * max_par + 2);
-    int *n_items = A.take<int>(1);
+    int *n_items = A.take<int>(2);  // [0] items, [1] work counter
     Group *groups = A.take<Group>(hp.col ? 1 : G);
     ColGroup *cgroups = A.take<ColGroup>(hp.col ? G : 1);
     long long *hist_root = A.take<long long>(hist_unit + 2);  // root histogram + totals
@@ -2063,8 +2127,23 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
     unsigned *done = A.take<unsigned>(1);
 
-    if (hp.col) GBM_CUDA(cudaMemcpyAsync(cgroups, hp.cgroups.data(), G * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
-    else GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
+    // the group table is uploaded only when it changes (keeps gbm_build_tree free of pageable
+    // copies, so a whole round can be captured in a CUDA graph)
+    {
+        std::vector<int> key;
+        key.push_back(hp.col ? 1 : 0);
+        key.push_back((int)(reinterpret_cast<uintptr_t>(groups) & 0x7fffffff));
+        key.push_back((int)A.generation);
+        if (hp.col)
+            for (auto &g : hp.cgroups) { key.push_back(g.f_lo); key.push_back(g.f_hi); }
+        else
+            for (auto &g : hp.groups) { key.push_back(g.u_lo); key.push_back(g.u_hi); key.push_back(g.bin_lo); key.push_back(g.bin_hi); }
+        if (key != ctx->tree_groups_key) {
+            if (hp.col) GBM_CUDA(cudaMemcpyAsync(cgroups, hp.cgroups.data(), G * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
+            else GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
+            ctx->tree_groups_key = key;
+        }
+    }
     const TreeDev t = tree_dev(tree);
     const double row_bytes = (double)F * q->bits / 8.0;  // algorithmic bytes of one packed row
     {
@@ -2087,7 +2166,9 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         ca.hist = reinterpret_cast<unsigned long long *>(hist_root);
         ca.totals = reinterpret_cast<unsigned long long *>(hist_root + hist_unit);
         ca.cstride = hp.cstride;
-        ProfScope ps(ctx, PC_HIST_ROOT, s, (double)n * (row_bytes + 8.0));
+        int slot = -1;
+        ca.rows_ctr = prof_rows_slot(ctx, &slot);
+        ProfScope ps(ctx, PC_HIST_ROOT, s, 0.0, slot, row_bytes + 8.0);
         const long long n_it = (n + hp.chunk - 1) / hp.chunk * (long long)G;
         const int grid = (int)std::max<long long>(1, std::min<long long>(n_it, hp.blocks_range));
         launch_col_range(hp, ca, grid, s);
@@ -2105,7 +2186,9 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         ra.hist = reinterpret_cast<unsigned long long *>(hist_root);
         ra.totals = reinterpret_cast<unsigned long long *>(hist_root + hist_unit);
         ra.hstride = hp.hstride;
-        ProfScope ps(ctx, PC_HIST_ROOT, s, (double)n * (row_bytes + 8.0));
+        int slot = -1;
+        ra.rows_ctr = prof_rows_slot(ctx, &slot);  // device-counted: correct under graph replays too
+        ProfScope ps(ctx, PC_HIST_ROOT, s, 0.0, slot, row_bytes + 8.0);
         GBM_TRY(GBM_DISPATCH(hp, launch_range, ctx, hp, ra, s));
     } else if (n > 0) {
         return fail(GBM_E_ARG, "gbm_build_tree: no feature has a cut (all values missing)");
@@ -2120,7 +2203,14 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     ea.hist_root = hist_root;
     ea.hist_build = hist_build;
     ea.fb = fb;
+    // tiles per fused work item: about 4 items per resident block at the widest level (items are
+    // claimed dynamically; measured on Higgs: 4 tiles 0.79 ms, 8 tiles 0.84, 16 tiles 0.99 / round)
+    const long long tiles_all = (n + PT - 1) / PT;
+    const long long target = 4ll * hp.blocks_fused;
+    const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
+        1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
     ea.plan_groups = G;
+    ea.plan_run = run_tiles;
     ea.tile_base = tile_base;
     ea.run_base = run_base;
     ea.n_items = n_items;
@@ -2148,6 +2238,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     fa.tile_base = tile_base;
     fa.run_base = run_base;
     fa.n_groups = G;
+    fa.run_tiles = run_tiles;
     fa.n_items = n_items;
     fa.flags = flags;
     fa.tile_left = tile_left;
@@ -2212,6 +2303,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
                 ca.tile_base = tile_base;
                 ca.run_base = run_base;
                 ca.n_groups = G;
+                ca.run_tiles = run_tiles;
                 ca.n_items = n_items;
                 ca.ridx_in = rin;
                 ca.flags = flags;
