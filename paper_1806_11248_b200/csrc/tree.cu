@@ -862,6 +862,83 @@ __global__ void __launch_bounds__(256) sum_qpair_kernel(const int2 *__restrict__
     block_totals(tg, th, red, out);
 }
 
+// ============================================================== staged bank-column histograms
+// GBM_OPT_HIST_LAYOUT = 3 (byte symbols, narrow): every warp stages 32 rows at a time into shared
+// memory with coalesced 4-byte loads (the group's words of each row) plus the rows' gradient
+// pairs, then lane = (copy, feature column) reads its byte with a conflict-free LDS.U8, the pair
+// with a broadcast LDS.64, and updates its own bank column with conflict-free ATOMS.
+// Per row (Higgs): ~4.6 L1 data-pipe wavefronts vs ~7.8 for the compact layout.
+constexpr int CS_WMAX = 8;                     // words per staged row (<= 32 byte features)
+struct CsWarp {
+    uint32_t w[32 * CS_WMAX];                  // staged rows: [32][Wg] words
+    int2 q[32];                                // their gradient pairs
+};
+
+// Stage rows row_i (i < 32, valid_i) of group words [u_lo, u_lo+Wg) and their pairs; then add.
+template <class RowF, class QF>
+__device__ __forceinline__ void cs_batch(const QM &qm, CsWarp &st, int *hs, int u_lo, int Wg, int Fg, int R, int copy,
+                                         int nrows, RowF rowf, QF qf) {
+    const int lane = threadIdx.x & 31;
+    const long long sw = qm.stride >> 5;
+    // pairs: lane i stages row i
+    {
+        const bool ok = lane < nrows;
+        const int2 q = ok ? qf(lane) : make_int2(0, 0);
+        st.q[lane] = q;
+    }
+    // words: flattened (row, word) over 32*Wg slots, consecutive lanes -> consecutive words
+    for (int idx = lane; idx < 32 * Wg; idx += 32) {
+        const int i = idx / Wg, w = idx - i * Wg;
+        st.w[idx] = i < nrows ? __ldg(qm.P + (long long)rowf(i) * sw + u_lo + w) : 0u;
+    }
+    __syncwarp();
+    const uint8_t *sb = reinterpret_cast<const uint8_t *>(st.w);
+    const int col = lane % Fg;  // byte of the feature within the staged row
+    const int rowbytes = Wg * 4;
+#pragma unroll 4
+    for (int i0 = 0; i0 < nrows; i0 += R) {
+        const int i = min(i0 + copy, 31);
+        const int sym = sb[i * rowbytes + col];
+        const int2 q = (i0 + copy < nrows) ? st.q[i] : make_int2(0, 0);
+        col_add_b<false>(hs, (sym << 5) + lane, q);
+    }
+    __syncwarp();
+}
+
+template <bool IDENT>
+__global__ void __launch_bounds__(H_THREADS) hist_cs_range_kernel(ColRangeArgs a) {
+    extern __shared__ int smem[];
+    CsWarp *stage = reinterpret_cast<CsWarp *>(smem + 2 * COLB_STRIDE);
+    const QM &qm = a.qm;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = H_THREADS / 32;
+    const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int g = it % a.n_groups;
+        const long long start = (long long)(it / a.n_groups) * a.chunk;
+        const long long end = min(a.n_sel, start + a.chunk);
+        const ColGroup cg = a.groups[g];
+        for (int i = threadIdx.x; i < 2 * COLB_STRIDE; i += H_THREADS) smem[i] = 0;
+        if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)(end - start));
+        __syncthreads();
+        const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
+        const int copy = min(lane / Fg, R - 1);
+        const int u_lo = cg.f_lo >> 2, Wg = ((cg.f_hi + 3) >> 2) - u_lo;
+        for (long long b0 = start + (long long)wid * 32; b0 < end; b0 += NW * 32) {
+            const int nrows = (int)min(32ll, end - b0);
+            auto rowf = [&](int i) -> uint32_t {
+                const long long r = b0 + i;
+                return IDENT ? (uint32_t)r : __ldg(a.ridx + r);
+            };
+            cs_batch(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, nrows, rowf,
+                     [&](int i) { return __ldg(a.qpair + rowf(i)); });
+        }
+        __syncthreads();
+        col_flush<false>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist);
+        __syncthreads();
+    }
+}
+
 struct ColFusedArgs {
     QM qm;
     const NodeDev *nodes;
@@ -1013,6 +1090,98 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
         if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
         __syncthreads();
         col_flush<WIDE>(smem, a.cstride, cg, a.cut_ptr, a.hist + (long long)j * a.TB * 2);
+        __syncthreads();
+    }
+}
+
+// fused partition + staged bank-column histogram (GBM_OPT_HIST_LAYOUT = 3)
+template <bool CARRY>
+__global__ void __launch_bounds__(H_THREADS) part_hist_cs_kernel(ColFusedArgs a) {
+    using E = typename EntryOf<CARRY>::T;
+    extern __shared__ int smem[];
+    CsWarp *stage = reinterpret_cast<CsWarp *>(smem + 2 * COLB_STRIDE);
+    __shared__ E s_rows[H_THREADS / 32][WROWS];
+    const QM &qm = a.qm;
+    const E *rin = static_cast<const E *>(a.ridx_in);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n_items = *a.n_items;
+    E *wrows = s_rows[wid];
+    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_items;
+         it = claim_item(const_cast<int *>(a.n_items) + 1)) {
+        const int run = it / a.n_groups, g = it - run * a.n_groups;
+        const int j = find_parent(a.run_base, a.n_par, run);
+        const int k = a.first + j;
+        const NodeDev nd = a.nodes[k];
+        const int tb = a.tile_base[j];
+        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const long long seg_end = nd.start + nd.count;
+        if (nd.state == GBM_NODE_LEAF) {
+            if (g != 0) continue;
+            for (int t = t0; t < t1; ++t) {
+                const long long base = nd.start + (long long)(t - tb) * PT;
+                for (int i = threadIdx.x; i < PT; i += H_THREADS) {
+                    const long long pos = base + i;
+                    if (pos < seg_end) a.row_leaf[rin ? row_of(rin[pos]) : (uint32_t)pos] = k;
+                }
+            }
+            continue;
+        }
+        const ColGroup cg = a.groups[g];
+        for (int i = threadIdx.x; i < 2 * COLB_STRIDE; i += H_THREADS) smem[i] = 0;
+        __syncthreads();
+        const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
+        const int copy = min(lane / Fg, R - 1);
+        const int u_lo = cg.f_lo >> 2, Wg = ((cg.f_hi + 3) >> 2) - u_lo;
+        const bool build_left = nd.build_left != 0;
+        unsigned long long bits_acc = 0;
+        for (int t = t0; t < t1; ++t) {
+            const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
+            E row[4];
+            uint32_t bw[4];
+            int nleft = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const long long pos = base + s2 * 32 + lane;
+                if (pos < seg_end) row[s2] = rin ? rin[pos] : make_entry<CARRY>((uint32_t)pos, a.qpair);
+                else row[s2] = E{};
+            }
+            bool left[4];
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+                left[s2] = base + s2 * 32 + lane < seg_end && goes_left(qm, nd, row_of(row[s2]));
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const bool valid = base + s2 * 32 + lane < seg_end;
+                const uint32_t lw = __ballot_sync(0xffffffffu, valid && left[s2]);
+                bw[s2] = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
+                if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 4 + s2] = lw;
+                nleft += __popc(lw);
+            }
+            int nbuild = 0;
+            const uint32_t ltm = (1u << lane) - 1u;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                if ((bw[s2] >> lane) & 1u) wrows[nbuild + __popc(bw[s2] & ltm)] = row[s2];
+                nbuild += __popc(bw[s2]);
+            }
+            if (g == 0 && lane == 0) {
+                if (nleft) atomicAdd(a.tile_left + t, nleft);
+                if (a.rows_ctr) {
+                    const long long nv = max(0ll, min((long long)WROWS, seg_end - base));
+                    bits_acc += (unsigned long long)nv * a.bits_parent_row +
+                                (unsigned long long)nbuild * a.bits_built_row;
+                }
+            }
+            __syncwarp();
+            for (int b0 = 0; b0 < nbuild; b0 += 32)
+                cs_batch(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, min(32, nbuild - b0),
+                         [&](int i) { return row_of(wrows[b0 + i]); },
+                         [&](int i) { return entry_q(wrows[b0 + i], a.qpair); });
+            __syncwarp();
+        }
+        if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
+        __syncthreads();
+        col_flush<false>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist + (long long)j * a.TB * 2);
         __syncthreads();
     }
 }
@@ -1664,6 +1833,7 @@ struct HistPlan {
     bool wide = false, byte_path = false, sent = false;
     bool carry = false;   // level entries carry the gradient pairs (grad_bits <= 15)
     bool col = false;     // bank-column kernels (every feature has <= rows bins)
+    bool staged = false;  // staged bank-column kernels (layout 3: byte symbols, narrow)
     std::vector<ColGroup> cgroups;
     int cstride = 0;      // col: words per channel (rows * 32)
     int hstride = 0;      // words per smem channel
@@ -1724,7 +1894,7 @@ static int setup_col(gbm_ctx *ctx, HistPlan &hp) {
 }
 
 static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide, long long rows_hint,
-                     HistPlan &hp, int grad_bits = 30, bool allow_col = true) {
+                     HistPlan &hp, int grad_bits = 30, bool allow_col = true, bool staged = false) {
     const int *cp = q->cut_ptr_h;
     hp.wide = wide;
     hp.carry = !wide && grad_bits <= 15 && ctx->carry_gradients;
@@ -1736,6 +1906,34 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
         for (int f = 0; f < qm.F; ++f) max_nb = std::max(max_nb, cp[f + 1] - cp[f]);
         const bool byte_sym = q->bits == 8;
         const int rows = byte_sym ? 256 : (max_nb + 7) / 8 * 8;
+        if (staged && byte_sym && !wide && qm.stride % 32 == 0) {  // staged column kernels
+            hp.col = hp.staged = true;
+            hp.byte_path = true;
+            hp.cstride = COLB_STRIDE;
+            hp.smem_bytes = 2 * COLB_STRIDE * 4 + (H_THREADS / 32) * (int)sizeof(CsWarp);
+            hp.cgroups.clear();
+            const int ng = (qm.F + 31) / 32, nu = (qm.F + 3) / 4;
+            for (int g = 0; g < ng; ++g) {  // groups of whole 4-feature words, <= 32 features
+                ColGroup c;
+                c.f_lo = 4 * (int)((long long)nu * g / ng);
+                c.f_hi = std::min(qm.F, 4 * (int)((long long)nu * (g + 1) / ng));
+                hp.cgroups.push_back(c);
+            }
+            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            int o1 = 0, o2 = 0;
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_cs_range_kernel<true>, H_THREADS, hp.smem_bytes));
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_cs_kernel<false>, H_THREADS, hp.smem_bytes));
+            if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "staged column kernels cannot be resident");
+            hp.blocks_range = o1 * ctx->sm_count;
+            hp.blocks_fused = o2 * ctx->sm_count;
+            const long long G = (long long)hp.cgroups.size();
+            long long per = (rows_hint + 2ll * hp.blocks_range - 1) / (2ll * hp.blocks_range) * G;
+            hp.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per));
+            return GBM_OK;
+        }
         if (allow_col && channels * rows * 32 * 4 <= budget) {
             hp.col = true;
             hp.byte_path = byte_sym;
@@ -1818,6 +2016,13 @@ static int launch_fused(gbm_ctx *ctx, const HistPlan &hp, FusedArgs a, cudaStrea
 
 static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int grid, cudaStream_t s) {
     const int sm = hp.smem_bytes;
+    if (hp.staged) {
+        if (ca.totals) sum_qpair_kernel<<<std::min<long long>((ca.n_sel + 255) / 256, 148 * 8), 256, 0, s>>>(
+            ca.qpair, ca.n_sel, ca.totals);
+        if (ca.ridx) hist_cs_range_kernel<false><<<grid, H_THREADS, sm, s>>>(ca);
+        else hist_cs_range_kernel<true><<<grid, H_THREADS, sm, s>>>(ca);
+        return;
+    }
     if (hp.byte_path) {
         if (ca.totals) sum_qpair_kernel<<<std::min<long long>((ca.n_sel + 255) / 256, 148 * 8), 256, 0, s>>>(
             ca.qpair, ca.n_sel, ca.totals);
@@ -1841,6 +2046,11 @@ static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int gri
 
 static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStream_t s) {
     const int g = hp.blocks_fused, sm = hp.smem_bytes;
+    if (hp.staged) {
+        if (hp.carry) part_hist_cs_kernel<true><<<g, H_THREADS, sm, s>>>(ca);
+        else part_hist_cs_kernel<false><<<g, H_THREADS, sm, s>>>(ca);
+        return;
+    }
     if (hp.wide) {
         if (hp.byte_path) part_hist_col_kernel<true, false, true><<<g, H_THREADS, sm, s>>>(ca);
         else part_hist_col_kernel<true, false, false><<<g, H_THREADS, sm, s>>>(ca);
@@ -1913,7 +2123,7 @@ int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair
     const QM qm = make_qm(q);
     const int TB = q->cut_ptr_h[q->n_features];
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp, grad_bits, ctx->hist_layout == 2));
+    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp, grad_bits, ctx->hist_layout >= 2, ctx->hist_layout == 3));
     GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)std::max(TB, 1) * 2 * 8, s));
     if (n_sel == 0 || TB == 0) return GBM_OK;
     if (hp.col) {
@@ -2089,7 +2299,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     const long long cap = (1ll << (D + 1)) - 1;
     HistPlan hp;
     GBM_TRY(plan_hist(ctx, q, qm, prm->grad_bits > 15, std::max<long long>(n, 1), hp, prm->grad_bits,
-                      ctx->hist_layout == 2));
+                      ctx->hist_layout >= 2, ctx->hist_layout == 3));
     const int G = hp.col ? (int)hp.cgroups.size() : (int)hp.groups.size();
     const size_t esz = hp.carry ? 8 : 4;  // bytes per level entry
 

@@ -157,7 +157,7 @@ def test_gradients_label_error(ctx, G):
 
 
 # ------------------------------------------------------------------ a4/a6: histograms
-@pytest.mark.parametrize("layout", [1, 2])
+@pytest.mark.parametrize("layout", [1, 2, 3])
 @pytest.mark.parametrize("P", [15, 30])
 @pytest.mark.parametrize("cfg,align,missing", [("higgs", 32, 0.0), ("tiny", 0, 0.05),
                                                ("airline", 128, 0.0), ("yearmsd", 32, 0.01)])
@@ -250,7 +250,8 @@ TREE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("layout,colsym,carry", [(0, True, 0), (2, True, 0), (0, False, 1), (2, False, 1)])
+@pytest.mark.parametrize("layout,colsym,carry", [(0, True, 0), (2, True, 0), (0, False, 1), (2, False, 1),
+                                                 (3, True, 0), (3, False, 1)])
 @pytest.mark.parametrize("cfg,n,missing,align,P,rounds,depth", TREE_CASES)
 def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth, colsym, layout,
                                 carry):
