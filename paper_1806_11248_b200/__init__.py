@@ -286,6 +286,7 @@ class Context:
     HIST_LAYOUT = 1
     CARRY_GRADIENTS = 2
     RUN_TILES = 3
+    GROUP_UNITS = 4
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

@@ -257,6 +257,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->run_tiles = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_GROUP_UNITS) {
+        if (value < 0 || value > 32) return fail(GBM_E_ARG, "GBM_OPT_GROUP_UNITS: 0 (auto) .. 32");
+        ctx->group_units = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_CARRY_GRADIENTS) {
         ctx->carry_gradients = value != 0;
         return GBM_OK;

@@ -108,6 +108,7 @@ struct gbm_ctx {
     int hist_layout = 0;           // GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 bank-column
     int carry_gradients = 0;       // GBM_OPT_CARRY_GRADIENTS
     int run_tiles = 0;             // GBM_OPT_RUN_TILES (0 = auto)
+    int group_units = 0;           // GBM_OPT_GROUP_UNITS (0 = auto = 32)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
 };
 

@@ -220,23 +220,33 @@ __device__ __forceinline__ void accumulate(const QM &qm, const Group &grp, const
         const uint32_t total = (uint32_t)nrows * (uint32_t)Ug;
         const int f_lo = grp.u_lo * qm.S;
         const uint32_t mask = (1u << qm.bits) - 1u;
-        for (uint32_t j = threadIdx.x; j < total; j += H_THREADS) {
-            const uint32_t r = Ug == 1 ? j : fast_div(j, magic);
-            const int u = grp.u_lo + (int)(j - r * (uint32_t)Ug);
-            const uint32_t row = rowf((int)r);
-            const int2 q = __ldg(qpair + row);
-            if (totals && u == grp.u_lo) {
-                *tg += q.x;
-                *th += q.y;
+        for (uint32_t j0 = threadIdx.x; j0 < total; j0 += 4 * H_THREADS) {  // four (row, unit) in flight
+            uint32_t win[4];
+            int2 q[4];
+            int f0[4], ns[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t j = j0 + i * H_THREADS;
+                const bool ok = j < total;
+                const uint32_t r = Ug == 1 ? j : fast_div(j, magic);
+                const int u = grp.u_lo + (int)(j - r * (uint32_t)Ug);
+                const uint32_t row = rowf(ok ? (int)r : 0);
+                q[i] = __ldg(qpair + row);
+                if (totals && ok && u == grp.u_lo) {
+                    *tg += q[i].x;
+                    *th += q[i].y;
+                }
+                f0[i] = ok ? u * qm.S : f_lo;
+                ns[i] = ok ? min(qm.S, qm.F - f0[i]) : 0;
+                win[i] = get_bits(qm.P, (long long)row * qm.stride + (long long)f0[i] * qm.bits, max(ns[i], 1) * qm.bits);
             }
-            const int f0 = u * qm.S;
-            const int ns = min(qm.S, qm.F - f0);
-            const uint32_t win = get_bits(qm.P, (long long)row * qm.stride + (long long)f0 * qm.bits, ns * qm.bits);
-            for (int jj = 0; jj < ns; ++jj) {
-                const int s = (int)((win >> (jj * qm.bits)) & mask);
-                if (s == qm.B) continue;  // missing: mass recovered as total - sum (R7)
-                hist_add<WIDE>(h.base, h.hstride, s_off[f0 + jj - f_lo] + s, q);
-            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                for (int jj = 0; jj < ns[i]; ++jj) {
+                    const int s = (int)((win[i] >> (jj * qm.bits)) & mask);
+                    if (s == qm.B) continue;  // missing: mass recovered as total - sum (R7)
+                    hist_add<WIDE>(h.base, h.hstride, s_off[f0[i] + jj - f_lo] + s, q[i]);
+                }
         }
     }
 }
@@ -617,7 +627,26 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
                 {
                     const int f0 = my_u * qm.S;
                     const int ns = min(qm.S, qm.F - f0);
-                    for (int rr = my_r; rr < nbuild; rr += rpp) {
+                    const long long boff = (long long)f0 * qm.bits;
+                    int rr = my_r;
+                    for (; rr + 3 * rpp < nbuild; rr += 4 * rpp) {  // four rows in flight
+                        uint32_t win[4];
+                        int2 qq[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const E ea = wrows[rr + i * rpp];
+                            qq[i] = entry_q(ea, a.qpair);
+                            win[i] = get_bits(qm.P, (long long)row_of(ea) * qm.stride + boff, ns * qm.bits);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            for (int jj = 0; jj < ns; ++jj) {
+                                const int sy = (int)((win[i] >> (jj * qm.bits)) & mask);
+                                if (sy == qm.B) continue;
+                                hist_add<WIDE>(h.base, h.hstride, s_off[f0 + jj - f_lo] + sy, qq[i]);
+                            }
+                    }
+                    for (; rr < nbuild; rr += rpp) {
                         const E ea = wrows[rr];
                         const uint32_t ra = row_of(ea);
                         const int2 q = entry_q(ea, a.qpair);
@@ -1962,26 +1991,47 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
     const int static_smem = 26 * 1024;
     const int budget = (int)std::min<size_t>(ctx->smem_optin - static_smem, 200 * 1024);
     const int max_bins_group = budget / (4 * channels) - DUMMY_BINS - 32;
-    hp.groups.clear();
-    int u = 0;
-    while (u < qm.U) {
-        Group g;
-        g.u_lo = u;
-        g.bin_lo = cp[std::min(u * qm.S, qm.F)];
-        int u_end = u;
-        while (u_end < qm.U) {
-            const int f_hi = std::min((u_end + 1) * qm.S, qm.F);
-            const int nb = cp[f_hi] - g.bin_lo;
-            const int nf = f_hi - u * qm.S;
-            if ((nb > max_bins_group || nf > 2048 || (u_end - u + 1) > 32) && u_end > u) break;
-            if (nb > max_bins_group)
-                return fail(GBM_E_ARG, "a single feature unit has more bins than fit in shared memory");
-            u_end++;
+    // Feature groups of <= ucap units.  Auto: the largest power of two (a warp's lanes map to
+    // whole rows x units) whose groups still leave two blocks resident per SM -- measured on the
+    // wide workloads (Epsilon 8 units: level pass 2.5 vs 3.6 ms at 24; Bosch 16: 1.8 vs 2.7 at 32).
+    auto make_groups = [&](int ucap, std::vector<Group> &out) -> int {
+        out.clear();
+        const int ng = (qm.U + ucap - 1) / ucap;
+        const int umax = (qm.U + ng - 1) / ng;  // balanced: the last group is not a sliver
+        int u = 0, mx = 1;
+        while (u < qm.U) {
+            Group g;
+            g.u_lo = u;
+            g.bin_lo = cp[std::min(u * qm.S, qm.F)];
+            int u_end = u;
+            while (u_end < qm.U) {
+                const int f_hi = std::min((u_end + 1) * qm.S, qm.F);
+                const int nb = cp[f_hi] - g.bin_lo;
+                const int nf = f_hi - u * qm.S;
+                if ((nb > max_bins_group || nf > 2048 || (u_end - u + 1) > umax) && u_end > u) break;
+                if (nb > max_bins_group) return -1;
+                u_end++;
+            }
+            g.u_hi = u_end;
+            g.bin_hi = cp[std::min(u_end * qm.S, qm.F)];
+            mx = std::max(mx, g.bin_hi - g.bin_lo);
+            out.push_back(g);
+            u = u_end;
         }
-        g.u_hi = u_end;
-        g.bin_hi = cp[std::min(u_end * qm.S, qm.F)];
-        hp.groups.push_back(g);
-        u = u_end;
+        return mx;
+    };
+    int sm_smem = 0;
+    GBM_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device));
+    if (ctx->group_units > 0) {
+        if (make_groups(ctx->group_units, hp.groups) < 0)
+            return fail(GBM_E_ARG, "a single feature unit has more bins than fit in shared memory");
+    } else {
+        for (int ucap = 32;; ucap >>= 1) {
+            const int mx = make_groups(ucap, hp.groups);
+            if (mx < 0) return fail(GBM_E_ARG, "a single feature unit has more bins than fit in shared memory");
+            const int bytes = channels * ((mx + DUMMY_BINS + 31) / 32 * 32) * 4 + static_smem + 1024;
+            if (ucap == 1 || 2 * bytes <= sm_smem) break;
+        }
     }
     int max_nb = 1;
     for (auto &g : hp.groups) max_nb = std::max(max_nb, g.bin_hi - g.bin_lo);

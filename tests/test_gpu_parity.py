@@ -247,6 +247,7 @@ TREE_CASES = [
     ("higgs", 50_000, 0.02, 128, 30, 2, None),
     ("airline", 120_000, 0.0, 32, 15, 2, None),
     ("airline", 60_000, 0.03, 0, 12, 2, None),
+    ("bosch", 12_000, 0.0, 32, 15, 2, None),   # ~81% missing: 9-bit symbols, default directions
 ]
 
 

@@ -49,6 +49,9 @@ CONFIGS = {
     "higgs": Config("higgs", 2, 11_000_000, 28, 256, "binary:logistic", 6, 500, "1/2/4/8"),
     "epsilon": Config("epsilon", 3, 500_000, 2000, 256, "binary:logistic", 6, 100, "1/2/4/8"),
     "airline": Config("airline", 4, 115_000_000, 13, 256, "binary:logistic", 8, 500, "1/2/4/8"),
+    # SURVEY.md §8(f) NEXT #4 (not a BASELINE.json config): Bosch-shaped sparse matrix
+    # (1M x 968 binary) -- ~81% of the values missing, ~0.6% positives
+    "bosch": Config("bosch", 5, 1_000_000, 968, 256, "binary:logistic", 6, 100, "1"),
 }
 
 # Airline-shaped cardinalities: Year, Month, DayofMonth, DayOfWeek, DepTime,
@@ -159,8 +162,30 @@ def _airline(rng, m, F):
     return X.astype(np.float32), y
 
 
+_BOSCH_W = None
+
+
+def _bosch(rng, m, F):
+    """Production-line measurements: ~81% missing (whole stations absent per part), values with a
+    few distinct levels for some features, rare failures (~0.6%) driven by a few measurements."""
+    global _BOSCH_W
+    if _BOSCH_W is None or _BOSCH_W[0].shape[0] != F:
+        r0 = _rng(BASE_SEED + 5, 1 << 30)
+        _BOSCH_W = (r0.standard_normal(F) * (r0.random(F) < 0.05), r0.integers(2, 40, F),
+                    r0.random(F) < 0.2)
+    w, levels, coarse = _BOSCH_W
+    X = rng.standard_normal((m, F), dtype=np.float32)
+    X[:, coarse] = np.round(X[:, coarse] * levels[coarse] / 4) / (levels[coarse] / 4)
+    station = rng.random((m, (F + 47) // 48), dtype=np.float32) < 0.19   # ~19% of stations visited
+    present = np.repeat(station, 48, axis=1)[:, :F]
+    z = np.where(present, X, 0.0).astype(np.float64) @ w - 7.0 + 0.5 * rng.standard_normal(m)
+    X[~present] = np.nan
+    y = (rng.random(m) < _sigmoid(z)).astype(np.float32)
+    return X, y
+
+
 _GEN = {"tiny": _tiny, "yearmsd": _yearmsd, "higgs": _higgs, "epsilon": _epsilon,
-        "airline": _airline}
+        "airline": _airline, "bosch": _bosch}
 
 
 def generate(name: str, lo: int = 0, hi: int | None = None, *, n_rows: int | None = None,
