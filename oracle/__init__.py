@@ -79,6 +79,15 @@ def lib():
                                                 i32, _P(C.c_int8), _P(i32), _P(i32), _P(f32),
                                                 _P(C.c_int8), _P(f64), _P(f64), _P(i64),
                                                 _P(i64), _P(i32)]),
+                "oracle_build_tree_lossguide": (C.c_int, [_P(C.c_uint32), i64, i32, i32, i32,
+                                                          _P(f32), _P(i32), i32, _P(i32), _P(i32),
+                                                          i32, i32, _P(f64), i32, _P(C.c_int8),
+                                                          _P(i32), _P(i32), _P(f32), _P(C.c_int8),
+                                                          _P(f64), _P(f64), _P(i64), _P(i64),
+                                                          _P(i32), _P(i32)]),
+                "oracle_predict_linked": (C.c_int, [i32, i64, _P(C.c_int8), _P(i32), _P(f32),
+                                                    _P(C.c_int8), _P(i32), _P(f64), f64, _P(f32),
+                                                    i64, i32, _P(f64)]),
                 "oracle_update_margins": (C.c_int, [_P(f64), _P(i32), i64, _P(f64)]),
                 "oracle_predict": (C.c_int, [i32, i32, _P(C.c_int8), _P(i32), _P(f32),
                                              _P(C.c_int8), _P(f64), f64, _P(f32), i64, i32,
@@ -234,11 +243,15 @@ def tree_capacity(max_depth: int) -> int:
 
 
 def build_tree(words, n, F, bits, row_align_bits, cut_values, cut_ptr, max_bins, qpair, scale,
-               max_depth, eta=0.3, reg_lambda=1.0, gamma=0.0, mcw=1.0, p_workers=1):
-    """Algorithm 1 on p logical workers.  Returns (tree dict of heap arrays,
-    row_leaf int32 [n])."""
-    cap = tree_capacity(max_depth)
-    t = {k: np.zeros(cap, dt) for k, dt in TREE_FIELDS}
+               max_depth, eta=0.3, reg_lambda=1.0, gamma=0.0, mcw=1.0, p_workers=1,
+               grow_policy="depthwise", max_leaves=0):
+    """Algorithm 1 on p logical workers.  Returns (tree dict, row_leaf int32 [n]).
+    depthwise: heap arrays of capacity 2^(D+1)-1 (FIFO queue, "nodes closer to the root").
+    lossguide: priority queue on the gain (R25-R27), capacity 2*max_leaves-1, plus the
+    array left_child (right child = left + 1)."""
+    lossguide = grow_policy == "lossguide"
+    cap = 2 * max_leaves - 1 if lossguide else tree_capacity(max_depth)
+    t = {k: np.zeros(max(cap, 1), dt) for k, dt in TREE_FIELDS}
     row_leaf = np.zeros(n, np.int32)
     cv = np.ascontiguousarray(cut_values, dtype=np.float32)
     if cv.size == 0:
@@ -248,15 +261,22 @@ def build_tree(words, n, F, bits, row_align_bits, cut_values, cut_ptr, max_bins,
     sc = np.asarray(scale, dtype=np.int32)
     params = np.array([eta, reg_lambda, gamma, mcw], np.float64)
     words = np.ascontiguousarray(words, dtype=np.uint32)
-    _check(lib().oracle_build_tree(
-        _ptr(words, C.c_uint32), n, F, bits, row_align_bits, _ptr(cv, C.c_float),
-        _ptr(cp, C.c_int32), max_bins, _ptr(qpair, C.c_int32), _ptr(sc, C.c_int32), max_depth,
-        _ptr(params, C.c_double), p_workers, _ptr(t["kind"], C.c_int8),
-        _ptr(t["feature"], C.c_int32), _ptr(t["bin"], C.c_int32),
-        _ptr(t["threshold"], C.c_float), _ptr(t["default_left"], C.c_int8),
-        _ptr(t["gain"], C.c_double), _ptr(t["weight"], C.c_double),
-        _ptr(t["sum_qg"], C.c_int64), _ptr(t["sum_qh"], C.c_int64),
-        _ptr(row_leaf, C.c_int32)), "oracle_build_tree")
+    common = (_ptr(words, C.c_uint32), n, F, bits, row_align_bits, _ptr(cv, C.c_float),
+              _ptr(cp, C.c_int32), max_bins, _ptr(qpair, C.c_int32), _ptr(sc, C.c_int32))
+    arrays = (_ptr(t["kind"], C.c_int8), _ptr(t["feature"], C.c_int32), _ptr(t["bin"], C.c_int32),
+              _ptr(t["threshold"], C.c_float), _ptr(t["default_left"], C.c_int8),
+              _ptr(t["gain"], C.c_double), _ptr(t["weight"], C.c_double),
+              _ptr(t["sum_qg"], C.c_int64), _ptr(t["sum_qh"], C.c_int64))
+    if lossguide:
+        t["left_child"] = np.full(max(cap, 1), -1, np.int32)
+        _check(lib().oracle_build_tree_lossguide(
+            *common, max_depth, max_leaves, _ptr(params, C.c_double), p_workers, *arrays,
+            _ptr(t["left_child"], C.c_int32), _ptr(row_leaf, C.c_int32)),
+            "oracle_build_tree_lossguide")
+    else:
+        _check(lib().oracle_build_tree(
+            *common, max_depth, _ptr(params, C.c_double), p_workers, *arrays,
+            _ptr(row_leaf, C.c_int32)), "oracle_build_tree")
     return t, row_leaf
 
 
@@ -271,16 +291,30 @@ def update_margins(weight: np.ndarray, row_leaf: np.ndarray, margin: np.ndarray)
 
 
 def predict(trees: list[dict], max_depth: int, base_margin: float, X: np.ndarray) -> np.ndarray:
-    """§2.4 prediction: base + sum over trees of the reached leaf weight."""
+    """§2.4 prediction: base + sum over trees of the reached leaf weight.  Trees with
+    a "left_child" array (loss-guided, R27) are walked through their links."""
     X = np.ascontiguousarray(X, dtype=np.float32)
     n, F = X.shape
+    out = np.zeros(n, np.float64)
+    if trees and "left_child" in trees[0]:
+        cap = int(trees[0]["kind"].shape[0])
+        cat = {k: np.ascontiguousarray(np.concatenate([t[k][:cap] for t in trees]))
+               for k in ("kind", "feature", "threshold", "default_left", "left_child", "weight")}
+        _check(lib().oracle_predict_linked(len(trees), cap, _ptr(cat["kind"], C.c_int8),
+                                           _ptr(cat["feature"], C.c_int32),
+                                           _ptr(cat["threshold"], C.c_float),
+                                           _ptr(cat["default_left"], C.c_int8),
+                                           _ptr(cat["left_child"], C.c_int32),
+                                           _ptr(cat["weight"], C.c_double), float(base_margin),
+                                           _ptr(X, C.c_float), n, F, _ptr(out, C.c_double)),
+               "oracle_predict_linked")
+        return out
     cap = tree_capacity(max_depth)
     if trees:
         cat = {k: np.ascontiguousarray(np.concatenate([t[k][:cap] for t in trees]))
                for k in ("kind", "feature", "threshold", "default_left", "weight")}
     else:
         cat = {k: np.zeros(1, dt) for k, dt in TREE_FIELDS}
-    out = np.zeros(n, np.float64)
     _check(lib().oracle_predict(len(trees), max_depth, _ptr(cat["kind"], C.c_int8),
                                 _ptr(cat["feature"], C.c_int32),
                                 _ptr(cat["threshold"], C.c_float),
@@ -298,13 +332,14 @@ class Booster:
 
     def __init__(self, X, y, *, max_bins, objective, max_depth, eta=0.3, reg_lambda=1.0,
                  gamma=0.0, mcw=1.0, grad_bits=15, p_workers=1, row_align_bits=32,
-                 base_margin=None):
+                 base_margin=None, grow_policy="depthwise", max_leaves=0):
         self.X = np.ascontiguousarray(X, np.float32)
         self.y = np.ascontiguousarray(y, np.float32)
         self.n, self.F = self.X.shape
         self.max_bins, self.objective, self.max_depth = max_bins, objective, max_depth
         self.eta, self.reg_lambda, self.gamma, self.mcw = eta, reg_lambda, gamma, mcw
         self.P, self.p_workers, self.row_align_bits = grad_bits, p_workers, row_align_bits
+        self.grow_policy, self.max_leaves = grow_policy, max_leaves
         self.cut_values, self.cut_ptr = cuts(self.X, max_bins)
         self.sym, self.max_symbol = symbols(self.X, self.cut_values, self.cut_ptr, max_bins)
         self.bits = symbol_bits(self.max_symbol)
@@ -322,7 +357,7 @@ class Booster:
         tree, row_leaf = build_tree(self.words, self.n, self.F, self.bits, self.row_align_bits,
                                     self.cut_values, self.cut_ptr, self.max_bins, q, sc,
                                     self.max_depth, self.eta, self.reg_lambda, self.gamma,
-                                    self.mcw, self.p_workers)
+                                    self.mcw, self.p_workers, self.grow_policy, self.max_leaves)
         self.margin = update_margins(tree["weight"], row_leaf, self.margin)
         self.trees.append(tree)
         self.last = dict(qpair=q, scale=sc, row_leaf=row_leaf)

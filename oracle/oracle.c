@@ -574,6 +574,190 @@ int oracle_build_tree(const uint32_t *words, int64_t n, int32_t F, int32_t bits,
     return OR_OK;
 }
 
+/* Loss-guided growth (the loop of Alg. 1 "reconfigurable to prioritise expanding nodes
+ * with a higher reduction in the objective function").  Readings:
+ * R25  expand_queue is a priority queue: pop = the entry of largest priority, priority = the
+ *      entry's split gain if it is expandable, else below every gain; ties to the smaller node
+ *      id.  (Non-expandable entries become leaves whenever popped, so their order is moot.)
+ * R26  an entry is expandable iff its EvaluateSplit found gain > 0, its depth < max_depth and
+ *      fewer than max_leaves - 1 expansions were made (at most max_leaves leaves).
+ * R27  node ids: root 0; the j-th expansion (j = 0, 1, ...) creates left 2j+1, right 2j+2;
+ *      left_child[k] = 2j+1 for a split node, -1 otherwise; capacity 2 max_leaves - 1.
+ * Children are evaluated iff depth + 1 < max_depth (as oracle_build_tree).  Everything else --
+ * repartition, both child histograms built directly, AllReduce order, EvaluateSplit, leaf
+ * weights -- is oracle_build_tree's. */
+int oracle_build_tree_lossguide(const uint32_t *words, int64_t n, int32_t F, int32_t bits,
+                                int32_t row_align_bits, const float *cut_values,
+                                const int32_t *cut_ptr, int32_t B, const int32_t *qpair,
+                                const int32_t *scale, int32_t max_depth, int32_t max_leaves,
+                                const double *params, int32_t p_workers, int8_t *kind,
+                                int32_t *feature, int32_t *bin, float *threshold,
+                                int8_t *default_left, double *gain, double *weight,
+                                int64_t *sum_qg, int64_t *sum_qh, int32_t *left_child,
+                                int32_t *row_leaf)
+{
+    if (n <= 0)
+        return OR_E_EMPTY;
+    if (max_depth < 0 || max_leaves < 1 || max_leaves > (1 << 20) || p_workers < 1)
+        return OR_E_ARG;
+    const double eta = params[0], lambda = params[1], gamma = params[2], mcw = params[3];
+    const int32_t sg = scale[0], sh = scale[1];
+    const int64_t stride = row_stride_bits(F, bits, row_align_bits);
+    const int32_t TB = cut_ptr[F];
+    const int64_t cap = 2 * (int64_t)max_leaves - 1;
+    for (int64_t k = 0; k < cap; k++) {
+        kind[k] = 0;
+        feature[k] = -1;
+        bin[k] = -1;
+        threshold[k] = 0.0f;
+        default_left[k] = 0;
+        gain[k] = 0.0;
+        weight[k] = 0.0;
+        sum_qg[k] = 0;
+        sum_qh[k] = 0;
+        left_child[k] = -1;
+    }
+    int64_t *hist = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1), sizeof(int64_t));
+    int64_t *part = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1), sizeof(int64_t));
+    int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    entry_t *queue = (entry_t *)malloc(sizeof(entry_t) * (size_t)cap);
+    if (!hist || !part || !rows || !queue) {
+        free(hist);
+        free(part);
+        free(rows);
+        free(queue);
+        return OR_E_NOMEM;
+    }
+    for (int64_t i = 0; i < n; i++)
+        row_leaf[i] = 0;
+
+#define BUILD_REDUCED_HIST(node_id)                                                              \
+    do {                                                                                         \
+        memset(hist, 0, sizeof(int64_t) * 2 * (size_t)TB);                                      \
+        for (int32_t w = 0; w < p_workers; w++) {                                                \
+            int64_t lo = (w * n) / p_workers, hi = ((w + 1) * n) / p_workers, m = 0;             \
+            for (int64_t i = lo; i < hi; i++)                                                    \
+                if (row_leaf[i] == (node_id))                                                    \
+                    rows[m++] = i;                                                               \
+            oracle_node_histogram(words, F, bits, row_align_bits, cut_ptr, B, qpair, rows, m,    \
+                                  part);                                                         \
+            for (int32_t t = 0; t < 2 * TB; t++)                                                 \
+                hist[t] += part[t];                                                              \
+        }                                                                                        \
+    } while (0)
+
+    entry_t root;
+    memset(&root, 0, sizeof(root));
+    for (int32_t w = 0; w < p_workers; w++) {
+        int64_t lo = (w * n) / p_workers, hi = ((w + 1) * n) / p_workers;
+        for (int64_t i = lo; i < hi; i++) {
+            root.Tg += qpair[2 * i + 0];
+            root.Th += qpair[2 * i + 1];
+        }
+    }
+    if (max_depth > 0) {
+        BUILD_REDUCED_HIST(0);
+        root.split = oracle_evaluate_split(hist, F, cut_ptr, root.Tg, root.Th, sg, sh, lambda,
+                                           gamma, mcw, root.si, &root.gain, root.sl);
+    }
+    int64_t qn = 0;         /* entries in the queue: queue[0 .. qn) */
+    int32_t expansions = 0; /* j */
+    queue[qn++] = root;
+
+    while (qn > 0) { /* while expand_queue is not empty */
+        /* expand_entry <- expand_queue.pop(): largest priority (R25) */
+        int64_t bi = -1;
+        for (int64_t q = 0; q < qn; q++) {
+            const entry_t *c = &queue[q];
+            int c_exp = c->split && c->depth < max_depth && expansions < max_leaves - 1;
+            if (!c_exp)
+                continue;
+            if (bi < 0 || c->gain > queue[bi].gain ||
+                (c->gain == queue[bi].gain && c->node < queue[bi].node))
+                bi = q;
+        }
+        if (bi < 0)
+            bi = 0; /* only non-expandable entries remain: any of them */
+        entry_t e = queue[bi];
+        queue[bi] = queue[--qn];
+        int32_t k = e.node; /* tree.insert(expand_entry) */
+        sum_qg[k] = e.Tg;
+        sum_qh[k] = e.Th;
+        weight[k] = oracle_leaf_weight(e.Tg, e.Th, sg, sh, lambda, eta);
+        if (!(e.split && e.depth < max_depth && expansions < max_leaves - 1)) {
+            kind[k] = 2;
+            continue;
+        }
+        int32_t left = 2 * expansions + 1, right = 2 * expansions + 2; /* R27 */
+        expansions++;
+        kind[k] = 1;
+        feature[k] = e.si[0];
+        bin[k] = e.si[1];
+        default_left[k] = (int8_t)e.si[2];
+        threshold[k] = cut_values[cut_ptr[e.si[0]] + e.si[1]];
+        gain[k] = e.gain;
+        left_child[k] = left;
+        for (int64_t i = 0; i < n; i++) { /* RepartitionInstances on every worker */
+            if (row_leaf[i] != k)
+                continue;
+            uint32_t s = read_symbol(words, stride, bits, i, e.si[0]);
+            int go_left = ((int32_t)s == B) ? e.si[2] : ((int32_t)s <= e.si[1]);
+            row_leaf[i] = go_left ? left : right;
+        }
+        entry_t le, re;
+        memset(&le, 0, sizeof(le));
+        memset(&re, 0, sizeof(re));
+        le.node = left;
+        re.node = right;
+        le.depth = re.depth = e.depth + 1;
+        le.Tg = e.sl[0];
+        le.Th = e.sl[1];
+        re.Tg = e.sl[2];
+        re.Th = e.sl[3];
+        if (e.depth + 1 < max_depth) {
+            BUILD_REDUCED_HIST(left);
+            le.split = oracle_evaluate_split(hist, F, cut_ptr, le.Tg, le.Th, sg, sh, lambda,
+                                             gamma, mcw, le.si, &le.gain, le.sl);
+            BUILD_REDUCED_HIST(right);
+            re.split = oracle_evaluate_split(hist, F, cut_ptr, re.Tg, re.Th, sg, sh, lambda,
+                                             gamma, mcw, re.si, &re.gain, re.sl);
+        }
+        queue[qn++] = le; /* expand_queue.push(left_expand_entry) */
+        queue[qn++] = re; /* expand_queue.push(right_expand_entry) */
+    }
+#undef BUILD_REDUCED_HIST
+    free(hist);
+    free(part);
+    free(rows);
+    free(queue);
+    return OR_OK;
+}
+
+/* Prediction over trees with explicit child links (loss-guided layout, R27): as
+ * oracle_predict, but the children of split node k are left_child[k] and left_child[k] + 1;
+ * trees are concatenated arrays of capacity cap each. */
+int oracle_predict_linked(int32_t n_trees, int64_t cap, const int8_t *kind, const int32_t *feature,
+                          const float *threshold, const int8_t *default_left,
+                          const int32_t *left_child, const double *weight, double base_margin,
+                          const float *X, int64_t n, int32_t F, double *margin)
+{
+    for (int64_t i = 0; i < n; i++) {
+        double m = base_margin;
+        for (int32_t t = 0; t < n_trees; t++) {
+            int64_t o = t * cap, k = 0;
+            while (kind[o + k] == 1) {
+                int32_t f = feature[o + k];
+                float v = f < F ? X[i * F + f] : NAN;
+                int go_left = isnan(v) ? default_left[o + k] : (v <= threshold[o + k]);
+                k = go_left ? left_child[o + k] : left_child[o + k] + 1;
+            }
+            m = m + weight[o + k];
+        }
+        margin[i] = m;
+    }
+    return OR_OK;
+}
+
 /* Margin update (Q6): margin[i] = margin[i] + w[row_leaf[i]] in fp64. */
 int oracle_update_margins(const double *weight, const int32_t *row_leaf, int64_t n,
                           double *margin)
