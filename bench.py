@@ -52,6 +52,12 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=500_000)
     ap.add_argument("--cpu-rounds", type=int, default=3)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--grow-policy", default="depthwise", choices=["depthwise", "lossguide"],
+                    help="lossguide: priority-queue growth (P:65) with --max-leaves")
+    ap.add_argument("--max-leaves", type=int, default=None,
+                    help="lossguide leaf budget (default 2^max_depth of the config)")
+    ap.add_argument("--max-depth", type=int, default=None,
+                    help="depth limit (default: the config's; lossguide default 16)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     return a
@@ -159,9 +165,10 @@ def run_ours(a, world, rank, local):
     ctx = G.Context(local)
     if world > 1:
         ctx.comm_init_from_torch()
-    kw = dict(max_bins=cfg.max_bins, objective=cfg.objective, max_depth=cfg.max_depth,
+    kw = dict(max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
               eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
-              min_child_weight=cfg.min_child_weight, grad_bits=a.grad_bits, base_margin=beta)
+              min_child_weight=cfg.min_child_weight, grad_bits=a.grad_bits, base_margin=beta,
+              grow_policy=a.grow_policy, max_leaves=a.leaves)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -289,7 +296,7 @@ def run_ours(a, world, rank, local):
     if not a.no_e2e:
         Xh = torch.from_numpy(X).pin_memory()
         yh = torch.from_numpy(y).pin_memory()
-        cap = (1 << (cfg.max_depth + 1)) - 1
+        cap = 2 * a.leaves - 1 if a.grow_policy == "lossguide" else (1 << (a.depth + 1)) - 1
         host_trees = {nm: torch.empty((a.steps, cap), dtype=dt, pin_memory=True)
                       for nm, dt in G.TREE_FIELDS}
         barrier()
@@ -325,20 +332,21 @@ def run_ours(a, world, rank, local):
     # ---- CPU baseline: the oracle as it stands, on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(a.config, min(a.cpu_rows, n), a.cpu_rounds, n)
+        cpu = cpu_baseline(a.config, min(a.cpu_rows, n), a.cpu_rounds, n, a)
     return dict(ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages,
                 one_time=one_time, clocks=clk, launches=launches, e2e=e2e, cpu=cpu,
                 predict_ms=predict_ms, allreduce_ms=allreduce_ms, grad_bits=a.grad_bits)
 
 
-def cpu_baseline(config, rows, rounds, n_full):
+def cpu_baseline(config, rows, rounds, n_full, a):
     import oracle as O
     cfg = W.CONFIGS[config]
     X, y = W.generate(config, 0, rows, n_rows=max(rows, cfg.n_rows))
     beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
     b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective,
-                  max_depth=cfg.max_depth, eta=cfg.eta, reg_lambda=cfg.reg_lambda,
-                  gamma=cfg.gamma, mcw=cfg.min_child_weight, base_margin=beta)
+                  max_depth=a.depth, eta=cfg.eta, reg_lambda=cfg.reg_lambda,
+                  gamma=cfg.gamma, mcw=cfg.min_child_weight, base_margin=beta,
+                  grow_policy=a.grow_policy, max_leaves=a.leaves)
     t = time.perf_counter()
     for _ in range(rounds):
         b.round()
@@ -356,12 +364,15 @@ def run_reference(a):
     n = a.rows or cfg.n_rows
     budget_s = 90.0   # whole --steps K --warmup W run (plus ~10 s of preparation)
     per_row = 4.5e-6 * (cfg.n_features / 28.0) * (cfg.max_depth / 6.0)
+    if a.grow_policy == "lossguide":  # one partition / histogram pass per expansion
+        per_row *= max(1.0, a.leaves / 2 ** cfg.max_depth) * 2
     rows = int(min(n, 2_000_000, max(20_000, budget_s / (a.steps + a.warmup) / per_row)))
     X, y = W.generate(a.config, 0, rows, n_rows=max(rows, cfg.n_rows))
     beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
-    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective, max_depth=cfg.max_depth,
+    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
                   eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
-                  mcw=cfg.min_child_weight, base_margin=beta)
+                  mcw=cfg.min_child_weight, base_margin=beta, grow_policy=a.grow_policy,
+                  max_leaves=a.leaves)
     for _ in range(a.warmup):
         b.round()
     t = time.perf_counter()
@@ -371,13 +382,13 @@ def run_reference(a):
     value = per * n / rows
     sample = (f"each step = one oracle boosting round on the first {rows} of {n} rows "
               f"({per:.3f} s measured), scaled x{n / rows:.1f} to the full workload")
-    out = {"metric": METRIC, "value": value, "unit": "s/round", "n_gpus": 0, "steps": a.steps,
+    out = {"metric": metric_of(a), "value": value, "unit": "s/round", "n_gpus": 0, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": a.config, "rows": n, "features": cfg.n_features,
-                      "max_bins": cfg.max_bins, "max_depth": cfg.max_depth,
-                      "objective": cfg.objective},
+                      "max_bins": cfg.max_bins, "max_depth": a.depth,
+                      "objective": cfg.objective, **policy_keys(a)},
            "cpu_baseline": {"value": value, "unit": "s/round", "cores": 1, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": value, "unit": "s/round", "h2d_bytes_per_step": 0,
@@ -386,8 +397,26 @@ def run_reference(a):
     return 0
 
 
+def metric_of(a):
+    if a.grow_policy == "lossguide":
+        return (f"sec/boosting round (loss-guided, {a.leaves} leaves, depth <= {a.depth}, 256 bins); "
+                "histogram GB/s vs HBM peak")
+    return METRIC
+
+
+def policy_keys(a):
+    if a.grow_policy == "lossguide":
+        return {"grow_policy": "lossguide", "max_leaves": a.leaves}
+    return {}
+
+
 def main():
     a = parse()
+    cfg0 = W.CONFIGS[a.config]
+    a.depth = a.max_depth if a.max_depth is not None else (
+        16 if a.grow_policy == "lossguide" else cfg0.max_depth)
+    a.leaves = a.max_leaves if a.max_leaves is not None else (
+        2 ** cfg0.max_depth if a.grow_policy == "lossguide" else 0)
     world, rank, local = dist_env()
     if world > 1:
         import torch
@@ -406,7 +435,7 @@ def main():
     if rank == 0:
         cfg = W.CONFIGS[a.config]
         out = {
-            "metric": METRIC,
+            "metric": metric_of(a),
             "value": r["ms_step"] / 1e3,
             "unit": "s/round",
             "n_gpus": world,
@@ -419,7 +448,7 @@ def main():
             "dtype": "int64",
             "data": "synthetic",
             "config": {"workload": a.config, "rows": r["n"], "features": cfg.n_features,
-                       "max_bins": cfg.max_bins, "max_depth": cfg.max_depth,
+                       "max_bins": cfg.max_bins, "max_depth": a.depth, **policy_keys(a),
                        "objective": cfg.objective, "eta": cfg.eta, "grad_bits": r["grad_bits"],
                        "parallelism": f"dp{world} (rows sharded, NCCL histogram allreduce)",
                        "l2": "inputs larger than L2 (packed matrix + per-row state > 126 MB)"},

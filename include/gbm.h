@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GBM_ABI_VERSION 1
+#define GBM_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define GBM_API __attribute__((visibility("default")))
@@ -55,6 +55,7 @@ enum {
 
 enum { GBM_SQUARED_ERROR = 0, GBM_LOGISTIC = 1 };   /* objectives */
 enum { GBM_NODE_ABSENT = 0, GBM_NODE_SPLIT = 1, GBM_NODE_LEAF = 2 };
+enum { GBM_GROW_DEPTHWISE = 0, GBM_GROW_LOSSGUIDE = 1 };  /* tree growth policies      */
 
 typedef struct gbm_ctx gbm_ctx;
 
@@ -187,10 +188,13 @@ GBM_API int gbm_transpose_symbols(gbm_ctx *ctx, const gbm_qmatrix *qm, uint8_t *
 
 typedef struct {
     int32_t objective;         /* GBM_SQUARED_ERROR | GBM_LOGISTIC                          */
-    int32_t max_depth;         /* D >= 0: root depth 0, at most 2^D leaves (R23)            */
+    int32_t max_depth;         /* D >= 0: root depth 0, no node deeper than D (R23)         */
     int32_t grad_bits;         /* fixed-point precision P of the gradient pairs (R14); 1..30 */
-    int32_t reserved;
+    int32_t grow_policy;       /* GBM_GROW_DEPTHWISE (0, the zero-initialised default) or   */
+                               /* GBM_GROW_LOSSGUIDE (R25-R27)                          */
     double eta, lambda, gamma, min_child_weight;   /* S:311-314, defaults 0.3/1/0/1 */
+    int32_t max_leaves;        /* lossguide: at most this many leaves, 1..65536      */
+    int32_t reserved;          /* 0                                                          */
 } gbm_params;
 
 /* ---------------------------------------------------------------- §2.5 gradients
@@ -207,11 +211,15 @@ GBM_API int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, co
                   void *stream);
 
 /* ---------------------------------------------------------------- §2.3 trees (Alg. 1)
- * A tree is a set of DEVICE arrays in heap order (root 0, children 2k+1 / 2k+2) of capacity
- * 2^(max_depth+1) - 1.  kind: GBM_NODE_*.  For split nodes: feature, bin, threshold =
- * cuts_feature[bin], default_left, gain.  For every present node: weight (R11: -G/(H+lambda)
- * * eta, the leaf value for leaves), sum_qg / sum_qh (the node's fixed-point totals over all
- * ranks).  Absent slots: kind 0, feature/bin -1, other fields 0. */
+ * A tree is a set of DEVICE arrays.  Depth-wise: heap order (root 0, children 2k+1 / 2k+2),
+ * capacity 2^(max_depth+1) - 1.  Loss-guided (R27): root 0, the j-th expansion (j = 0, 1, ...)
+ * creates children 2j+1 (left) and 2j+2 (right), capacity 2*max_leaves - 1.  kind: GBM_NODE_*.
+ * For split nodes: feature, bin, threshold = cuts_feature[bin], default_left, gain, and
+ * left_child (the right child is left_child + 1).  For every present node: weight (R11:
+ * -G/(H+lambda) * eta, the leaf value for leaves), sum_qg / sum_qh (the node's fixed-point
+ * totals over all ranks).  Absent slots and leaves: feature/bin/left_child -1, gain 0; absent
+ * slots kind 0 and every other field 0.  left_child may be NULL for depth-wise trees (then it
+ * is not written); loss-guided trees require it. */
 typedef struct {
     int8_t *kind;
     int32_t *feature;
@@ -222,13 +230,19 @@ typedef struct {
     double *weight;
     int64_t *sum_qg;
     int64_t *sum_qh;
+    int32_t *left_child;
 } gbm_tree;
 
-/* gbm_build_tree: Algorithm 1, grown depth-wise and level-synchronously (R15):
- * InitRoot; then per level: RepartitionInstances (stable), BuildPartialHistograms of the
- * smaller child of every split (R17), AllReduceHistograms (collective: one NCCL int64 sum per
- * level), sibling histogram = parent - built child (north star), EvaluateSplit for every node
- * of the level (R8-R10).  row_leaf_d int32 [n_rows] receives the leaf each row ends in.
+/* gbm_build_tree: Algorithm 1.
+ * Depth-wise (grow_policy 0), level-synchronously (R15): InitRoot; then per level:
+ * RepartitionInstances (stable), BuildPartialHistograms of the smaller child of every split
+ * (R17), AllReduceHistograms (collective: one NCCL int64 sum per level), sibling histogram =
+ * parent - built child (north star), EvaluateSplit for every node of the level (R8-R10).
+ * Loss-guided (grow_policy 1, R25-R27): max_leaves - 1 expansion steps, each: pop the
+ * open node of largest gain (selected on the device), repartition its rows, build the smaller
+ * child's histogram, one allreduce, sibling by subtraction, evaluate both children.  Uses the
+ * compact histogram layout whatever GBM_OPT_HIST_LAYOUT says.
+ * row_leaf_d int32 [n_rows] receives the leaf each row ends in.
  * Asynchronous (no host synchronisation inside a tree). */
 GBM_API int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *qm, const int32_t *qpair_d,
                    const int32_t *scale_d, const gbm_params *params, const gbm_tree *tree,
@@ -272,6 +286,16 @@ GBM_API int gbm_predict(gbm_ctx *ctx, int32_t n_trees, int32_t max_depth, const 
                 const int32_t *feature_d, const float *threshold_d, const int8_t *default_left_d,
                 const double *weight_d, double base_margin, const float *X_d, int64_t n_rows,
                 int32_t n_features, double *margin_d, void *stream);
+
+/* gbm_predict_linked: as gbm_predict for trees with explicit child links (the loss-guided
+ * layout, R27; depth-wise trees written with left_child work too): the children of split node
+ * k are left_child[k] and left_child[k] + 1.  Trees are concatenated device arrays of capacity
+ * `cap` each. */
+GBM_API int gbm_predict_linked(gbm_ctx *ctx, int32_t n_trees, int64_t cap, const int8_t *kind_d,
+                       const int32_t *feature_d, const float *threshold_d,
+                       const int8_t *default_left_d, const int32_t *left_child_d,
+                       const double *weight_d, double base_margin, const float *X_d,
+                       int64_t n_rows, int32_t n_features, double *margin_d, void *stream);
 
 #ifdef __cplusplus
 }

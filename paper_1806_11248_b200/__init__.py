@@ -38,8 +38,9 @@ class GbmError(RuntimeError):
 
 class _Params(C.Structure):
     _fields_ = [("objective", C.c_int32), ("max_depth", C.c_int32), ("grad_bits", C.c_int32),
-                ("reserved", C.c_int32), ("eta", C.c_double), ("reg_lambda", C.c_double),
-                ("gamma", C.c_double), ("min_child_weight", C.c_double)]
+                ("grow_policy", C.c_int32), ("eta", C.c_double), ("reg_lambda", C.c_double),
+                ("gamma", C.c_double), ("min_child_weight", C.c_double),
+                ("max_leaves", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _QM(C.Structure):
@@ -51,7 +52,7 @@ class _QM(C.Structure):
 
 class _Tree(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("kind", "feature", "bin", "threshold", "default_left",
-                                          "gain", "weight", "sum_qg", "sum_qh")]
+                                          "gain", "weight", "sum_qg", "sum_qh", "left_child")]
 
 
 class _ProfEntry(C.Structure):
@@ -104,6 +105,9 @@ EXPORTS = {
     "gbm_predict": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                               C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    "gbm_predict_linked": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                     C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
 }
 
 
@@ -157,9 +161,14 @@ def packed_words(n_rows: int, n_features: int, bits: int, row_align_bits: int = 
     return int(w)
 
 
-def _params(objective, max_depth, eta, reg_lambda, gamma, mcw, grad_bits):
-    return _Params(OBJECTIVES.get(objective, objective), max_depth, grad_bits, 0, eta,
-                   reg_lambda, gamma, mcw)
+GROW_POLICIES = {"depthwise": 0, "lossguide": 1}
+
+
+def _params(objective, max_depth, eta, reg_lambda, gamma, mcw, grad_bits, grow_policy="depthwise",
+            max_leaves=0):
+    return _Params(OBJECTIVES.get(objective, objective), max_depth, grad_bits,
+                   GROW_POLICIES.get(grow_policy, grow_policy), eta, reg_lambda, gamma, mcw,
+                   max_leaves, 0)
 
 
 @dataclasses.dataclass
@@ -193,15 +202,17 @@ class QMatrix:
 TREE_FIELDS = (("kind", torch.int8), ("feature", torch.int32), ("bin", torch.int32),
                ("threshold", torch.float32), ("default_left", torch.int8),
                ("gain", torch.float64), ("weight", torch.float64), ("sum_qg", torch.int64),
-               ("sum_qh", torch.int64))
+               ("sum_qh", torch.int64), ("left_child", torch.int32))
 
 
 class Tree:
-    """Heap-ordered device arrays of one tree (capacity 2^(D+1)-1)."""
+    """Device arrays of one tree.  Depth-wise: heap order, capacity 2^(D+1)-1.  Loss-guided
+    (max_leaves > 0, R27): children of the j-th expansion at 2j+1 / 2j+2, capacity
+    2*max_leaves-1.  left_child links the children in both layouts (-1 for leaves)."""
 
-    def __init__(self, max_depth: int, device):
-        cap = (1 << (max_depth + 1)) - 1
-        self.max_depth = max_depth
+    def __init__(self, max_depth: int, device, max_leaves: int = 0):
+        cap = 2 * max_leaves - 1 if max_leaves > 0 else (1 << (max_depth + 1)) - 1
+        self.max_depth, self.max_leaves, self.capacity = max_depth, max_leaves, cap
         self.arrays = {n: torch.empty(cap, dtype=dt, device=device) for n, dt in TREE_FIELDS}
 
     def c(self) -> _Tree:
@@ -363,11 +374,15 @@ class Context:
     # ------------------------------------------------------------ §2.3
     def build_tree(self, qm: QMatrix, qpair, scale, *, objective, max_depth, eta=0.3,
                    reg_lambda=1.0, gamma=0.0, min_child_weight=1.0,
-                   grad_bits=DEFAULT_GRAD_BITS, tree: Tree | None = None, row_leaf=None):
-        tree = tree if tree is not None else Tree(max_depth, self.dev)
+                   grad_bits=DEFAULT_GRAD_BITS, tree: Tree | None = None, row_leaf=None,
+                   grow_policy="depthwise", max_leaves=0):
+        lossguide = GROW_POLICIES.get(grow_policy, grow_policy) == 1
+        tree = tree if tree is not None else Tree(max_depth, self.dev,
+                                                  max_leaves if lossguide else 0)
         rl = row_leaf if row_leaf is not None else torch.empty(qm.n_rows, dtype=torch.int32,
                                                                device=self.dev)
-        prm = _params(objective, max_depth, eta, reg_lambda, gamma, min_child_weight, grad_bits)
+        prm = _params(objective, max_depth, eta, reg_lambda, gamma, min_child_weight, grad_bits,
+                      grow_policy, max_leaves)
         qc, tc = qm.c(), tree.c()
         _call("gbm_build_tree", self.h, C.byref(qc), _p(qpair), _p(scale), C.byref(prm),
               C.byref(tc), _p(rl), _stream())
@@ -416,6 +431,14 @@ class Context:
     def predict(self, trees: list[Tree], max_depth: int, base_margin: float, X: torch.Tensor):
         n, F = X.shape
         out = torch.empty(n, dtype=torch.float64, device=self.dev)
+        if trees and trees[0].max_leaves > 0:  # loss-guided layout: follow the links
+            names = ("kind", "feature", "threshold", "default_left", "left_child", "weight")
+            cat = {k: torch.cat([t[k] for t in trees]) for k in names}
+            _call("gbm_predict_linked", self.h, len(trees), trees[0].capacity, _p(cat["kind"]),
+                  _p(cat["feature"]), _p(cat["threshold"]), _p(cat["default_left"]),
+                  _p(cat["left_child"]), _p(cat["weight"]), float(base_margin), _p(X), n, F,
+                  _p(out), _stream())
+            return out
         if trees:
             cat = {k: torch.cat([t[k] for t in trees]) for k in
                    ("kind", "feature", "threshold", "default_left", "weight")}
@@ -455,11 +478,12 @@ class Booster:
     def __init__(self, ctx: Context, X: torch.Tensor, y: torch.Tensor, *, max_bins: int,
                  objective: str, max_depth: int, eta=0.3, reg_lambda=1.0, gamma=0.0,
                  min_child_weight=1.0, grad_bits=DEFAULT_GRAD_BITS, row_align_bits=32,
-                 base_margin=0.0, cuts=None, colsym=True):
+                 base_margin=0.0, cuts=None, colsym=True, grow_policy="depthwise", max_leaves=0):
         self.ctx, self.y = ctx, y
         self.objective, self.max_depth, self.grad_bits = objective, max_depth, grad_bits
         self.kw = dict(eta=eta, reg_lambda=reg_lambda, gamma=gamma,
-                       min_child_weight=min_child_weight)
+                       min_child_weight=min_child_weight, grow_policy=grow_policy,
+                       max_leaves=max_leaves)
         self.qm = ctx.make_qmatrix(X, max_bins, row_align_bits, cuts=cuts, colsym=colsym)
         self.base_margin = float(base_margin)
         n = X.shape[0]

@@ -128,11 +128,13 @@ __global__ void update_margins_kernel(const double *__restrict__ w, const int32_
         margin[i] = dadd(margin[i], __ldg(w + __ldg(leaf + i)));
 }
 
+// LINKED: children of k are left_child[k], left_child[k] + 1 (R27); else heap 2k+1, 2k+2
+template <bool LINKED>
 __global__ void predict_kernel(int n_trees, long long cap, const int8_t *__restrict__ kind,
                                const int32_t *__restrict__ feature, const float *__restrict__ thr,
-                               const int8_t *__restrict__ dl, const double *__restrict__ weight,
-                               double base, const float *__restrict__ X, long long n, int F,
-                               double *__restrict__ out) {
+                               const int8_t *__restrict__ dl, const int32_t *__restrict__ left_child,
+                               const double *__restrict__ weight, double base, const float *__restrict__ X,
+                               long long n, int F, double *__restrict__ out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const float *x = X + i * F;
@@ -143,7 +145,12 @@ __global__ void predict_kernel(int n_trees, long long cap, const int8_t *__restr
                 int f = __ldg(feature + o + k);
                 float v = f < F ? __ldg(x + f) : __int_as_float(0x7fffffff);
                 bool left = isnan(v) ? (__ldg(dl + o + k) != 0) : (v <= __ldg(thr + o + k));
-                k = left ? 2 * k + 1 : 2 * k + 2;
+                if (LINKED) {
+                    const long long c = __ldg(left_child + o + k);
+                    k = left ? c : c + 1;
+                } else {
+                    k = left ? 2 * k + 1 : 2 * k + 2;
+                }
             }
             m = dadd(m, __ldg(weight + o + k));
         }
@@ -222,9 +229,29 @@ int gbm_predict(gbm_ctx *ctx, int32_t n_trees, int32_t max_depth, const int8_t *
     if (n_rows == 0) return GBM_OK;
     long long cap = (1ll << (max_depth + 1)) - 1;
     ProfScope ps(ctx, PC_PREDICT, (cudaStream_t)stream, (double)n_rows * (4.0 * n_features + 8.0));
-    predict_kernel<<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
-        n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, weight_d, base_margin, X_d,
+    predict_kernel<false><<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
+        n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, nullptr, weight_d, base_margin, X_d,
         n_rows, n_features, margin_d);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
+int gbm_predict_linked(gbm_ctx *ctx, int32_t n_trees, int64_t cap, const int8_t *kind_d,
+                       const int32_t *feature_d, const float *threshold_d, const int8_t *default_left_d,
+                       const int32_t *left_child_d, const double *weight_d, double base_margin,
+                       const float *X_d, int64_t n_rows, int32_t n_features, double *margin_d, void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(n_trees >= 0 && cap >= 1 && n_rows >= 0 && n_features > 0, GBM_E_ARG,
+                "gbm_predict_linked: bad sizes");
+    GBM_REQUIRE(margin_d && (X_d || n_rows == 0) &&
+                    (n_trees == 0 || (kind_d && feature_d && threshold_d && default_left_d && left_child_d &&
+                                      weight_d)),
+                GBM_E_ARG, "gbm_predict_linked: null pointer");
+    if (n_rows == 0) return GBM_OK;
+    ProfScope ps(ctx, PC_PREDICT, (cudaStream_t)stream, (double)n_rows * (4.0 * n_features + 8.0));
+    predict_kernel<true><<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
+        n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, left_child_d, weight_d, base_margin,
+        X_d, n_rows, n_features, margin_d);
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }

@@ -42,6 +42,23 @@ struct NodeDev {
     int pad;
 };
 
+// Loss-guided growth (R25-R27).  A node evaluated with a positive-gain split that may still be
+// expanded is OPEN until the step kernel selects it (then SPLIT) -- internal state only.
+constexpr int NODE_OPEN = 3;
+struct LgNode {        // per node, loss-guided only
+    double gain;       // best split gain (OPEN nodes)
+    long long Lg, Lh;  // left child totals of that split
+    int depth;
+    int hslot;         // histogram pool slot (nodes that may be expanded)
+    int buf;           // ridx buffer holding the node's rows: 0 / 1, -1 = identity (root)
+    int pad;
+};
+struct StepDev {       // the expansion of the current step, written by lg_select_kernel
+    int k;             // parent (-1: nothing left to expand -- every later launch is a no-op)
+    int c;             // its left child (2j+1); right = c + 1
+    int in_buf, out_buf;
+};
+
 struct RangeItem {  // rows [start, start+len) of a row source, one feature group
     int slot, group;
     long long start;
@@ -451,6 +468,8 @@ struct FusedArgs {
     int n_groups, run_tiles;
     const int *n_items;
     const void *ridx_in;      // entries (EntryOf<CARRY>), null = identity (level 1)
+    const StepDev *step;      // loss-guided: parent and ridx buffer come from the device
+    const void *bufs[2];      // loss-guided: the two ridx buffers
     uint32_t *flags;          // [tiles][PT/32]
     int *tile_left;           // [tiles]
     int32_t *row_leaf;
@@ -476,6 +495,11 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
     __shared__ int s_off[2049];
     __shared__ E s_rows[H_THREADS / 32][WROWS];
     const E *rin = static_cast<const E *>(a.ridx_in);
+    int first = a.first;
+    if (a.step) {  // loss-guided step (n_par = 1): no items at all when nothing is expanded
+        first = a.step->k;
+        rin = a.step->in_buf < 0 ? nullptr : static_cast<const E *>(a.bufs[a.step->in_buf]);
+    }
     const QM &qm = a.qm;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int n_items = *a.n_items;
@@ -484,7 +508,7 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
          it = claim_item(const_cast<int *>(a.n_items) + 1)) {
         const int run = it / a.n_groups, g = it - run * a.n_groups;
         const int j = find_parent(a.run_base, a.n_par, run);
-        const int k = a.first + j;
+        const int k = first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
         const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
@@ -1338,11 +1362,18 @@ __device__ __forceinline__ long long block_exscan(long long v, long long *total,
 // one block per parent: exclusive scan of its tiles' left counts; children segments
 __global__ void __launch_bounds__(1024) part_scan_kernel(NodeDev *__restrict__ nodes, int first,
                                                          const int *__restrict__ tile_base,
-                                                         const int *__restrict__ tile_left, int *__restrict__ tile_off) {
+                                                         const int *__restrict__ tile_left, int *__restrict__ tile_off,
+                                                         const StepDev *__restrict__ step) {
     __shared__ long long sm32[32];
-    const int j = blockIdx.x, k = first + j;
+    const int j = blockIdx.x;
+    int k = first + j, c = 2 * k + 1;
+    if (step) {  // loss-guided: the step's parent and its children 2j+1, 2j+2
+        k = step->k;
+        c = step->c;
+        if (k < 0) return;
+    }
     const NodeDev nd = nodes[k];
-    NodeDev *Lc = nodes + 2 * k + 1, *Rc = nodes + 2 * k + 2;
+    NodeDev *Lc = nodes + c, *Rc = nodes + c + 1;
     if (nd.state != GBM_NODE_SPLIT) {
         if (threadIdx.x == 0) {
             Lc->count = 0; Lc->start = 0; Lc->state = GBM_NODE_ABSENT;
@@ -1385,18 +1416,24 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
     const NodeDev *__restrict__ nodes, int first, int n_par, const int *__restrict__ tile_base,
     const uint32_t *__restrict__ flags, const int *__restrict__ tile_off,
     const typename EntryOf<CARRY>::T *__restrict__ ridx_in, typename EntryOf<CARRY>::T *__restrict__ ridx_out,
-    const int2 *__restrict__ qpair, unsigned long long *__restrict__ rows_ctr) {
+    const int2 *__restrict__ qpair, unsigned long long *__restrict__ rows_ctr,
+    const StepDev *__restrict__ step = nullptr, void *buf0 = nullptr, void *buf1 = nullptr) {
     using E = typename EntryOf<CARRY>::T;
     constexpr int WPW = PT / 32 / (P_THREADS / 32);  // flag words per warp (8)
+    if (step) {  // loss-guided: rows move from the parent's buffer to the other one
+        const int ib = step->in_buf, ob = step->out_buf;
+        ridx_in = ib < 0 ? nullptr : static_cast<const E *>(ib ? buf1 : buf0);
+        ridx_out = static_cast<E *>(ob ? buf1 : buf0);
+    }
     __shared__ int wpre[PT / 32];
     const int n_tiles = tile_base[n_par];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int j = find_parent(tile_base, n_par, t);
-        const int k = first + j;
+        const int k = step ? step->k : first + j;
         const NodeDev nd = nodes[k];
         if (nd.state != GBM_NODE_SPLIT) continue;  // uniform per block
-        const long long n_left = nodes[2 * k + 1].count;
+        const long long n_left = nodes[step ? step->c : 2 * k + 1].count;
         const int lt = t - tile_base[j];
         if (rows_ctr && threadIdx.x == 0)
             atomicAdd(rows_ctr, (unsigned long long)min((long long)PT, nd.count - (long long)lt * PT));
@@ -1606,6 +1643,9 @@ struct EvalArgs {
     const long long *hist_direct;   // direct mode: [n_nodes][TB][2]
     const long long *totals_direct; // direct mode: [n_nodes][2]
     FeatBest *fb;                   // [n_nodes][F]
+    LgNode *lg;                     // loss-guided mode (null = depth-wise)
+    const StepDev *step;            // loss-guided: the current expansion
+    long long *hist_pool;           // loss-guided: [max_leaves][TB][2] by LgNode::hslot
 };
 
 // Node j's histogram source and totals; false if the node does not exist.
@@ -1619,6 +1659,22 @@ __device__ __forceinline__ bool node_source(const EvalArgs &a, int j, NodeHist &
         return true;
     }
     const int k = a.first + j;
+    if (a.lg && a.level > 0) {  // loss-guided child k of the step's parent
+        const int pk = a.step->k;
+        if (pk < 0) return false;
+        Tg = a.nodes[k].Tg;
+        Th = a.nodes[k].Th;
+        const bool is_left = k == a.step->c;
+        const bool built = a.nodes[pk].build_left ? is_left : !is_left;
+        if (built) {
+            src.direct = a.hist_build;
+        } else {  // in place: the sibling's histogram replaces the parent's in its pool slot
+            src.parent = a.hist_pool + (long long)a.lg[pk].hslot * a.TB * 2;
+            src.build = a.hist_build;
+        }
+        if (a.lg[k].depth < a.p.max_depth) src.store = a.hist_pool + (long long)a.lg[k].hslot * a.TB * 2;
+        return true;
+    }
     if (a.level == 0) {
         src.direct = a.hist_root;
         Tg = a.hist_root[2 * a.TB];
@@ -1651,6 +1707,7 @@ __global__ void __launch_bounds__(E_THREADS) eval_feat_kernel(EvalArgs a) {
     NodeHist src;
     long long Tg, Th;
     if (!node_source(a, j, src, Tg, Th)) return;
+    if (a.lg && a.lg[a.first + j].depth >= a.p.max_depth) return;  // a leaf: not evaluated
     const int sg = a.scale[0], sh = a.scale[1];
     const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
     const double e = ddiv(dmul(G, G), dadd(H, a.p.lambda));
@@ -1675,6 +1732,7 @@ struct TreeDev {
     int8_t *default_left;
     double *gain, *weight;
     long long *sum_qg, *sum_qh;
+    int32_t *left_child;  // optional for depth-wise trees
 };
 
 __device__ __forceinline__ void write_leaf(const TreeDev &t, int k, long long Tg, long long Th, int sg, int sh,
@@ -1760,7 +1818,7 @@ __device__ void eval_final_body(const EvalArgs &a, const TreeDev &t) {
     }
     const int sg = a.scale[0], sh = a.scale[1];
     const EvalParams &p = a.p;
-    if (a.level >= p.max_depth) {  // max_depth == 0: the root is a leaf
+    if ((a.lg ? a.lg[k].depth : a.level) >= p.max_depth) {  // max_depth == 0: the root is a leaf
         if (threadIdx.x == 0) {
             write_leaf(t, k, Tg, Th, sg, sh, p);
             a.nodes[k].state = GBM_NODE_LEAF;
@@ -1786,12 +1844,25 @@ __device__ void eval_final_body(const EvalArgs &a, const TreeDev &t) {
     const int gbin = (int)(b.idx >> 1), dl = (b.idx & 1) == 0;
     const int f = feature_of_bin(a.cut_ptr, a.F, gbin);
     const int bb = gbin - __ldg(a.cut_ptr + f);
+    if (a.lg) {  // loss-guided: a leaf until lg_select_kernel pops it (R25)
+        t.kind[k] = GBM_NODE_LEAF;
+        nd.state = NODE_OPEN;
+        nd.f = f;
+        nd.b = bb;
+        nd.dl = dl;
+        nd.build_left = b.Lh <= Th - b.Lh;  // smaller hessian sum; ties -> left (R17)
+        a.lg[k].gain = b.gain;
+        a.lg[k].Lg = b.Lg;
+        a.lg[k].Lh = b.Lh;
+        return;
+    }
     t.kind[k] = GBM_NODE_SPLIT;
     t.feature[k] = f;
     t.bin[k] = bb;
     t.threshold[k] = __ldg(a.cut_values + gbin);
     t.default_left[k] = (int8_t)dl;
     t.gain[k] = b.gain;
+    if (t.left_child) t.left_child[k] = 2 * k + 1;
     nd.state = GBM_NODE_SPLIT;
     nd.f = f;
     nd.b = bb;
@@ -1847,12 +1918,126 @@ __global__ void init_tree_kernel(TreeDev t, long long cap, NodeDev *nodes, long 
         t.weight[k] = 0.0;
         t.sum_qg[k] = 0;
         t.sum_qh[k] = 0;
+        if (t.left_child) t.left_child[k] = -1;
         NodeDev nd = {};
         nodes[k] = nd;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         nodes[0].start = 0;
         nodes[0].count = n_rows;
+    }
+}
+
+// ============================================================== loss-guided growth (R25-R27)
+__global__ void lg_init_kernel(LgNode *__restrict__ lg, long long cap) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < cap;
+         k += (long long)gridDim.x * blockDim.x) {
+        LgNode z = {};
+        z.buf = k == 0 ? -1 : 0;  // the root's rows are the identity list
+        lg[k] = z;
+    }
+}
+
+// Step s: expand_queue.pop() -- the OPEN node of largest gain, ties to the smaller id (R25) --
+// made a split node with children 2s+1, 2s+2 (R27); plans the step's single-parent partition.
+// With nothing OPEN the step is void: k = -1 and zero work items, so every later launch of the
+// step returns at once (the host enqueues a fixed max_leaves - 1 steps: graph-capturable).
+__global__ void __launch_bounds__(1024) lg_select_kernel(NodeDev *__restrict__ nodes, LgNode *__restrict__ lg,
+                                                         TreeDev t, const int32_t *__restrict__ cut_ptr,
+                                                         const float *__restrict__ cut_values, int s, int n_groups,
+                                                         int run_tiles, StepDev *__restrict__ step,
+                                                         int *__restrict__ tile_base, int *__restrict__ run_base,
+                                                         int *__restrict__ n_items) {
+    __shared__ double s_g[32];
+    __shared__ int s_k[32];
+    const int n_nodes = 2 * s + 1;
+    double bg = 0.0;
+    int bk = -1;
+    auto take = [&](double g, int k) {
+        if (k >= 0 && (bk < 0 || g > bg || (g == bg && k < bk))) {
+            bg = g;
+            bk = k;
+        }
+    };
+    for (int k = threadIdx.x; k < n_nodes; k += blockDim.x)
+        if (nodes[k].state == NODE_OPEN) take(lg[k].gain, k);
+    for (int o = 16; o > 0; o >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        take(og, ok);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_g[w] = bg;
+        s_k[w] = bk;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) take(s_g[i], s_k[i]);
+    const int c = 2 * s + 1;
+    if (bk < 0) {
+        step->k = -1;
+        step->c = c;
+        step->in_buf = step->out_buf = 0;
+        tile_base[0] = tile_base[1] = 0;
+        run_base[0] = run_base[1] = 0;
+        n_items[0] = n_items[1] = 0;
+        return;
+    }
+    const int k = bk;
+    NodeDev &nd = nodes[k];
+    nd.state = GBM_NODE_SPLIT;
+    t.kind[k] = GBM_NODE_SPLIT;
+    t.feature[k] = nd.f;
+    t.bin[k] = nd.b;
+    t.threshold[k] = __ldg(cut_values + __ldg(cut_ptr + nd.f) + nd.b);
+    t.default_left[k] = (int8_t)nd.dl;
+    t.gain[k] = lg[k].gain;
+    t.left_child[k] = c;
+    NodeDev L = {}, R = {};
+    L.Tg = lg[k].Lg;
+    L.Th = lg[k].Lh;
+    R.Tg = nd.Tg - lg[k].Lg;
+    R.Th = nd.Th - lg[k].Lh;
+    L.state = R.state = GBM_NODE_ABSENT;  // set by the children's evaluation
+    nodes[c] = L;                        // start / count: part_scan_kernel
+    nodes[c + 1] = R;
+    const int in = lg[k].buf, out = in < 0 ? 0 : 1 - in;
+    const int built = nd.build_left ? c : c + 1;
+    for (int i = 0; i < 2; ++i) {
+        LgNode z = {};
+        z.depth = lg[k].depth + 1;
+        z.hslot = (c + i == built) ? s + 1 : lg[k].hslot;  // the sibling takes over the parent's slot
+        z.buf = out;
+        lg[c + i] = z;
+    }
+    step->k = k;
+    step->c = c;
+    step->in_buf = in;
+    step->out_buf = out;
+    const long long tiles = nd.count > 0 ? (nd.count + PT - 1) / PT : 0;
+    const long long runs = (tiles + run_tiles - 1) / run_tiles;
+    tile_base[0] = 0;
+    tile_base[1] = (int)tiles;
+    run_base[0] = 0;
+    run_base[1] = (int)runs;
+    n_items[0] = (int)runs * n_groups;
+    n_items[1] = 0;
+}
+
+// every row's leaf: walk the linked tree from the root in row order (coalesced row_leaf)
+__global__ void __launch_bounds__(WALK_THREADS) lg_walk_kernel(QM qm, TreeDev t, long long n,
+                                                               int32_t *__restrict__ row_leaf) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (__ldg(t.kind + k) == GBM_NODE_SPLIT) {
+            const int sym = (int)split_symbol(qm, r, __ldg(t.feature + k));
+            const bool left = sym == qm.B ? __ldg(t.default_left + k) != 0 : sym <= __ldg(t.bin + k);
+            const int c = __ldg(t.left_child + k);
+            k = left ? c : c + 1;
+        }
+        row_leaf[r] = k;
     }
 }
 
@@ -2129,6 +2314,7 @@ static TreeDev tree_dev(const gbm_tree *t) {
     d.default_left = t->default_left;
     d.gain = t->gain;
     d.weight = t->weight;
+    d.left_child = t->left_child;
     d.sum_qg = reinterpret_cast<long long *>(t->sum_qg);
     d.sum_qh = reinterpret_cast<long long *>(t->sum_qh);
     return d;
@@ -2154,6 +2340,224 @@ static EvalArgs eval_args_base(const gbm_qmatrix *q, const int32_t *scale_d, con
     a.scale = scale_d;
     a.p = EvalParams{prm->eta, prm->lambda, prm->gamma, prm->min_child_weight, prm->max_depth};
     return a;
+}
+
+// Upload the feature-group table when it changed (keeps tree builds free of pageable copies so
+// a whole round can be captured in a CUDA graph).
+static int upload_groups(gbm_ctx *ctx, const HistPlan &hp, Group *groups, ColGroup *cgroups, const Arena &A,
+                         cudaStream_t s) {
+    const int G = hp.col ? (int)hp.cgroups.size() : (int)hp.groups.size();
+    std::vector<int> key;
+    key.push_back(hp.col ? 1 : 0);
+    key.push_back((int)(reinterpret_cast<uintptr_t>(hp.col ? (void *)cgroups : (void *)groups) & 0x7fffffff));
+    key.push_back((int)A.generation);
+    if (hp.col)
+        for (auto &g : hp.cgroups) { key.push_back(g.f_lo); key.push_back(g.f_hi); }
+    else
+        for (auto &g : hp.groups) { key.push_back(g.u_lo); key.push_back(g.u_hi); key.push_back(g.bin_lo); key.push_back(g.bin_hi); }
+    if (key != ctx->tree_groups_key) {
+        if (hp.col) GBM_CUDA(cudaMemcpyAsync(cgroups, hp.cgroups.data(), G * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
+        else GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
+        ctx->tree_groups_key = key;
+    }
+    return GBM_OK;
+}
+
+// Loss-guided growth (R25-R27): InitRoot as depth-wise, then max_leaves - 1 device-driven
+// expansion steps, each = select (pop) -> fused repartition + smaller-child histogram of the one
+// parent -> scan -> scatter -> allreduce -> sibling by subtraction + EvaluateSplit of both
+// children.  Open nodes keep their histograms in a pool of max_leaves slots (the sibling
+// overwrites its parent's slot, the built child takes slot s+1); a node's rows stay in the
+// ridx buffer its parent's step wrote (segments of open nodes are disjoint, so two buffers do).
+static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, const int32_t *qpair_d,
+                                const int32_t *scale_d, const gbm_params *prm, const gbm_tree *tree,
+                                int32_t *row_leaf_d, cudaStream_t s) {
+    const long long n = q->n_rows;
+    const int F = q->n_features, D = prm->max_depth, L = prm->max_leaves;
+    const long long TB = q->cut_ptr_h[F];
+    const long long cap = 2ll * L - 1;
+    HistPlan hp;
+    GBM_TRY(plan_hist(ctx, q, qm, prm->grad_bits > 15, std::max<long long>(n, 1), hp, prm->grad_bits, false, false));
+    const int G = (int)hp.groups.size();
+    const size_t esz = hp.carry ? 8 : 4;
+    const long long max_tiles = (n + PT - 1) / PT + 2;
+    const size_t hist_unit = (size_t)std::max<long long>(TB, 1) * 2;
+    const bool grow = D > 0 && L > 1;
+    size_t need = 0;
+    need += 2 * (size_t)std::max<long long>(n, 1) * esz + 512;    // ridx buffers
+    need += (size_t)max_tiles * (PT / 32) * 4 + 256;              // flags
+    need += 2 * (size_t)max_tiles * 4 + 512;                      // tile_left / tile_off
+    need += 3 * 64 + 3 * 256;                                     // tile_base, run_base, n_items
+    need += (size_t)(cap + 2) * (sizeof(NodeDev) + sizeof(LgNode)) + 512;
+    need += sizeof(StepDev) + 256;
+    need += (size_t)G * sizeof(Group) + 256;
+    need += (2 * hist_unit + 2) * 8 + 512;                        // root (+ totals), build
+    need += (grow ? (size_t)L : 1) * hist_unit * 8 + 256;         // pool
+    need += 2 * (size_t)F * sizeof(FeatBest) + 256;
+    Arena &A = ctx->tree_arena;
+    GBM_TRY(A.reserve(need));
+    char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
+    uint32_t *flags = A.take<uint32_t>((size_t)max_tiles * (PT / 32));
+    int *tile_left = A.take<int>(max_tiles);
+    int *tile_off = A.take<int>(max_tiles);
+    int *tile_base = A.take<int>(4);
+    int *run_base = A.take<int>(4);
+    int *n_items = A.take<int>(2);
+    NodeDev *nodes = A.take<NodeDev>(cap + 2);
+    LgNode *lg = A.take<LgNode>(cap + 2);
+    StepDev *step = A.take<StepDev>(1);
+    Group *groups = A.take<Group>(G);
+    long long *hist_root = A.take<long long>(hist_unit + 2);
+    long long *hist_build = A.take<long long>(hist_unit);
+    long long *hist_pool = A.take<long long>((grow ? (size_t)L : 1) * hist_unit);
+    FeatBest *fb = A.take<FeatBest>(2 * (size_t)F);
+    GBM_TRY(upload_groups(ctx, hp, groups, nullptr, A, s));
+    const TreeDev t = tree_dev(tree);
+    const double row_bytes = (double)F * q->bits / 8.0;
+    {
+        ProfScope ps(ctx, PC_INIT, s);
+        const int g = (int)std::min<long long>((cap + 255) / 256, 1024);
+        init_tree_kernel<<<g, 256, 0, s>>>(t, cap, nodes, n);
+        lg_init_kernel<<<g, 256, 0, s>>>(lg, cap);
+    }
+    // ---- InitRoot
+    GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
+    if (n > 0 && TB > 0) {
+        RangeArgs ra = {};
+        ra.qm = qm;
+        ra.qpair = reinterpret_cast<const int2 *>(qpair_d);
+        ra.n_sel = n;
+        ra.chunk = hp.chunk;
+        ra.n_groups = G;
+        ra.groups = groups;
+        ra.cut_ptr = q->cut_ptr_d;
+        ra.hist = reinterpret_cast<unsigned long long *>(hist_root);
+        ra.totals = reinterpret_cast<unsigned long long *>(hist_root + hist_unit);
+        ra.hstride = hp.hstride;
+        int slot = -1;
+        ra.rows_ctr = prof_rows_slot(ctx, &slot);
+        ProfScope ps(ctx, PC_HIST_ROOT, s, 0.0, slot, row_bytes + 8.0);
+        GBM_TRY(GBM_DISPATCH(hp, launch_range, ctx, hp, ra, s));
+    } else if (n > 0) {
+        return fail(GBM_E_ARG, "gbm_build_tree: no feature has a cut (all values missing)");
+    }
+    {
+        ProfScope ps(ctx, PC_ALLREDUCE, s, (double)(hist_unit + 2) * 8);
+        GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
+    }
+    EvalArgs ea = eval_args_base(q, scale_d, prm);
+    ea.nodes = nodes;
+    ea.hist_root = hist_root;
+    ea.hist_build = hist_build;
+    ea.fb = fb;
+    ea.lg = lg;
+    ea.step = step;
+    ea.hist_pool = hist_pool;
+    ea.level = 0;
+    ea.first = 0;
+    ea.n_nodes = 1;
+    ea.hist_store = grow ? hist_pool : nullptr;  // the root's histogram -> pool slot 0
+    if (D > 0) {
+        ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
+        eval_feat_kernel<<<(F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
+    }
+    {
+        ProfScope ps(ctx, PC_EVAL_FINAL, s);
+        eval_final_kernel<<<1, E_THREADS, 0, s>>>(ea, t);
+        GBM_CUDA(cudaGetLastError());
+    }
+    if (!grow) {  // a single leaf
+        GBM_CUDA(cudaMemsetAsync(row_leaf_d, 0, sizeof(int32_t) * (size_t)std::max<long long>(n, 0), s));
+        return GBM_OK;
+    }
+    const long long tiles_all = (n + PT - 1) / PT;
+    const long long target = 4ll * hp.blocks_fused;
+    const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
+        1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
+    FusedArgs fa = {};
+    fa.qm = qm;
+    fa.nodes = nodes;
+    fa.first = 0;
+    fa.n_par = 1;
+    fa.tile_base = tile_base;
+    fa.run_base = run_base;
+    fa.n_groups = G;
+    fa.run_tiles = run_tiles;
+    fa.n_items = n_items;
+    fa.ridx_in = nullptr;
+    fa.step = step;
+    fa.bufs[0] = ridx[0];
+    fa.bufs[1] = ridx[1];
+    fa.flags = flags;
+    fa.tile_left = tile_left;
+    fa.row_leaf = row_leaf_d;
+    fa.qpair = reinterpret_cast<const int2 *>(qpair_d);
+    fa.groups = groups;
+    fa.cut_ptr = q->cut_ptr_d;
+    fa.hist = reinterpret_cast<unsigned long long *>(hist_build);
+    fa.TB = std::max<long long>(TB, 1);
+    fa.hstride = hp.hstride;
+    fa.bits_parent_row = q->bits + 32;  // split symbol + entry (identity at the root: upper bound)
+    fa.bits_built_row = F * q->bits + 64;
+    const int pgrid = ctx->sm_count * 8;
+    ea.level = 1;  // child mode of node_source
+    ea.n_nodes = 2;
+    ea.hist_store = nullptr;
+    for (int st = 0; st < L - 1; ++st) {
+        {
+            ProfScope ps(ctx, PC_PLAN, s);
+            lg_select_kernel<<<1, 1024, 0, s>>>(nodes, lg, t, q->cut_ptr_d, q->cut_values_d, st, G, run_tiles, step,
+                                                tile_base, run_base, n_items);
+            GBM_CUDA(cudaGetLastError());
+        }
+        GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
+        GBM_CUDA(cudaMemsetAsync(hist_build, 0, hist_unit * 8, s));
+        {
+            int slot;
+            fa.rows_ctr = prof_rows_slot(ctx, &slot);
+            ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
+            GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));
+        }
+        {
+            ProfScope ps(ctx, PC_PART_SCAN, s);
+            part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, tile_base, tile_left, tile_off, step);
+        }
+        {
+            int slot;
+            unsigned long long *rc = prof_rows_slot(ctx, &slot);
+            ProfScope ps(ctx, PC_PART_SCATTER, s, 0.0, slot, 8.0);
+            if (hp.carry)
+                part_scatter_kernel<true><<<pgrid, P_THREADS, 0, s>>>(
+                    nodes, 0, 1, tile_base, flags, tile_off, nullptr, nullptr, reinterpret_cast<const int2 *>(qpair_d),
+                    rc, step, ridx[0], ridx[1]);
+            else
+                part_scatter_kernel<false><<<pgrid, P_THREADS, 0, s>>>(
+                    nodes, 0, 1, tile_base, flags, tile_off, nullptr, nullptr, nullptr, rc, step, ridx[0], ridx[1]);
+            GBM_CUDA(cudaGetLastError());
+        }
+        {
+            ProfScope ps(ctx, PC_ALLREDUCE, s, (double)hist_unit * 8);
+            GBM_TRY(allreduce_i64(ctx, hist_build, hist_unit, s));
+        }
+        ea.first = 2 * st + 1;
+        {
+            ProfScope ps(ctx, PC_EVAL, s, (double)hist_unit * 8 * 4.0);
+            eval_feat_kernel<<<(2 * F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
+        }
+        {
+            ProfScope ps(ctx, PC_EVAL_FINAL, s);
+            eval_final_kernel<<<2, E_THREADS, 0, s>>>(ea, t);
+            GBM_CUDA(cudaGetLastError());
+        }
+    }
+    if (n > 0) {
+        ProfScope ps(ctx, PC_PART_FINAL, s, (double)n * 4.0);
+        const int grid = (int)std::max<long long>(1, std::min<long long>((n + WALK_THREADS - 1) / WALK_THREADS,
+                                                                        (long long)ctx->sm_count * 8));
+        lg_walk_kernel<<<grid, WALK_THREADS, 0, s>>>(qm, t, n, row_leaf_d);
+        GBM_CUDA(cudaGetLastError());
+    }
+    return GBM_OK;
 }
 
 }  // namespace gbm
@@ -2318,7 +2722,7 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     GBM_CUDA(cudaMemsetAsync(zq, 0, sizeof(int2) * (size_t)q->n_rows, s));
     fa.qpair = zq;
     GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, false));
-    part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, tile_base, tile_left, tile_off);
+    part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, tile_base, tile_left, tile_off, nullptr);
     part_scatter_kernel<false><<<std::max(1, std::min(tiles, ctx->sm_count * 8)), P_THREADS, 0, s>>>(
         nodes, 0, 1, tile_base, flags, tile_off, rows_d, out_d, nullptr, nullptr);
     GBM_CUDA(cudaGetLastError());
@@ -2336,7 +2740,16 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     GBM_REQUIRE(tree->kind && tree->feature && tree->bin && tree->threshold && tree->default_left && tree->gain &&
                     tree->weight && tree->sum_qg && tree->sum_qh,
                 GBM_E_ARG, "gbm_build_tree: null tree array");
-    GBM_REQUIRE(prm->max_depth >= 0 && prm->max_depth <= 16, GBM_E_ARG, "gbm_build_tree: max_depth in 0..16");
+    GBM_REQUIRE(prm->grow_policy == GBM_GROW_DEPTHWISE || prm->grow_policy == GBM_GROW_LOSSGUIDE, GBM_E_ARG,
+                "gbm_build_tree: grow_policy must be GBM_GROW_DEPTHWISE or GBM_GROW_LOSSGUIDE");
+    if (prm->grow_policy == GBM_GROW_LOSSGUIDE) {
+        GBM_REQUIRE(prm->max_leaves >= 1 && prm->max_leaves <= 65536, GBM_E_ARG,
+                    "gbm_build_tree: lossguide max_leaves in 1..65536");
+        GBM_REQUIRE(prm->max_depth >= 0, GBM_E_ARG, "gbm_build_tree: max_depth >= 0");
+        GBM_REQUIRE(tree->left_child, GBM_E_ARG, "gbm_build_tree: lossguide trees need left_child");
+    } else {
+        GBM_REQUIRE(prm->max_depth >= 0 && prm->max_depth <= 16, GBM_E_ARG, "gbm_build_tree: max_depth in 0..16");
+    }
     GBM_REQUIRE(prm->grad_bits >= 1 && prm->grad_bits <= 30, GBM_E_ARG, "gbm_build_tree: grad_bits in 1..30");
     GBM_REQUIRE(prm->lambda >= 0 && prm->gamma >= 0 && prm->min_child_weight >= 0, GBM_E_ARG,
                 "gbm_build_tree: lambda, gamma, min_child_weight must be >= 0");
@@ -2344,6 +2757,8 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     GBM_REQUIRE(n > 0 || (ctx->comm && ctx->nranks > 1), GBM_E_EMPTY, "gbm_build_tree: zero rows (S:321)");
     cudaStream_t s = (cudaStream_t)stream;
     const QM qm = make_qm(q);
+    if (prm->grow_policy == GBM_GROW_LOSSGUIDE)
+        return build_tree_lossguide(ctx, q, qm, qpair_d, scale_d, prm, tree, row_leaf_d, s);
     const int F = q->n_features, D = prm->max_depth;
     const long long TB = q->cut_ptr_h[F];
     const long long cap = (1ll << (D + 1)) - 1;
@@ -2387,23 +2802,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
     unsigned *done = A.take<unsigned>(1);
 
-    // the group table is uploaded only when it changes (keeps gbm_build_tree free of pageable
-    // copies, so a whole round can be captured in a CUDA graph)
-    {
-        std::vector<int> key;
-        key.push_back(hp.col ? 1 : 0);
-        key.push_back((int)(reinterpret_cast<uintptr_t>(groups) & 0x7fffffff));
-        key.push_back((int)A.generation);
-        if (hp.col)
-            for (auto &g : hp.cgroups) { key.push_back(g.f_lo); key.push_back(g.f_hi); }
-        else
-            for (auto &g : hp.groups) { key.push_back(g.u_lo); key.push_back(g.u_hi); key.push_back(g.bin_lo); key.push_back(g.bin_hi); }
-        if (key != ctx->tree_groups_key) {
-            if (hp.col) GBM_CUDA(cudaMemcpyAsync(cgroups, hp.cgroups.data(), G * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
-            else GBM_CUDA(cudaMemcpyAsync(groups, hp.groups.data(), G * sizeof(Group), cudaMemcpyHostToDevice, s));
-            ctx->tree_groups_key = key;
-        }
-    }
+    GBM_TRY(upload_groups(ctx, hp, groups, cgroups, A, s));
     const TreeDev t = tree_dev(tree);
     const double row_bytes = (double)F * q->bits / 8.0;  // algorithmic bytes of one packed row
     {
@@ -2586,7 +2985,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         }
         {
             ProfScope ps(ctx, PC_PART_SCAN, s);
-            part_scan_kernel<<<n_par, 1024, 0, s>>>(nodes, first, tile_base, tile_left, tile_off);
+            part_scan_kernel<<<n_par, 1024, 0, s>>>(nodes, first, tile_base, tile_left, tile_off, nullptr);
         }
         {
             int slot;

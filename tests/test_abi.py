@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(G.EXPORTS), set(names) ^ set(G.EXPORTS)
-    assert lib.gbm_abi_version() == 1
+    assert lib.gbm_abi_version() == 2
 
 
 @pytest.mark.parametrize("mx", [0, 1, 2, 3, 15, 16, 255, 256, 4095, 65535])
@@ -65,3 +65,20 @@ def test_no_cpu_fallback():
     h = ctypes.c_void_p()
     assert G.lib().gbm_ctx_create(0, ctypes.byref(h)) == -10
     assert b"no CUDA device" in G.lib().gbm_last_error()
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of gbm_params / gbm_qmatrix / gbm_tree have the header's offsets."""
+    import subprocess
+    c = tmp_path / "layout.c"
+    c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "gbm.h"\n'
+                 'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(gbm_params),'
+                 ' offsetof(gbm_params, grow_policy), offsetof(gbm_params, eta),'
+                 ' offsetof(gbm_params, max_leaves), sizeof(gbm_qmatrix), sizeof(gbm_tree),'
+                 ' offsetof(gbm_tree, left_child)); return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(c)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    P, Q, T = G._Params, G._QM, G._Tree
+    assert got == [ctypes.sizeof(P), P.grow_policy.offset, P.eta.offset, P.max_leaves.offset,
+                   ctypes.sizeof(Q), ctypes.sizeof(T), T.left_child.offset]

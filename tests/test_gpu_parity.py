@@ -293,6 +293,56 @@ def test_max_depth_zero_and_one(ctx, G):
         np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
 
 
+# ------------------------------------------------------------------ loss-guided growth
+LG_CASES = [
+    # cfg, rows, missing, align, P, rounds, max_depth, max_leaves
+    ("tiny", 2000, 0.05, 32, 15, 3, 8, 12),
+    ("tiny", 2000, 0.0, 0, 30, 2, 3, 64),       # budget not binding
+    ("tiny", 2000, 0.0, 32, 15, 2, 6, 1),       # a single leaf
+    ("tiny", 2000, 0.0, 32, 15, 2, 0, 8),       # max_depth 0
+    ("higgs", 100_000, 0.0, 32, 15, 3, 12, 31),
+    ("higgs", 50_000, 0.02, 128, 16, 2, 10, 63),  # wide fixed point
+    ("yearmsd", 30_000, 0.0, 32, 15, 2, 8, 20),
+    ("airline", 60_000, 0.03, 0, 12, 2, 16, 40),
+    ("bosch", 12_000, 0.0, 32, 15, 2, 8, 16),   # 9-bit symbols, ~81% missing
+]
+
+
+@pytest.mark.parametrize("colsym,carry", [(True, 0), (False, 1)])
+@pytest.mark.parametrize("cfg,n,missing,align,P,rounds,D,L", LG_CASES)
+def test_lossguide_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, D, L, colsym, carry):
+    ctx.set_option(ctx.CARRY_GRADIENTS, carry)
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    kw = dict(eta=0.3, reg_lambda=1.0, gamma=0.0)
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=D, grad_bits=P,
+                   row_align_bits=align, mcw=1.0, grow_policy="lossguide", max_leaves=L, **kw)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=D,
+                   grad_bits=P, row_align_bits=align, base_margin=ob.base_margin,
+                   min_child_weight=1.0, colsym=colsym, grow_policy="lossguide", max_leaves=L, **kw)
+    for r in range(rounds):
+        ot = ob.round()
+        gt = gb.round().to_numpy()
+        _compare_tree(gt, ot)
+        np.testing.assert_array_equal(gt["left_child"], ot["left_child"])
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    Xt, _ = W.generate(cfg, n, n + 3000, n_rows=max(n + 3000, c.n_rows))
+    np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
+    np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy(), ob.predict(Xt))
+    ctx.set_option(ctx.CARRY_GRADIENTS, 0)
+
+
+def test_depthwise_trees_carry_links(ctx, G):
+    """Depth-wise trees fill left_child (2k+1) too, so the linked predictor walks them."""
+    X, y = W.generate("tiny")
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=16, objective="reg:squarederror", max_depth=4)
+    t = gb.round().to_numpy()
+    k = np.nonzero(t["kind"] == 1)[0]
+    np.testing.assert_array_equal(t["left_child"][k], 2 * k + 1)
+    assert np.all(t["left_child"][t["kind"] != 1] == -1)
+
+
 # ------------------------------------------------------------------ full-size properties
 @pytest.mark.parametrize("cfg", ["higgs"])
 def test_full_size_round_properties(ctx, G, cfg):
