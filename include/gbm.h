@@ -99,8 +99,12 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  * GBM_OPT_RUN_TILES: 2048-row tiles per work item of the fused level kernel (0 = auto).
  * GBM_OPT_GROUP_UNITS: at most this many packed units (S features each) per shared-memory
  *   feature group of the compact layout (0 = auto = 32; 1..32).  Smaller groups mean less
- *   shared memory per block (more resident blocks) but more passes over the row list. */
-enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4 };
+ *   shared memory per block (more resident blocks) but more passes over the row list.
+ * GBM_OPT_EVAL_WARP: EvaluateSplit with one warp per (node, feature), 8 bins per lane (1), or
+ *   one block per (node, feature), one bin per thread (2); 0 (default) = warps when there are
+ *   at least 16 per SM, else blocks. */
+enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
+       GBM_OPT_EVAL_WARP = 5 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

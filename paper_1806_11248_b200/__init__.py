@@ -298,6 +298,7 @@ class Context:
     CARRY_GRADIENTS = 2
     RUN_TILES = 3
     GROUP_UNITS = 4
+    EVAL_WARP = 5
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

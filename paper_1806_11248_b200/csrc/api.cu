@@ -262,6 +262,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->group_units = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_EVAL_WARP) {
+        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_EVAL_WARP: 0 auto, 1 warp, 2 block");
+        ctx->eval_warp = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_CARRY_GRADIENTS) {
         ctx->carry_gradients = value != 0;
         return GBM_OK;

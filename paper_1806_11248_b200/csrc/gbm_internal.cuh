@@ -109,6 +109,7 @@ struct gbm_ctx {
     int carry_gradients = 0;       // GBM_OPT_CARRY_GRADIENTS
     int run_tiles = 0;             // GBM_OPT_RUN_TILES (0 = auto)
     int group_units = 0;           // GBM_OPT_GROUP_UNITS (0 = auto = 32)
+    int eval_warp = 0;             // GBM_OPT_EVAL_WARP (0 auto, 1 warp per feature, 2 block)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
 };
 

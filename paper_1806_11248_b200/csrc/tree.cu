@@ -57,6 +57,8 @@ struct StepDev {       // the expansion of the current step, written by lg_selec
     int k;             // parent (-1: nothing left to expand -- every later launch is a no-op)
     int c;             // its left child (2j+1); right = c + 1
     int in_buf, out_buf;
+    int run_tiles;     // tiles per work item of the fused kernel, sized to the parent
+    int pad;
 };
 
 struct RangeItem {  // rows [start, start+len) of a row source, one feature group
@@ -495,9 +497,10 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
     __shared__ int s_off[2049];
     __shared__ E s_rows[H_THREADS / 32][WROWS];
     const E *rin = static_cast<const E *>(a.ridx_in);
-    int first = a.first;
+    int first = a.first, run_tiles = a.run_tiles;
     if (a.step) {  // loss-guided step (n_par = 1): no items at all when nothing is expanded
         first = a.step->k;
+        run_tiles = a.step->run_tiles;
         rin = a.step->in_buf < 0 ? nullptr : static_cast<const E *>(a.bufs[a.step->in_buf]);
     }
     const QM &qm = a.qm;
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
         const int k = first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const int t0 = tb + (run - a.run_base[j]) * run_tiles, t1 = min(a.tile_base[j + 1], t0 + run_tiles);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             if (g != 0) continue;
@@ -1624,10 +1627,123 @@ __device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long
     return best;
 }
 
+// Block-per-feature variant: thread t owns bin c+t of each E_THREADS-bin chunk, so one thread
+// evaluates one candidate (two with missing mass) -- the latency of a feature is one candidate
+// plus a block scan, where the warp variant runs KB candidates back to back per lane.
+constexpr int EWPB = E_THREADS / 32;
+// block-wide inclusive scan of an int64 pair; also returns the block totals
+__device__ __forceinline__ void block_scan2(long long &g, long long &h, long long &tot_g, long long &tot_h) {
+    __shared__ long long s_sg[EWPB], s_sh[EWPB];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long yg = __shfl_up_sync(0xffffffffu, g, o), yh = __shfl_up_sync(0xffffffffu, h, o);
+        if (lane >= o) {
+            g += yg;
+            h += yh;
+        }
+    }
+    if (lane == 31) {
+        s_sg[w] = g;
+        s_sh[w] = h;
+    }
+    __syncthreads();
+    long long pg = 0, ph = 0, tg = 0, th = 0;
+#pragma unroll
+    for (int i = 0; i < EWPB; ++i) {
+        if (i < w) {
+            pg += s_sg[i];
+            ph += s_sh[i];
+        }
+        tg += s_sg[i];
+        th += s_sh[i];
+    }
+    g += pg;
+    h += ph;
+    tot_g = tg;
+    tot_h = th;
+    __syncthreads();
+}
+
+// canonical argmax over the block; the result is valid in thread 0
+__device__ __forceinline__ FeatBest block_best(FeatBest b) {
+    __shared__ double s_g[EWPB];
+    __shared__ long long s_i[EWPB], s_lg[EWPB], s_lh[EWPB];
+    for (int o = 16; o > 0; o >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, b.gain, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, b.idx, o);
+        const long long olg = __shfl_xor_sync(0xffffffffu, b.Lg, o), olh = __shfl_xor_sync(0xffffffffu, b.Lh, o);
+        if (better(og, oi, b.gain, b.idx)) {
+            b.gain = og; b.idx = oi; b.Lg = olg; b.Lh = olh;
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_g[w] = b.gain; s_i[w] = b.idx; s_lg[w] = b.Lg; s_lh[w] = b.Lh;
+    }
+    __syncthreads();
+    FeatBest r;
+    r.gain = s_g[0]; r.idx = s_i[0]; r.Lg = s_lg[0]; r.Lh = s_lh[0];
+    for (int i = 1; i < EWPB; ++i)
+        if (better(s_g[i], s_i[i], r.gain, r.idx)) {
+            r.gain = s_g[i]; r.idx = s_i[i]; r.Lg = s_lg[i]; r.Lh = s_lh[i];
+        }
+    __syncthreads();
+    return r;
+}
+
+// Best candidate of feature f of one node, computed by the whole block (valid in thread 0).
+__device__ FeatBest eval_feature_blk(const NodeHist &src, int b0, int nbf, long long Tg, long long Th, int sg, int sh,
+                                     double e, const EvalParams &p) {
+    long long Mg = 0, Mh = 0;
+    if (nbf > E_THREADS) {  // wide features: totals first
+        long long g2 = 0, h2 = 0, tg, th;
+        for (int b = threadIdx.x; b < nbf; b += E_THREADS) {
+            long long g, h;
+            src.get(b0 + b, g, h);
+            g2 += g;
+            h2 += h;
+        }
+        block_scan2(g2, h2, tg, th);
+        Mg = Tg - tg;
+        Mh = Th - th;
+    }
+    FeatBest best;
+    best.gain = 0.0;
+    best.idx = LLONG_MAX;
+    best.Lg = best.Lh = 0;
+    long long cg = 0, ch = 0;  // prefix of earlier chunks
+    for (int c = 0; c < nbf; c += E_THREADS) {
+        const int b = c + (int)threadIdx.x;
+        long long vg = 0, vh = 0;
+        if (b < nbf) {
+            src.get(b0 + b, vg, vh);
+            if (src.store) {
+                src.store[2 * (b0 + b)] = vg;
+                src.store[2 * (b0 + b) + 1] = vh;
+            }
+        }
+        long long tg, th;
+        block_scan2(vg, vh, tg, th);
+        if (nbf <= E_THREADS) {  // single chunk: the feature sum is the scan's total
+            Mg = Tg - tg;
+            Mh = Th - th;
+        }
+        if (b < nbf) eval_candidate(cg + vg, ch + vh, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), best);
+        cg += tg;
+        ch += th;
+    }
+    return block_best(best);
+}
+
 struct EvalArgs {
     int level, first, F, n_nodes;
     // tree mode: the last eval_final block plans the next level's partition (plan_block)
-    unsigned *done;                 // block counter (reset by the last block), null = no plan
+    unsigned *done;                 // tree mode: completed-node counter (reset by the last block)
+    unsigned *node_done;            // tree mode: [n_nodes] finished warps per node (reset by finishers)
+    int plan_mode;                  // tree mode, last block: 0 nothing, 1 plan the next level,
+                                    // 2 loss-guided pop of step sel_step (R25)
+    int sel_step;
+    int *tile_left;                 // loss-guided: zeroed for the popped node's tiles
     int plan_groups, plan_run;
     int *tile_base, *run_base, *n_items;
     long long TB;
@@ -1644,7 +1760,7 @@ struct EvalArgs {
     const long long *totals_direct; // direct mode: [n_nodes][2]
     FeatBest *fb;                   // [n_nodes][F]
     LgNode *lg;                     // loss-guided mode (null = depth-wise)
-    const StepDev *step;            // loss-guided: the current expansion
+    StepDev *step;                  // loss-guided: the current expansion
     long long *hist_pool;           // loss-guided: [max_leaves][TB][2] by LgNode::hslot
 };
 
@@ -1699,10 +1815,8 @@ __device__ __forceinline__ bool node_source(const EvalArgs &a, int j, NodeHist &
     return true;
 }
 
-// one warp per (node, feature)
-__global__ void __launch_bounds__(E_THREADS) eval_feat_kernel(EvalArgs a) {
-    const long long gw = ((long long)blockIdx.x * E_THREADS + threadIdx.x) >> 5;
-    if (gw >= (long long)a.n_nodes * a.F) return;
+// one warp per (node, feature): the feature's best candidate into fb[gw]
+__device__ __forceinline__ void eval_warp(const EvalArgs &a, long long gw) {
     const int j = (int)(gw / a.F), f = (int)(gw - (long long)j * a.F);
     NodeHist src;
     long long Tg, Th;
@@ -1715,6 +1829,28 @@ __global__ void __launch_bounds__(E_THREADS) eval_feat_kernel(EvalArgs a) {
     const FeatBest b = eval_feature(src, b0, nbf, Tg, Th, sg, sh, e, a.p);
     if ((threadIdx.x & 31) == 0) a.fb[gw] = b;
 }
+
+// one block per (node, feature) = blk: the feature's best candidate into fb[blk]
+__device__ __forceinline__ void eval_block(const EvalArgs &a, long long blk) {
+    const int j = (int)(blk / a.F), f = (int)(blk - (long long)j * a.F);
+    NodeHist src;
+    long long Tg, Th;
+    if (!node_source(a, j, src, Tg, Th)) return;                    // block-uniform
+    if (a.lg && a.lg[a.first + j].depth >= a.p.max_depth) return;  // a leaf: not evaluated
+    const int sg = a.scale[0], sh = a.scale[1];
+    const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
+    const double e = ddiv(dmul(G, G), dadd(H, a.p.lambda));
+    const int b0 = __ldg(a.cut_ptr + f), nbf = __ldg(a.cut_ptr + f + 1) - b0;
+    const FeatBest b = eval_feature_blk(src, b0, nbf, Tg, Th, sg, sh, e, a.p);
+    if (threadIdx.x == 0) a.fb[blk] = b;
+}
+
+__global__ void __launch_bounds__(E_THREADS) eval_feat_kernel(EvalArgs a) {
+    const long long gw = ((long long)blockIdx.x * E_THREADS + threadIdx.x) >> 5;
+    if (gw < (long long)a.n_nodes * a.F) eval_warp(a, gw);
+}
+
+__global__ void __launch_bounds__(E_THREADS) eval_feat_blk_kernel(EvalArgs a) { eval_block(a, blockIdx.x); }
 
 __device__ __forceinline__ double leaf_weight(long long Tg, long long Th, int sg, int sh, double lambda, double eta) {
     const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
@@ -1760,7 +1896,12 @@ __device__ FeatBest reduce_node(const EvalArgs &a, int j) {
     double bg = 0.0;
     long long bi = LLONG_MAX, blg = 0, blh = 0;
     for (int f = threadIdx.x; f < a.F; f += E_THREADS) {
-        const FeatBest c = a.fb[(long long)j * a.F + f];
+        const FeatBest *cp = a.fb + (long long)j * a.F + f;
+        FeatBest c;
+        c.gain = __ldcg(&cp->gain);
+        c.idx = __ldcg(&cp->idx);
+        c.Lg = __ldcg(&cp->Lg);
+        c.Lh = __ldcg(&cp->Lh);
         if (better(c.gain, c.idx, bg, bi)) {
             bg = c.gain; bi = c.idx; blg = c.Lg; blh = c.Lh;
         }
@@ -1787,28 +1928,85 @@ __device__ FeatBest reduce_node(const EvalArgs &a, int j) {
     return r;
 }
 
-__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t);
+__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j);
+__device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s);
 
-// tree mode: one block per node of the level; the last block to finish plans the next level
-__global__ void __launch_bounds__(E_THREADS) eval_final_kernel(EvalArgs a, TreeDev t) {
-    eval_final_body(a, t);
-    if (!a.done) return;
-    __shared__ bool last;
-    __syncthreads();
+// Tree mode, one launch per level / loss-guided step: warp per (node, feature) evaluation; the
+// block that completes a node's last feature reduces that node (eval_final_body); the block that
+// completes the last node plans the next level (plan_mode 1) or pops the next loss-guided
+// expansion (plan_mode 2).  Threadfence + counter pattern: every fb / node write is fenced
+// before the counter it is published by, and the finisher fences before reading.
+// nodes fin[0..nfin) were completed by this block: reduce them; count them; the block that
+// completes the level plans / pops the next step
+__device__ void eval_finish(const EvalArgs &a, const TreeDev &t, const int *fin, int nfin) {
+    __shared__ bool s_last;
+    __threadfence();
+    for (int i = 0; i < nfin; ++i) {
+        const int j = fin[i];
+        eval_final_body(a, t, j);
+        __syncthreads();
+        if (threadIdx.x == 0) a.node_done[j] = 0;
+    }
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+        s_last = atomicAdd(a.done, (unsigned)nfin) + nfin == (unsigned)a.n_nodes;
     }
     __syncthreads();
-    if (!last) return;
+    if (!s_last) return;
     __threadfence();
-    // the children of this level are the next level's parents
-    plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.plan_run, a.tile_base, a.run_base, a.n_items);
+    if (a.plan_mode == 1)  // the children of this level are the next level's parents
+        plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.plan_run, a.tile_base, a.run_base, a.n_items);
+    else if (a.plan_mode == 2)
+        lg_select_block(a, t, a.sel_step);
     if (threadIdx.x == 0) *a.done = 0;
 }
 
-__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t) {
-    const int j = blockIdx.x, k = a.first + j;
+__global__ void __launch_bounds__(E_THREADS) eval_tree_kernel(EvalArgs a, TreeDev t) {
+    constexpr int WPB = E_THREADS / 32;
+    __shared__ int s_fin[WPB + 1];
+    __shared__ int s_nfin;
+    const long long total = (long long)a.n_nodes * a.F;
+    const long long gw = ((long long)blockIdx.x * E_THREADS + threadIdx.x) >> 5;
+    if (gw < total) eval_warp(a, gw);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int nf = 0;
+        const long long w1 = min(total, (long long)(blockIdx.x + 1) * WPB);
+        for (long long w = (long long)blockIdx.x * WPB; w < w1;) {
+            const int j = (int)(w / a.F);
+            const long long we = min(w1, (long long)(j + 1) * a.F);
+            const unsigned cnt = (unsigned)(we - w);
+            if (atomicAdd(a.node_done + j, cnt) + cnt == (unsigned)a.F) s_fin[nf++] = j;
+            w = we;
+        }
+        s_nfin = nf;
+    }
+    __syncthreads();
+    if (s_nfin == 0) return;
+    eval_finish(a, t, s_fin, s_nfin);
+}
+
+// block per (node, feature); the block completing a node's last feature reduces the node
+__global__ void __launch_bounds__(E_THREADS) eval_tree_blk_kernel(EvalArgs a, TreeDev t) {
+    __shared__ int s_fin[1];
+    __shared__ int s_nfin;
+    const long long blk = blockIdx.x;
+    eval_block(a, blk);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int j = (int)(blk / a.F);
+        s_fin[0] = j;
+        s_nfin = atomicAdd(a.node_done + j, 1u) + 1 == (unsigned)a.F ? 1 : 0;
+    }
+    __syncthreads();
+    if (s_nfin == 0) return;
+    eval_finish(a, t, s_fin, 1);
+}
+
+__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j) {
+    const int k = a.first + j;
     NodeHist src;
     long long Tg, Th;
     const bool exists = node_source(a, j, src, Tg, Th);
@@ -1939,17 +2137,16 @@ __global__ void lg_init_kernel(LgNode *__restrict__ lg, long long cap) {
 }
 
 // Step s: expand_queue.pop() -- the OPEN node of largest gain, ties to the smaller id (R25) --
-// made a split node with children 2s+1, 2s+2 (R27); plans the step's single-parent partition.
-// With nothing OPEN the step is void: k = -1 and zero work items, so every later launch of the
-// step returns at once (the host enqueues a fixed max_leaves - 1 steps: graph-capturable).
-__global__ void __launch_bounds__(1024) lg_select_kernel(NodeDev *__restrict__ nodes, LgNode *__restrict__ lg,
-                                                         TreeDev t, const int32_t *__restrict__ cut_ptr,
-                                                         const float *__restrict__ cut_values, int s, int n_groups,
-                                                         int run_tiles, StepDev *__restrict__ step,
-                                                         int *__restrict__ tile_base, int *__restrict__ run_base,
-                                                         int *__restrict__ n_items) {
+// made a split node with children 2s+1, 2s+2 (R27); plans the step's single-parent partition
+// and zeroes its tile counters.  With nothing OPEN the step is void: k = -1 and zero work items,
+// so every launch of the step returns at once (the host enqueues a fixed max_leaves - 1 steps:
+// graph-capturable).  Runs in the last block of the previous evaluation (any block size).
+__device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s) {
     __shared__ double s_g[32];
     __shared__ int s_k[32];
+    __shared__ long long s_tiles;
+    NodeDev *nodes = a.nodes;
+    LgNode *lg = a.lg;
     const int n_nodes = 2 * s + 1;
     double bg = 0.0;
     int bk = -1;
@@ -1960,7 +2157,7 @@ __global__ void __launch_bounds__(1024) lg_select_kernel(NodeDev *__restrict__ n
         }
     };
     for (int k = threadIdx.x; k < n_nodes; k += blockDim.x)
-        if (nodes[k].state == NODE_OPEN) take(lg[k].gain, k);
+        if (__ldcg(&nodes[k].state) == NODE_OPEN) take(__ldcg(&lg[k].gain), k);
     for (int o = 16; o > 0; o >>= 1) {
         const double og = __shfl_xor_sync(0xffffffffu, bg, o);
         const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
@@ -1972,57 +2169,67 @@ __global__ void __launch_bounds__(1024) lg_select_kernel(NodeDev *__restrict__ n
         s_k[w] = bk;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) take(s_g[i], s_k[i]);
-    const int c = 2 * s + 1;
-    if (bk < 0) {
-        step->k = -1;
-        step->c = c;
-        step->in_buf = step->out_buf = 0;
-        tile_base[0] = tile_base[1] = 0;
-        run_base[0] = run_base[1] = 0;
-        n_items[0] = n_items[1] = 0;
-        return;
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) take(s_g[i], s_k[i]);
+        const int c = 2 * s + 1;
+        StepDev *step = a.step;
+        s_tiles = 0;
+        if (bk < 0) {
+            step->k = -1;
+            step->c = c;
+            step->in_buf = step->out_buf = 0;
+            step->run_tiles = 1;
+            a.tile_base[0] = a.tile_base[1] = 0;
+            a.run_base[0] = a.run_base[1] = 0;
+            a.n_items[0] = a.n_items[1] = 0;
+        } else {
+            const int k = bk;
+            NodeDev &nd = nodes[k];
+            nd.state = GBM_NODE_SPLIT;
+            t.kind[k] = GBM_NODE_SPLIT;
+            t.feature[k] = nd.f;
+            t.bin[k] = nd.b;
+            t.threshold[k] = __ldg(a.cut_values + __ldg(a.cut_ptr + nd.f) + nd.b);
+            t.default_left[k] = (int8_t)nd.dl;
+            t.gain[k] = lg[k].gain;
+            t.left_child[k] = c;
+            NodeDev L = {}, R = {};
+            L.Tg = lg[k].Lg;
+            L.Th = lg[k].Lh;
+            R.Tg = nd.Tg - lg[k].Lg;
+            R.Th = nd.Th - lg[k].Lh;
+            L.state = R.state = GBM_NODE_ABSENT;  // set by the children's evaluation
+            nodes[c] = L;                        // start / count: part_scan_kernel
+            nodes[c + 1] = R;
+            const int in = lg[k].buf, out = in < 0 ? 0 : 1 - in;
+            const int built = nd.build_left ? c : c + 1;
+            for (int i = 0; i < 2; ++i) {
+                LgNode z = {};
+                z.depth = lg[k].depth + 1;
+                z.hslot = (c + i == built) ? s + 1 : lg[k].hslot;  // the sibling takes the parent's slot
+                z.buf = out;
+                lg[c + i] = z;
+            }
+            step->k = k;
+            step->c = c;
+            step->in_buf = in;
+            step->out_buf = out;
+            const long long tiles = nd.count > 0 ? (nd.count + PT - 1) / PT : 0;
+            // about plan_run (4 x resident blocks) items for this parent (the depth-wise rule)
+            const long long rt = max(1ll, min((long long)RUN_MAX, (tiles * a.plan_groups + a.plan_run - 1) / a.plan_run));
+            const long long runs = (tiles + rt - 1) / rt;
+            step->run_tiles = (int)rt;
+            a.tile_base[0] = 0;
+            a.tile_base[1] = (int)tiles;
+            a.run_base[0] = 0;
+            a.run_base[1] = (int)runs;
+            a.n_items[0] = (int)runs * a.plan_groups;
+            a.n_items[1] = 0;
+            s_tiles = tiles;
+        }
     }
-    const int k = bk;
-    NodeDev &nd = nodes[k];
-    nd.state = GBM_NODE_SPLIT;
-    t.kind[k] = GBM_NODE_SPLIT;
-    t.feature[k] = nd.f;
-    t.bin[k] = nd.b;
-    t.threshold[k] = __ldg(cut_values + __ldg(cut_ptr + nd.f) + nd.b);
-    t.default_left[k] = (int8_t)nd.dl;
-    t.gain[k] = lg[k].gain;
-    t.left_child[k] = c;
-    NodeDev L = {}, R = {};
-    L.Tg = lg[k].Lg;
-    L.Th = lg[k].Lh;
-    R.Tg = nd.Tg - lg[k].Lg;
-    R.Th = nd.Th - lg[k].Lh;
-    L.state = R.state = GBM_NODE_ABSENT;  // set by the children's evaluation
-    nodes[c] = L;                        // start / count: part_scan_kernel
-    nodes[c + 1] = R;
-    const int in = lg[k].buf, out = in < 0 ? 0 : 1 - in;
-    const int built = nd.build_left ? c : c + 1;
-    for (int i = 0; i < 2; ++i) {
-        LgNode z = {};
-        z.depth = lg[k].depth + 1;
-        z.hslot = (c + i == built) ? s + 1 : lg[k].hslot;  // the sibling takes over the parent's slot
-        z.buf = out;
-        lg[c + i] = z;
-    }
-    step->k = k;
-    step->c = c;
-    step->in_buf = in;
-    step->out_buf = out;
-    const long long tiles = nd.count > 0 ? (nd.count + PT - 1) / PT : 0;
-    const long long runs = (tiles + run_tiles - 1) / run_tiles;
-    tile_base[0] = 0;
-    tile_base[1] = (int)tiles;
-    run_base[0] = 0;
-    run_base[1] = (int)runs;
-    n_items[0] = (int)runs * n_groups;
-    n_items[1] = 0;
+    __syncthreads();
+    for (long long i = threadIdx.x; i < s_tiles; i += blockDim.x) a.tile_left[i] = 0;
 }
 
 // every row's leaf: walk the linked tree from the root in row order (coalesced row_leaf)
@@ -2342,6 +2549,20 @@ static EvalArgs eval_args_base(const gbm_qmatrix *q, const int32_t *scale_d, con
     return a;
 }
 
+static int launch_eval_tree(gbm_ctx *ctx, const EvalArgs &ea, const TreeDev &t, cudaStream_t s) {
+    const long long units = (long long)ea.n_nodes * ea.F;
+    // auto: a warp per (node, feature) once there are enough of them to fill the GPU
+    // (throughput: Epsilon 5.13 vs 5.32 ms/round), else a block per (node, feature) (latency:
+    // loss-guided Higgs 6.49 vs 7.29 ms/round)
+    const bool warp = ctx->eval_warp == 1 || (ctx->eval_warp == 0 && units >= 16ll * ctx->sm_count);
+    if (warp)
+        eval_tree_kernel<<<(int)((units + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(ea, t);
+    else
+        eval_tree_blk_kernel<<<(int)units, E_THREADS, 0, s>>>(ea, t);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
 // Upload the feature-group table when it changed (keeps tree builds free of pageable copies so
 // a whole round can be captured in a CUDA graph).
 static int upload_groups(gbm_ctx *ctx, const HistPlan &hp, Group *groups, ColGroup *cgroups, const Arena &A,
@@ -2394,6 +2615,7 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     need += (2 * hist_unit + 2) * 8 + 512;                        // root (+ totals), build
     need += (grow ? (size_t)L : 1) * hist_unit * 8 + 256;         // pool
     need += 2 * (size_t)F * sizeof(FeatBest) + 256;
+    need += 4 * sizeof(unsigned) + 256;                           // eval counters
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
@@ -2411,7 +2633,9 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     long long *hist_build = A.take<long long>(hist_unit);
     long long *hist_pool = A.take<long long>((grow ? (size_t)L : 1) * hist_unit);
     FeatBest *fb = A.take<FeatBest>(2 * (size_t)F);
+    unsigned *done = A.take<unsigned>(4);  // [0] nodes completed, [1..2] warps per node
     GBM_TRY(upload_groups(ctx, hp, groups, nullptr, A, s));
+    GBM_CUDA(cudaMemsetAsync(done, 0, 4 * sizeof(unsigned), s));
     const TreeDev t = tree_dev(tree);
     const double row_bytes = (double)F * q->bits / 8.0;
     {
@@ -2457,23 +2681,28 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     ea.first = 0;
     ea.n_nodes = 1;
     ea.hist_store = grow ? hist_pool : nullptr;  // the root's histogram -> pool slot 0
-    if (D > 0) {
-        ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
-        eval_feat_kernel<<<(F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
-    }
+    const long long tiles_all = (n + PT - 1) / PT;
+    const long long target = 4ll * hp.blocks_fused;
+    const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
+        1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
+    ea.done = done;
+    ea.node_done = done + 1;
+    ea.plan_groups = G;
+    ea.plan_run = (int)target;  // loss-guided: the pop sizes the work items to the parent
+    ea.tile_base = tile_base;
+    ea.run_base = run_base;
+    ea.n_items = n_items;
+    ea.tile_left = tile_left;
+    ea.plan_mode = grow ? 2 : 0;  // the root's evaluation pops the first expansion
+    ea.sel_step = 0;
     {
-        ProfScope ps(ctx, PC_EVAL_FINAL, s);
-        eval_final_kernel<<<1, E_THREADS, 0, s>>>(ea, t);
-        GBM_CUDA(cudaGetLastError());
+        ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
+        GBM_TRY(launch_eval_tree(ctx, ea, t, s));
     }
     if (!grow) {  // a single leaf
         GBM_CUDA(cudaMemsetAsync(row_leaf_d, 0, sizeof(int32_t) * (size_t)std::max<long long>(n, 0), s));
         return GBM_OK;
     }
-    const long long tiles_all = (n + PT - 1) / PT;
-    const long long target = 4ll * hp.blocks_fused;
-    const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
-        1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
     FusedArgs fa = {};
     fa.qm = qm;
     fa.nodes = nodes;
@@ -2504,13 +2733,7 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     ea.n_nodes = 2;
     ea.hist_store = nullptr;
     for (int st = 0; st < L - 1; ++st) {
-        {
-            ProfScope ps(ctx, PC_PLAN, s);
-            lg_select_kernel<<<1, 1024, 0, s>>>(nodes, lg, t, q->cut_ptr_d, q->cut_values_d, st, G, run_tiles, step,
-                                                tile_base, run_base, n_items);
-            GBM_CUDA(cudaGetLastError());
-        }
-        GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
+        // (the pop of step st ran in the last block of the previous evaluation)
         GBM_CUDA(cudaMemsetAsync(hist_build, 0, hist_unit * 8, s));
         {
             int slot;
@@ -2540,14 +2763,11 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
             GBM_TRY(allreduce_i64(ctx, hist_build, hist_unit, s));
         }
         ea.first = 2 * st + 1;
+        ea.plan_mode = st + 1 < L - 1 ? 2 : 0;
+        ea.sel_step = st + 1;
         {
             ProfScope ps(ctx, PC_EVAL, s, (double)hist_unit * 8 * 4.0);
-            eval_feat_kernel<<<(2 * F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
-        }
-        {
-            ProfScope ps(ctx, PC_EVAL_FINAL, s);
-            eval_final_kernel<<<2, E_THREADS, 0, s>>>(ea, t);
-            GBM_CUDA(cudaGetLastError());
+            GBM_TRY(launch_eval_tree(ctx, ea, t, s));
         }
     }
     if (n > 0) {
@@ -2649,7 +2869,10 @@ int gbm_evaluate_splits(gbm_ctx *ctx, const gbm_qmatrix *q, const int64_t *hist_
     a.fb = ctx->arena.take<FeatBest>((size_t)n_nodes * a.F);
     ProfScope ps(ctx, PC_EVAL, s);
     const long long warps = (long long)n_nodes * a.F;
-    eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(a);
+    if (ctx->eval_warp == 1 || (ctx->eval_warp == 0 && warps >= 16ll * ctx->sm_count))
+        eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(a);
+    else
+        eval_feat_blk_kernel<<<(int)warps, E_THREADS, 0, s>>>(a);
     eval_out_kernel<<<n_nodes, E_THREADS, 0, s>>>(a, split_d, feature_d, bin_d, default_left_d, gain_d,
                                                   reinterpret_cast<long long *>(child_d));
     GBM_CUDA(cudaGetLastError());
@@ -2784,6 +3007,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     need += (slots * hist_unit + hist_unit + 2) * 8 + 512;            // build + root
     need += 2 * slots * hist_unit * 8 + 512;                          // level hists
     need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 512;
+    need += (1 + (size_t)max_par) * sizeof(unsigned) + 256;           // eval counters
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
@@ -2800,7 +3024,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     long long *hist_build = A.take<long long>(slots * hist_unit);
     long long *hist_lvl[2] = {A.take<long long>(slots * hist_unit), A.take<long long>(slots * hist_unit)};
     FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
-    unsigned *done = A.take<unsigned>(1);
+    unsigned *done = A.take<unsigned>(1 + (size_t)max_par);  // [0] nodes completed, [1..] warps per node
 
     GBM_TRY(upload_groups(ctx, hp, groups, cgroups, A, s));
     const TreeDev t = tree_dev(tree);
@@ -2856,7 +3080,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         ProfScope ps(ctx, PC_ALLREDUCE, s, (double)(hist_unit + 2) * 8);
         GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
     }
-    GBM_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), s));
+    GBM_CUDA(cudaMemsetAsync(done, 0, (1 + (size_t)max_par) * sizeof(unsigned), s));
     EvalArgs ea = eval_args_base(q, scale_d, prm);
     ea.nodes = nodes;
     ea.hist_root = hist_root;
@@ -2876,15 +3100,12 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     ea.level = 0;
     ea.first = 0;
     ea.n_nodes = 1;
-    ea.done = (1 < D) ? done : nullptr;  // the root's eval plans level 1
-    if (D > 0) {
-        ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
-        eval_feat_kernel<<<(F + E_THREADS / 32 - 1) / (E_THREADS / 32), E_THREADS, 0, s>>>(ea);
-    }
+    ea.done = done;
+    ea.node_done = done + 1;
+    ea.plan_mode = (1 < D) ? 1 : 0;  // the root's eval plans level 1
     {
-        ProfScope ps(ctx, PC_EVAL_FINAL, s);
-        eval_final_kernel<<<1, E_THREADS, 0, s>>>(ea, t);
-        GBM_CUDA(cudaGetLastError());
+        ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
+        GBM_TRY(launch_eval_tree(ctx, ea, t, s));
     }
     if (D == 0) {  // every row sits in the root leaf
         GBM_CUDA(cudaMemsetAsync(row_leaf_d, 0, sizeof(int32_t) * (size_t)std::max<long long>(n, 0), s));
@@ -3011,15 +3232,9 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             ea.n_nodes = 1 << l;
             ea.hist_prev = l == 1 ? nullptr : hist_lvl[(l - 1) & 1];
             ea.hist_store = (l < D - 1) ? hist_lvl[l & 1] : nullptr;
-            ea.done = (l + 1 < D) ? done : nullptr;  // this level's eval plans level l + 1
-            {
-                ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
-                const long long warps = (long long)ea.n_nodes * F;
-                eval_feat_kernel<<<(int)((warps + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(ea);
-            }
-            ProfScope ps(ctx, PC_EVAL_FINAL, s);
-            eval_final_kernel<<<ea.n_nodes, E_THREADS, 0, s>>>(ea, t);
-            GBM_CUDA(cudaGetLastError());
+            ea.plan_mode = (l + 1 < D) ? 1 : 0;  // this level's eval plans level l + 1
+            ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
+            GBM_TRY(launch_eval_tree(ctx, ea, t, s));
         }
     }
     return GBM_OK;

@@ -181,8 +181,10 @@ def test_histogram_parity(ctx, G, P, cfg, align, missing, layout):
 
 
 # ------------------------------------------------------------------ a9: EvaluateSplit
+@pytest.mark.parametrize("eval_warp", [1, 2])
 @pytest.mark.parametrize("seed", range(4))
-def test_evaluate_parity(ctx, G, seed):
+def test_evaluate_parity(ctx, G, seed, eval_warp):
+    ctx.set_option(ctx.EVAL_WARP, eval_warp)
     X, y = W.generate("higgs", 0, 20_000, seed_offset=seed)
     qm, v, p, s, bits, words = _qm_from_oracle(G, X, 256, 32)
     rng = np.random.default_rng(seed)
@@ -207,6 +209,7 @@ def test_evaluate_parity(ctx, G, seed):
             assert (out["feature"][j], out["bin"][j], bool(out["default_left"][j])) == \
                 (r["feature"], r["bin"], r["default_left"])
             assert tuple(out["child"][j]) == r["L"] + r["R"]
+    ctx.set_option(ctx.EVAL_WARP, 0)
 
 
 # ------------------------------------------------------------------ a5: RepartitionInstances
@@ -281,6 +284,28 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
     np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy(), ob.predict(Xt))
     ctx.set_option(ctx.HIST_LAYOUT, 0)
     ctx.set_option(ctx.CARRY_GRADIENTS, 0)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("cfg,n,missing,grow", [("airline", 60_000, 0.03, "depthwise"),
+                                                ("bosch", 12_000, 0.0, "depthwise"),
+                                                ("tiny", 2000, 0.05, "lossguide")])
+def test_eval_variant_rounds_parity(ctx, G, cfg, n, missing, grow, mode):
+    """Both evaluation kernels (GBM_OPT_EVAL_WARP 1 = warp, 2 = block per feature) on wide
+    features and missing mass."""
+    ctx.set_option(ctx.EVAL_WARP, mode)
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    L = 20 if grow == "lossguide" else 0
+    D = 10 if grow == "lossguide" else c.max_depth
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=D,
+                   grow_policy=grow, max_leaves=L)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=D,
+                   base_margin=ob.base_margin, grow_policy=grow, max_leaves=L)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.EVAL_WARP, 0)
 
 
 def test_max_depth_zero_and_one(ctx, G):
