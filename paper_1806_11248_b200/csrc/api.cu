@@ -132,6 +132,10 @@ int gbm_ctx_create(int device, gbm_ctx **out) {
     c->smem_optin = prop.sharedMemPerBlockOptin;
     GBM_CUDA(cudaMalloc(&c->dev_err, sizeof(uint32_t)));
     GBM_CUDA(cudaMemset(c->dev_err, 0, sizeof(uint32_t)));
+    GBM_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    GBM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    GBM_CUDA(cudaEventCreateWithFlags(&c->ev_scan, cudaEventDisableTiming));
+    GBM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     *out = c;
     return GBM_OK;
 }
@@ -146,6 +150,9 @@ int gbm_ctx_destroy(gbm_ctx *ctx) {
     if (ctx->dev_err) cudaFree(ctx->dev_err);
     if (ctx->prof.rows_dev) cudaFree(ctx->prof.rows_dev);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_scan, ctx->ev_join})
+        if (e) cudaEventDestroy(e);
     delete ctx;
     return GBM_OK;
 }

@@ -111,6 +111,10 @@ struct gbm_ctx {
     int group_units = 0;           // GBM_OPT_GROUP_UNITS (0 = auto = 32)
     int eval_warp = 0;             // GBM_OPT_EVAL_WARP (0 auto, 1 warp per feature, 2 block)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
+    // second stream of gbm_build_tree: the partition scatter of a level overlaps the allreduce
+    // and evaluation of that level (fork / join by events; captured as graph edges)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_scan = nullptr, ev_join = nullptr;
 };
 
 namespace gbm {

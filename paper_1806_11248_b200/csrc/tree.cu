@@ -1760,7 +1760,8 @@ struct EvalArgs {
     const long long *totals_direct; // direct mode: [n_nodes][2]
     FeatBest *fb;                   // [n_nodes][F]
     LgNode *lg;                     // loss-guided mode (null = depth-wise)
-    StepDev *step;                  // loss-guided: the current expansion
+    const StepDev *step;            // loss-guided: the current expansion
+    StepDev *step_next;             // loss-guided: written by the pop of the next step
     long long *hist_pool;           // loss-guided: [max_leaves][TB][2] by LgNode::hslot
 };
 
@@ -2172,7 +2173,7 @@ __device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s) {
     if (threadIdx.x == 0) {
         for (int i = 1; i < (int)(blockDim.x >> 5); ++i) take(s_g[i], s_k[i]);
         const int c = 2 * s + 1;
-        StepDev *step = a.step;
+        StepDev *step = a.step_next;
         s_tiles = 0;
         if (bk < 0) {
             step->k = -1;
@@ -2563,6 +2564,18 @@ static int launch_eval_tree(gbm_ctx *ctx, const EvalArgs &ea, const TreeDev &t, 
     return GBM_OK;
 }
 
+// Fork the side stream off s after the work enqueued so far / join it back.
+static int fork_side(gbm_ctx *ctx, cudaStream_t s) {
+    GBM_CUDA(cudaEventRecord(ctx->ev_fork, s));
+    GBM_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    return GBM_OK;
+}
+static int wait_on(cudaStream_t waiter, cudaEvent_t e, cudaStream_t signaller) {
+    GBM_CUDA(cudaEventRecord(e, signaller));
+    GBM_CUDA(cudaStreamWaitEvent(waiter, e, 0));
+    return GBM_OK;
+}
+
 // Upload the feature-group table when it changed (keeps tree builds free of pageable copies so
 // a whole round can be captured in a CUDA graph).
 static int upload_groups(gbm_ctx *ctx, const HistPlan &hp, Group *groups, ColGroup *cgroups, const Arena &A,
@@ -2608,9 +2621,9 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     need += 2 * (size_t)std::max<long long>(n, 1) * esz + 512;    // ridx buffers
     need += (size_t)max_tiles * (PT / 32) * 4 + 256;              // flags
     need += 2 * (size_t)max_tiles * 4 + 512;                      // tile_left / tile_off
-    need += 3 * 64 + 3 * 256;                                     // tile_base, run_base, n_items
+    need += 6 * 64 + 6 * 256;                                     // tile_base, run_base, n_items x2
     need += (size_t)(cap + 2) * (sizeof(NodeDev) + sizeof(LgNode)) + 512;
-    need += sizeof(StepDev) + 256;
+    need += 2 * (sizeof(StepDev) + 256);
     need += (size_t)G * sizeof(Group) + 256;
     need += (2 * hist_unit + 2) * 8 + 512;                        // root (+ totals), build
     need += (grow ? (size_t)L : 1) * hist_unit * 8 + 256;         // pool
@@ -2622,12 +2635,14 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     uint32_t *flags = A.take<uint32_t>((size_t)max_tiles * (PT / 32));
     int *tile_left = A.take<int>(max_tiles);
     int *tile_off = A.take<int>(max_tiles);
-    int *tile_base = A.take<int>(4);
-    int *run_base = A.take<int>(4);
-    int *n_items = A.take<int>(2);
+    // step plans double-buffered by step parity: step st+1 is popped (by step st's evaluation)
+    // while step st's scatter still reads step st's plan on the side stream
+    int *tile_base_b[2] = {A.take<int>(4), A.take<int>(4)};
+    int *run_base_b[2] = {A.take<int>(4), A.take<int>(4)};
+    int *n_items_b[2] = {A.take<int>(2), A.take<int>(2)};
     NodeDev *nodes = A.take<NodeDev>(cap + 2);
     LgNode *lg = A.take<LgNode>(cap + 2);
-    StepDev *step = A.take<StepDev>(1);
+    StepDev *step_b[2] = {A.take<StepDev>(1), A.take<StepDev>(1)};
     Group *groups = A.take<Group>(G);
     long long *hist_root = A.take<long long>(hist_unit + 2);
     long long *hist_build = A.take<long long>(hist_unit);
@@ -2675,7 +2690,8 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     ea.hist_build = hist_build;
     ea.fb = fb;
     ea.lg = lg;
-    ea.step = step;
+    ea.step = step_b[1];       // (unused at the root)
+    ea.step_next = step_b[0];  // the root's evaluation pops step 0
     ea.hist_pool = hist_pool;
     ea.level = 0;
     ea.first = 0;
@@ -2689,9 +2705,9 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     ea.node_done = done + 1;
     ea.plan_groups = G;
     ea.plan_run = (int)target;  // loss-guided: the pop sizes the work items to the parent
-    ea.tile_base = tile_base;
-    ea.run_base = run_base;
-    ea.n_items = n_items;
+    ea.tile_base = tile_base_b[0];
+    ea.run_base = run_base_b[0];
+    ea.n_items = n_items_b[0];
     ea.tile_left = tile_left;
     ea.plan_mode = grow ? 2 : 0;  // the root's evaluation pops the first expansion
     ea.sel_step = 0;
@@ -2708,13 +2724,9 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     fa.nodes = nodes;
     fa.first = 0;
     fa.n_par = 1;
-    fa.tile_base = tile_base;
-    fa.run_base = run_base;
     fa.n_groups = G;
     fa.run_tiles = run_tiles;
-    fa.n_items = n_items;
     fa.ridx_in = nullptr;
-    fa.step = step;
     fa.bufs[0] = ridx[0];
     fa.bufs[1] = ridx[1];
     fa.flags = flags;
@@ -2734,6 +2746,12 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     ea.hist_store = nullptr;
     for (int st = 0; st < L - 1; ++st) {
         // (the pop of step st ran in the last block of the previous evaluation)
+        StepDev *step = step_b[st & 1];
+        int *tile_base = tile_base_b[st & 1];
+        fa.step = step;
+        fa.tile_base = tile_base;
+        fa.run_base = run_base_b[st & 1];
+        fa.n_items = n_items_b[st & 1];
         GBM_CUDA(cudaMemsetAsync(hist_build, 0, hist_unit * 8, s));
         {
             int slot;
@@ -2741,20 +2759,23 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
             ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
             GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));
         }
+        GBM_TRY(fork_side(ctx, s));  // scan + scatter overlap the allreduce / evaluation
+        cudaStream_t ss = ctx->side;
         {
-            ProfScope ps(ctx, PC_PART_SCAN, s);
-            part_scan_kernel<<<1, 1024, 0, s>>>(nodes, 0, tile_base, tile_left, tile_off, step);
+            ProfScope ps(ctx, PC_PART_SCAN, ss);
+            part_scan_kernel<<<1, 1024, 0, ss>>>(nodes, 0, tile_base, tile_left, tile_off, step);
         }
+        GBM_CUDA(cudaEventRecord(ctx->ev_scan, ss));
         {
             int slot;
             unsigned long long *rc = prof_rows_slot(ctx, &slot);
-            ProfScope ps(ctx, PC_PART_SCATTER, s, 0.0, slot, 8.0);
+            ProfScope ps(ctx, PC_PART_SCATTER, ss, 0.0, slot, 8.0);
             if (hp.carry)
-                part_scatter_kernel<true><<<pgrid, P_THREADS, 0, s>>>(
+                part_scatter_kernel<true><<<pgrid, P_THREADS, 0, ss>>>(
                     nodes, 0, 1, tile_base, flags, tile_off, nullptr, nullptr, reinterpret_cast<const int2 *>(qpair_d),
                     rc, step, ridx[0], ridx[1]);
             else
-                part_scatter_kernel<false><<<pgrid, P_THREADS, 0, s>>>(
+                part_scatter_kernel<false><<<pgrid, P_THREADS, 0, ss>>>(
                     nodes, 0, 1, tile_base, flags, tile_off, nullptr, nullptr, nullptr, rc, step, ridx[0], ridx[1]);
             GBM_CUDA(cudaGetLastError());
         }
@@ -2765,10 +2786,17 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
         ea.first = 2 * st + 1;
         ea.plan_mode = st + 1 < L - 1 ? 2 : 0;
         ea.sel_step = st + 1;
+        ea.step = step;  // this step's parent (node_source) ...
+        ea.step_next = step_b[(st + 1) & 1];  // ... and the pop of the next one
+        ea.tile_base = tile_base_b[(st + 1) & 1];
+        ea.run_base = run_base_b[(st + 1) & 1];
+        ea.n_items = n_items_b[(st + 1) & 1];
+        GBM_CUDA(cudaStreamWaitEvent(s, ctx->ev_scan, 0));  // the pop reads the children's counts
         {
             ProfScope ps(ctx, PC_EVAL, s, (double)hist_unit * 8 * 4.0);
             GBM_TRY(launch_eval_tree(ctx, ea, t, s));
         }
+        GBM_TRY(wait_on(s, ctx->ev_join, ctx->side));
     }
     if (n > 0) {
         ProfScope ps(ctx, PC_PART_FINAL, s, (double)n * 4.0);
@@ -3000,9 +3028,9 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     need += 2 * (size_t)std::max<long long>(n, 1) * 8 + 512;          // ridx entries x2
     need += (size_t)max_tiles * (PT / 32) * 4 + 256;                  // flags
     need += 2 * (size_t)max_tiles * 4 + 512;                          // tile_left/off
-    need += (size_t)(2 * max_par + 2) * 4 + 256;                      // tile base
+    need += 2 * ((size_t)(2 * max_par + 2) * 4 + 256);                // tile base x2
     need += (size_t)(2 * cap + 2) * sizeof(NodeDev) + 256;            // nodes
-    need += (size_t)(2 * max_par + 2) * 4 + 512;                      // run base + count
+    need += 2 * ((size_t)(2 * max_par + 2) * 4 + 512);                // run base + count x2
     need += G * std::max(sizeof(Group), sizeof(ColGroup)) + 256;
     need += (slots * hist_unit + hist_unit + 2) * 8 + 512;            // build + root
     need += 2 * slots * hist_unit * 8 + 512;                          // level hists
@@ -3014,10 +3042,12 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     uint32_t *flags = A.take<uint32_t>((size_t)max_tiles * (PT / 32));
     int *tile_left = A.take<int>(max_tiles);
     int *tile_off = A.take<int>(max_tiles);
-    int *tile_base = A.take<int>(2 * max_par + 2);
+    // plans double-buffered by level parity: level l+1 is planned (by level l's evaluation) while
+    // level l's scatter still reads level l's plan on the side stream
+    int *tile_base_b[2] = {A.take<int>(2 * max_par + 2), A.take<int>(2 * max_par + 2)};
     NodeDev *nodes = A.take<NodeDev>(2 * cap + 2);
-    int *run_base = A.take<int>(2 * max_par + 2);
-    int *n_items = A.take<int>(2);  // [0] items, [1] work counter
+    int *run_base_b[2] = {A.take<int>(2 * max_par + 2), A.take<int>(2 * max_par + 2)};
+    int *n_items_b[2] = {A.take<int>(2), A.take<int>(2)};  // [0] items, [1] work counter
     Group *groups = A.take<Group>(hp.col ? 1 : G);
     ColGroup *cgroups = A.take<ColGroup>(hp.col ? G : 1);
     long long *hist_root = A.take<long long>(hist_unit + 2);  // root histogram + totals
@@ -3094,15 +3124,15 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
     ea.plan_groups = G;
     ea.plan_run = run_tiles;
-    ea.tile_base = tile_base;
-    ea.run_base = run_base;
-    ea.n_items = n_items;
+    ea.tile_base = tile_base_b[1];  // the root's evaluation plans level 1
+    ea.run_base = run_base_b[1];
+    ea.n_items = n_items_b[1];
     ea.level = 0;
     ea.first = 0;
     ea.n_nodes = 1;
     ea.done = done;
     ea.node_done = done + 1;
-    ea.plan_mode = (1 < D) ? 1 : 0;  // the root's eval plans level 1
+    ea.plan_mode = (1 < D) ? 1 : 0;
     {
         ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
         GBM_TRY(launch_eval_tree(ctx, ea, t, s));
@@ -3115,11 +3145,8 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     FusedArgs fa = {};
     fa.qm = qm;
     fa.nodes = nodes;
-    fa.tile_base = tile_base;
-    fa.run_base = run_base;
     fa.n_groups = G;
     fa.run_tiles = run_tiles;
-    fa.n_items = n_items;
     fa.flags = flags;
     fa.tile_left = tile_left;
     fa.row_leaf = row_leaf_d;
@@ -3134,6 +3161,10 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         const int first = (1 << (l - 1)) - 1, n_par = 1 << (l - 1);
         const char *rin = l == 1 ? nullptr : ridx[(l - 1) & 1];
         char *rout = ridx[l & 1];
+        int *tile_base = tile_base_b[l & 1], *run_base = run_base_b[l & 1], *n_items = n_items_b[l & 1];
+        fa.tile_base = tile_base;
+        fa.run_base = run_base;
+        fa.n_items = n_items;
         const double ridx_b = rin ? 4.0 : 0.0;
         if (l == D) {  // final level: every row's leaf by a row-order walk of the tree
             const int n_internal = (1 << D) - 1;
@@ -3204,20 +3235,25 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
                 GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));
             }
         }
+        // side stream: scan + scatter of this level, concurrent with the allreduce and (after the
+        // scan: the plan of level l+1 needs the children's counts) the evaluation
+        GBM_TRY(fork_side(ctx, s));
+        cudaStream_t ss = ctx->side;
         {
-            ProfScope ps(ctx, PC_PART_SCAN, s);
-            part_scan_kernel<<<n_par, 1024, 0, s>>>(nodes, first, tile_base, tile_left, tile_off, nullptr);
+            ProfScope ps(ctx, PC_PART_SCAN, ss);
+            part_scan_kernel<<<n_par, 1024, 0, ss>>>(nodes, first, tile_base, tile_left, tile_off, nullptr);
         }
+        GBM_CUDA(cudaEventRecord(ctx->ev_scan, ss));
         {
             int slot;
             unsigned long long *rc = prof_rows_slot(ctx, &slot);
-            ProfScope ps(ctx, PC_PART_SCATTER, s, 0.0, slot, ridx_b + 4.0);
+            ProfScope ps(ctx, PC_PART_SCATTER, ss, 0.0, slot, ridx_b + 4.0);
             if (hp.carry)
-                part_scatter_kernel<true><<<pgrid, P_THREADS, 0, s>>>(
+                part_scatter_kernel<true><<<pgrid, P_THREADS, 0, ss>>>(
                     nodes, first, n_par, tile_base, flags, tile_off, reinterpret_cast<const uint2 *>(rin),
                     reinterpret_cast<uint2 *>(rout), reinterpret_cast<const int2 *>(qpair_d), rc);
             else
-                part_scatter_kernel<false><<<pgrid, P_THREADS, 0, s>>>(
+                part_scatter_kernel<false><<<pgrid, P_THREADS, 0, ss>>>(
                     nodes, first, n_par, tile_base, flags, tile_off, reinterpret_cast<const uint32_t *>(rin),
                     reinterpret_cast<uint32_t *>(rout), nullptr, rc);
         }
@@ -3233,8 +3269,15 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             ea.hist_prev = l == 1 ? nullptr : hist_lvl[(l - 1) & 1];
             ea.hist_store = (l < D - 1) ? hist_lvl[l & 1] : nullptr;
             ea.plan_mode = (l + 1 < D) ? 1 : 0;  // this level's eval plans level l + 1
-            ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
-            GBM_TRY(launch_eval_tree(ctx, ea, t, s));
+            ea.tile_base = tile_base_b[(l + 1) & 1];
+            ea.run_base = run_base_b[(l + 1) & 1];
+            ea.n_items = n_items_b[(l + 1) & 1];
+            GBM_CUDA(cudaStreamWaitEvent(s, ctx->ev_scan, 0));
+            {
+                ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
+                GBM_TRY(launch_eval_tree(ctx, ea, t, s));
+            }
+            GBM_TRY(wait_on(s, ctx->ev_join, ctx->side));  // join: the next level reads the scatter
         }
     }
     return GBM_OK;
