@@ -299,6 +299,7 @@ class Context:
     RUN_TILES = 3
     GROUP_UNITS = 4
     EVAL_WARP = 5
+    LEAF_WALK = 6
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

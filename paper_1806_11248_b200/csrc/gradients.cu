@@ -51,6 +51,7 @@ __device__ __forceinline__ void grad_hess_s(int obj, double m_or_s, float yl, do
 }
 
 constexpr int G_THREADS = 256;
+constexpr int GU = 4;  // rows in flight per thread in the streaming kernels
 
 // pass 1: per-row (g, h), the block maxima of |g|, |h|; for the logistic objective the
 // sigmoid of each row is kept (sig) so that pass 2 does not evaluate det_exp again
@@ -60,19 +61,30 @@ __global__ void __launch_bounds__(G_THREADS) grad_max_kernel(int obj, const doub
                                                              double *__restrict__ sig, uint32_t *dev_err) {
     double mg = 0.0, mh = 0.0;
     bool bad = false;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const float yl = __ldg(label + i);
-        double v = __ldg(margin + i);
-        if (obj == GBM_LOGISTIC) {
-            v = sigmoid(v);
-            sig[i] = v;
-            bad |= !(yl == 0.0f || yl == 1.0f);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += GU * stride) {
+        float yl[GU];
+        double v[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {  // GU rows' loads in flight
+            const long long i = i0 + u * stride;
+            yl[u] = i < n ? __ldg(label + i) : 0.0f;
+            v[u] = i < n ? __ldg(margin + i) : 0.0;
         }
-        double g, h;
-        grad_hess_s(obj, v, yl, g, h);
-        mg = fmax(mg, fabs(g));
-        mh = fmax(mh, fabs(h));
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            const long long i = i0 + u * stride;
+            if (i >= n) break;
+            if (obj == GBM_LOGISTIC) {
+                v[u] = sigmoid(v[u]);
+                sig[i] = v[u];
+                bad |= !(yl[u] == 0.0f || yl[u] == 1.0f);
+            }
+            double g, h;
+            grad_hess_s(obj, v[u], yl[u], g, h);
+            mg = fmax(mg, fabs(g));
+            mh = fmax(mh, fabs(h));
+        }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(dev_err, DERR_LABEL);
     for (int o = 16; o > 0; o >>= 1) {
@@ -113,19 +125,46 @@ __global__ void __launch_bounds__(G_THREADS) grad_quant_kernel(int obj, int P, c
         scale[0] = sg;
         scale[1] = sh;
     }
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        double g, h;
-        grad_hess_s(obj, obj == GBM_LOGISTIC ? __ldg(sig + i) : __ldg(margin + i), __ldg(label + i), g, h);
-        qpair[i] = make_int2(__double2int_rn(ldexp_exact(g, sg)), __double2int_rn(ldexp_exact(h, sh)));
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const double *src = obj == GBM_LOGISTIC ? sig : margin;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += GU * stride) {
+        double v[GU];
+        float yl[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            const long long i = i0 + u * stride;
+            v[u] = i < n ? __ldg(src + i) : 0.0;
+            yl[u] = i < n ? __ldg(label + i) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            const long long i = i0 + u * stride;
+            if (i >= n) break;
+            double g, h;
+            grad_hess_s(obj, v[u], yl[u], g, h);
+            qpair[i] = make_int2(__double2int_rn(ldexp_exact(g, sg)), __double2int_rn(ldexp_exact(h, sh)));
+        }
     }
 }
 
 __global__ void update_margins_kernel(const double *__restrict__ w, const int32_t *__restrict__ leaf,
                                       long long n, double *__restrict__ margin) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        margin[i] = dadd(margin[i], __ldg(w + __ldg(leaf + i)));
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += GU * stride) {
+        double m[GU];
+        int lf[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            const long long i = i0 + u * stride;
+            m[u] = i < n ? margin[i] : 0.0;
+            lf[u] = i < n ? __ldg(leaf + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n) margin[i] = dadd(m[u], __ldg(w + lf[u]));
+        }
+    }
 }
 
 // LINKED: children of k are left_child[k], left_child[k] + 1 (R27); else heap 2k+1, 2k+2

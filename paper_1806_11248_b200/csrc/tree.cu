@@ -61,6 +61,16 @@ struct StepDev {       // the expansion of the current step, written by lg_selec
     int pad;
 };
 
+struct TreeDev {
+    int8_t *kind;
+    int32_t *feature, *bin;
+    float *threshold;
+    int8_t *default_left;
+    double *gain, *weight;
+    long long *sum_qg, *sum_qh;
+    int32_t *left_child;  // optional for depth-wise trees
+};
+
 struct RangeItem {  // rows [start, start+len) of a row source, one feature group
     int slot, group;
     long long start;
@@ -1337,6 +1347,86 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_reg_kernel(QM qm, cons
     }
 }
 
+// Staged variant: a warp loads 32 whole rows (W words each, contiguous) with W coalesced loads
+// into shared memory (row pitch W|1 words: conflict-free), then each lane walks its row from
+// registers.  Moves exactly the packed bytes once, in row order (vs a 32-byte sector per level
+// and row for the feature-major gathers of leaf_walk_kernel once the rows' nodes diverge).
+template <int W>
+__global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, const int8_t *__restrict__ kind,
+                                                                     const int32_t *__restrict__ feature,
+                                                                     const int32_t *__restrict__ bin,
+                                                                     const int8_t *__restrict__ dl, int n_internal,
+                                                                     int depth, long long n,
+                                                                     int32_t *__restrict__ row_leaf) {
+    constexpr int PW = W | 1;
+    extern __shared__ int s_tree[];
+    __shared__ uint32_t s_rows[WALK_THREADS / 32][32 * PW];
+    int *s_f = s_tree, *s_b = s_tree + n_internal;
+    for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
+        s_f[k] = kind[k] == GBM_NODE_SPLIT ? (feature[k] | ((int)dl[k] << 20) | (1 << 21)) : 0;
+        s_b[k] = bin[k];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *sr = s_rows[wid];
+    const long long n_chunks = (n + 31) / 32;
+    const long long cstep = (long long)gridDim.x * (WALK_THREADS / 32);
+    uint32_t v[W];
+    auto load = [&](long long c) {  // chunk c's words into registers (coalesced)
+        const uint32_t *src = qm.P + c * 32 * W;
+        const long long rows_c = c < n_chunks ? min(32ll, n - c * 32) : 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int j = lane + 32 * k;
+            v[k] = j / W < rows_c ? __ldg(src + j) : 0u;
+        }
+    };
+    long long c = blockIdx.x * (long long)(WALK_THREADS / 32) + wid;
+    if (c < n_chunks) load(c);
+    for (; c < n_chunks; c += cstep) {
+        const long long rows_here = min(32ll, n - c * 32);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int j = lane + 32 * k;
+            sr[(j / W) * PW + j % W] = v[k];
+        }
+        __syncwarp();
+        load(c + cstep);  // the next chunk's loads fly during this chunk's walk
+        if (lane < rows_here) {  // walk on the staged row: one shared-memory read per level
+            const uint32_t *row = sr + lane * PW;
+            const uint32_t mask = (1u << qm.bits) - 1u;
+            int k = 0;
+            for (int d = 0; d < depth; ++d) {
+                const int fk = s_f[k];
+                if (!(fk & (1 << 21))) break;
+                const int bp = (fk & 0xfffff) * qm.bits, wi = bp >> 5, off = bp & 31;
+                uint64_t v = row[wi];
+                if (off + qm.bits > 32) v |= (uint64_t)row[wi + 1] << 32;
+                const int sym = (int)((uint32_t)(v >> off) & mask);
+                const bool left = sym == qm.B ? ((fk >> 20) & 1) : (sym <= s_b[k]);
+                k = left ? 2 * k + 1 : 2 * k + 2;
+            }
+            row_leaf[c * 32 + lane] = k;
+        }
+        __syncwarp();
+    }
+}
+
+// Deep trees (the heap of internal nodes does not fit shared memory): tree read through L1.
+__global__ void __launch_bounds__(WALK_THREADS) leaf_walk_global_kernel(QM qm, TreeDev t, int depth, long long n,
+                                                                        int32_t *__restrict__ row_leaf) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x) {
+        int k = 0;
+        for (int d = 0; d < depth && __ldg(t.kind + k) == GBM_NODE_SPLIT; ++d) {
+            const int sym = (int)split_symbol(qm, r, __ldg(t.feature + k));
+            const bool left = sym == qm.B ? __ldg(t.default_left + k) != 0 : sym <= __ldg(t.bin + k);
+            k = left ? 2 * k + 1 : 2 * k + 2;
+        }
+        row_leaf[r] = k;
+    }
+}
+
 // ============================================================== scan + scatter
 __device__ __forceinline__ long long block_exscan(long long v, long long *total, long long *sm32) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1861,16 +1951,6 @@ __device__ __forceinline__ double leaf_weight(long long Tg, long long Th, int sg
     w = -w;
     return dmul(w, eta);
 }
-
-struct TreeDev {
-    int8_t *kind;
-    int32_t *feature, *bin;
-    float *threshold;
-    int8_t *default_left;
-    double *gain, *weight;
-    long long *sum_qg, *sum_qh;
-    int32_t *left_child;  // optional for depth-wise trees
-};
 
 __device__ __forceinline__ void write_leaf(const TreeDev &t, int k, long long Tg, long long Th, int sg, int sh,
                                            const EvalParams &p) {
@@ -2509,8 +2589,8 @@ static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStr
 template <int W>
 static void launch_walk_reg(int grid, size_t sm, cudaStream_t s, const QM &qm, const TreeDev &t, int n_int, int D,
                             long long n, int32_t *rl) {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(leaf_walk_reg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    leaf_walk_reg_kernel<W><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl);
+    if (sm > 16 * 1024) cudaFuncSetAttribute(leaf_walk_stg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    leaf_walk_stg_kernel<W><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl);
 }
 
 static TreeDev tree_dev(const gbm_tree *t) {
@@ -3172,10 +3252,12 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             ProfScope ps(ctx, PC_PART_FINAL, s, (double)n * (q->bits * D / 8.0 + 4.0));
             const int grid = (int)std::max<long long>(1, std::min<long long>((n + WALK_THREADS - 1) / WALK_THREADS,
                                                                             (long long)ctx->sm_count * 8));
-            // with the feature-major copy the walk reads one byte per level (coalesced at the top
-            // levels); without it the row's words are loaded once into registers
+            // rows of whole words: staged row-order walk (each packed byte read once); else the
+            // feature-major copy (one byte per level) or per-level gathers from the packed rows
             const int W = (qm.stride % 32 == 0) ? (int)(qm.stride / 32) : 0;
-            if (n > 0 && !qm.col && W >= 1 && W <= 16) {
+            if (n > 0 && sm > 64 * 1024) {
+                leaf_walk_global_kernel<<<grid, WALK_THREADS, 0, s>>>(qm, t, D, n, row_leaf_d);
+            } else if (n > 0 && W >= 1 && W <= 16 && ctx->walk_mode != 1) {
                 switch (W) {
 #define GBM_WALK(w) case w: launch_walk_reg<w>(grid, sm, s, qm, t, n_internal, D, n, row_leaf_d); break;
                     GBM_WALK(1) GBM_WALK(2) GBM_WALK(3) GBM_WALK(4) GBM_WALK(5) GBM_WALK(6) GBM_WALK(7) GBM_WALK(8)

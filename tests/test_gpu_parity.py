@@ -308,6 +308,22 @@ def test_eval_variant_rounds_parity(ctx, G, cfg, n, missing, grow, mode):
     ctx.set_option(ctx.EVAL_WARP, 0)
 
 
+@pytest.mark.parametrize("walk", [0, 1])
+@pytest.mark.parametrize("D", [3, 12, 16])
+def test_deep_trees_and_leaf_walks(ctx, G, D, walk):
+    """max_depth up to the ABI limit (16: the heap of internal nodes no longer fits shared memory)
+    and both final-level walks (staged rows / feature-major copy)."""
+    ctx.set_option(ctx.LEAF_WALK, walk)
+    X, y = W.generate("tiny", 0, 3000, n_rows=3000, missing=0.05)
+    ob = O.Booster(X, y, max_bins=64, objective="reg:squarederror", max_depth=D, mcw=0.0)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=64, objective="reg:squarederror", max_depth=D,
+                   base_margin=ob.base_margin, min_child_weight=0.0)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+    ctx.set_option(ctx.LEAF_WALK, 0)
+
+
 def test_max_depth_zero_and_one(ctx, G):
     X, y = W.generate("tiny")
     for D in (0, 1):
