@@ -324,6 +324,48 @@ def test_deep_trees_and_leaf_walks(ctx, G, D, walk):
     ctx.set_option(ctx.LEAF_WALK, 0)
 
 
+def _edge_matrix(kind):
+    rng = np.random.default_rng(77)
+    if kind == "one_row":
+        X = np.array([[1.5, -2.0, 0.25]], np.float32)
+    elif kind == "ragged_33":
+        X = W.random_matrix(5, 33, 4, distinct=7, missing=0.1)
+    elif kind == "one_feature":
+        X = W.random_matrix(6, 5000, 1)
+    elif kind == "constant_and_missing_features":
+        X = W.random_matrix(7, 4000, 5, missing=0.05)
+        X[:, 1] = 3.0            # one bin
+        X[:, 3] = np.nan         # no cuts at all
+    elif kind == "many_features_few_rows":
+        X = W.random_matrix(8, 64, 300, distinct=5, missing=0.2)
+    elif kind == "wide_bins_9bit":
+        X = W.random_matrix(9, 20000, 3)
+        X[rng.random(X.shape) < 0.01] = np.nan
+    else:
+        raise KeyError(kind)
+    y = (np.nan_to_num(X[:, 0]) + rng.standard_normal(X.shape[0]) > 0).astype(np.float32)
+    return X, y
+
+
+@pytest.mark.parametrize("grow", ["depthwise", "lossguide"])
+@pytest.mark.parametrize("kind", ["one_row", "ragged_33", "one_feature", "constant_and_missing_features",
+                                  "many_features_few_rows", "wide_bins_9bit"])
+def test_edge_shapes_parity(ctx, G, kind, grow):
+    """Degenerate shapes: one row, ragged tails, one feature, a constant feature and an
+    all-missing feature, more features than rows, 9-bit symbols from 256 bins + missing."""
+    X, y = _edge_matrix(kind)
+    B = 256 if kind == "wide_bins_9bit" else 16
+    L = 7 if grow == "lossguide" else 0
+    kw = dict(max_bins=B, objective="binary:logistic", max_depth=4, grow_policy=grow, max_leaves=L)
+    ob = O.Booster(X, y, mcw=0.0, **kw)
+    gb = G.Booster(ctx, dev(X), dev(y), base_margin=ob.base_margin, min_child_weight=0.0, **kw)
+    for _ in range(3):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
+
+
 def test_max_depth_zero_and_one(ctx, G):
     X, y = W.generate("tiny")
     for D in (0, 1):
