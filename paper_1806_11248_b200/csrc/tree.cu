@@ -92,6 +92,18 @@ constexpr int PT = 2048;         // partition tile (rows): 16 warps x 128 rows
 constexpr int WROWS = PT / 16;   // rows per warp per tile
 constexpr int P_THREADS = 256;   // partition kernels: 8 warps x 4 ballot words
 constexpr int H_THREADS = 512;   // histogram / fused kernels
+#ifndef GBM_PH_UNR
+#define GBM_PH_UNR 4
+#endif
+#ifndef GBM_PH_MINB
+#define GBM_PH_MINB 3
+#endif
+constexpr int PH_UNR = GBM_PH_UNR;    // rows in flight per lane in the fused level kernel's byte path
+// resident blocks the fused level kernel is compiled for: the byte path runs best with the
+// register room of 2 blocks (Higgs 1.86 vs 1.97 ms/round, Epsilon 5.09 vs 5.18), the generic path
+// with the occupancy of 3 (Bosch 4.73 vs 5.04)
+constexpr int PH_MINB = GBM_PH_MINB;
+constexpr int PH_MINB_BYTE = 2;
 constexpr int RUN_MAX = 16;      // tiles per fused work item: chosen per tree (flush amortisation
                                  // vs. enough items for every resident block)
 constexpr int E_THREADS = 256;   // evaluation kernels
@@ -501,7 +513,7 @@ struct FusedArgs {
 // warp's left count into tile_left, the rows of the built child compacted into a warp-private
 // list; (B) the listed rows' words accumulated by the warp (lane -> fixed word of the row).
 template <bool WIDE, bool BYTE, bool SENT, bool CARRY>
-__global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part_hist_kernel(FusedArgs a) {
     using E = typename EntryOf<CARRY>::T;
     extern __shared__ int smem[];
     __shared__ int s_off[2049];
@@ -630,19 +642,19 @@ __global__ void __launch_bounds__(H_THREADS, 3) part_hist_kernel(FusedArgs a) {
             } else if (BYTE) {
                 if (my_r >= 0) {
                     int rr = my_r;
-                    for (; rr + 3 * rpp < nbuild; rr += 4 * rpp) {
-                        E ew[4];
-                        uint32_t wd[4];
-                        int2 qq[4];
+                    for (; rr + (PH_UNR - 1) * rpp < nbuild; rr += PH_UNR * rpp) {
+                        E ew[PH_UNR];
+                        uint32_t wd[PH_UNR];
+                        int2 qq[PH_UNR];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) ew[i] = wrows[rr + i * rpp];
+                        for (int i = 0; i < PH_UNR; ++i) ew[i] = wrows[rr + i * rpp];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
+                        for (int i = 0; i < PH_UNR; ++i) {
                             wd[i] = __ldg(qm.P + row_of(ew[i]) * sw + my_u);
                             qq[i] = entry_q(ew[i], a.qpair);
                         }
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
+                        for (int i = 0; i < PH_UNR; ++i)
 #pragma unroll
                             for (int jj = 0; jj < 4; ++jj) {
                                 const int sy = (wd[i] >> (8 * jj)) & 255;
