@@ -98,6 +98,9 @@ constexpr int H_THREADS = 512;   // histogram / fused kernels
 #ifndef GBM_PH_MINB
 #define GBM_PH_MINB 3
 #endif
+#ifndef GBM_HR_MINB  // root histogram kernel: 2 resident blocks (Bosch root 1.65 vs 1.86 ms at 3)
+#define GBM_HR_MINB 2
+#endif
 constexpr int PH_UNR = GBM_PH_UNR;    // rows in flight per lane in the fused level kernel's byte path
 // resident blocks the fused level kernel is compiled for: the byte path runs best with the
 // register room of 2 blocks (Higgs 1.86 vs 1.97 ms/round, Epsilon 5.09 vs 5.18), the generic path
@@ -336,7 +339,7 @@ struct RangeArgs {
 };
 
 template <bool WIDE, bool BYTE, bool SENT>
-__global__ void __launch_bounds__(H_THREADS) hist_range_kernel(RangeArgs a) {
+__global__ void __launch_bounds__(H_THREADS, GBM_HR_MINB) hist_range_kernel(RangeArgs a) {
     extern __shared__ int smem[];
     __shared__ int s_off[2049];
     __shared__ long long s_red[2 * H_THREADS / 32];
