@@ -186,6 +186,9 @@ def run_ours(a, world, rank, local):
     # ---- device-resident run: inputs already in HBM when the timed region starts
     Xd = torch.from_numpy(X).to(dev)
     yd = torch.from_numpy(y).to(dev)
+    # warm the one-time kernels (lazy module loading, attributes) on a small slice, untimed
+    m = min(4096, n)
+    ctx.make_qmatrix(Xd[:m].contiguous(), cfg.max_bins, 32, cuts=ctx.cuts(Xd[:m].contiguous(), cfg.max_bins))
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
