@@ -309,6 +309,21 @@ def test_eval_variant_rounds_parity(ctx, G, cfg, n, missing, grow, mode):
 
 
 @pytest.mark.parametrize("walk", [0, 1])
+def test_lossguide_leaf_walks(ctx, G, walk):
+    """Loss-guided final assignment: staged linked walk (0) and the gather walk (1)."""
+    ctx.set_option(ctx.LEAF_WALK, walk)
+    X, y = W.generate("higgs", 0, 40_000)
+    kw = dict(max_bins=256, objective="binary:logistic", max_depth=12, grow_policy="lossguide",
+              max_leaves=40)
+    ob = O.Booster(X, y, **kw)
+    gb = G.Booster(ctx, dev(X), dev(y), base_margin=ob.base_margin, **kw)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+    ctx.set_option(ctx.LEAF_WALK, 0)
+
+
+@pytest.mark.parametrize("walk", [0, 1])
 @pytest.mark.parametrize("D", [3, 12, 16])
 def test_deep_trees_and_leaf_walks(ctx, G, D, walk):
     """max_depth up to the ABI limit (16: the heap of internal nodes no longer fits shared memory)
