@@ -1317,22 +1317,20 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const in
 // into shared memory (row pitch W|1 words: conflict-free), then each lane walks its row from
 // registers.  Moves exactly the packed bytes once, in row order (vs a 32-byte sector per level
 // and row for the feature-major gathers of leaf_walk_kernel once the rows' nodes diverge).
-template <int W, bool LINKED>
+template <int W>
 __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, const int8_t *__restrict__ kind,
                                                                      const int32_t *__restrict__ feature,
                                                                      const int32_t *__restrict__ bin,
-                                                                     const int8_t *__restrict__ dl,
-                                                                     const int32_t *__restrict__ left_child,
-                                                                     int n_internal, int depth, long long n,
+                                                                     const int8_t *__restrict__ dl, int n_internal,
+                                                                     int depth, long long n,
                                                                      int32_t *__restrict__ row_leaf) {
     constexpr int PW = W | 1;
     extern __shared__ int s_tree[];
     __shared__ uint32_t s_rows[WALK_THREADS / 32][32 * PW];
-    int *s_f = s_tree, *s_b = s_tree + n_internal, *s_l = s_tree + 2 * n_internal;
+    int *s_f = s_tree, *s_b = s_tree + n_internal;
     for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
         s_f[k] = kind[k] == GBM_NODE_SPLIT ? (feature[k] | ((int)dl[k] << 20) | (1 << 21)) : 0;
         s_b[k] = bin[k];
-        if (LINKED) s_l[k] = left_child[k];
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1364,7 +1362,7 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
             const uint32_t *row = sr + lane * PW;
             const uint32_t mask = (1u << qm.bits) - 1u;
             int k = 0;
-            for (int d = 0; LINKED || d < depth; ++d) {
+            for (int d = 0; d < depth; ++d) {
                 const int fk = s_f[k];
                 if (!(fk & (1 << 21))) break;
                 const int bp = (fk & 0xfffff) * qm.bits, wi = bp >> 5, off = bp & 31;
@@ -1372,8 +1370,7 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
                 if (off + qm.bits > 32) v |= (uint64_t)row[wi + 1] << 32;
                 const int sym = (int)((uint32_t)(v >> off) & mask);
                 const bool left = sym == qm.B ? ((fk >> 20) & 1) : (sym <= s_b[k]);
-                if (LINKED) k = left ? s_l[k] : s_l[k] + 1;
-                else k = left ? 2 * k + 1 : 2 * k + 2;
+                k = left ? 2 * k + 1 : 2 * k + 2;
             }
             row_leaf[c * 32 + lane] = k;
         }
@@ -2560,9 +2557,8 @@ static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStr
 template <int W>
 static void launch_walk_reg(int grid, size_t sm, cudaStream_t s, const QM &qm, const TreeDev &t, int n_int, int D,
                             long long n, int32_t *rl) {
-    if (sm > 16 * 1024) cudaFuncSetAttribute(leaf_walk_stg_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    leaf_walk_stg_kernel<W, false><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
-                                                                  nullptr, n_int, D, n, rl);
+    if (sm > 16 * 1024) cudaFuncSetAttribute(leaf_walk_stg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    leaf_walk_stg_kernel<W><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl);
 
 }
 
