@@ -504,3 +504,33 @@ def test_single_rank_communicator_paths(G):
     c.allreduce_histograms(h)
     assert h.cpu().tolist() == list(range(10))
     c.close()
+
+
+@pytest.mark.parametrize("grow", ["depthwise", "lossguide"])
+def test_graph_captured_rounds_with_communicator(G, grow):
+    """bench.py's launch configuration at N > 1: whole rounds captured as CUDA graphs with the
+    NCCL collectives (C1 max, C2 histogram sums) and the side-stream scatter inside, here with a
+    1-rank communicator.  Every replayed round equals the oracle's."""
+    X, y = W.generate("higgs", 0, 60_000)
+    c = G.Context(0)
+    c.comm_init(G.Context.comm_unique_id(), 1, 0)
+    L = 24 if grow == "lossguide" else 0
+    kw = dict(max_bins=256, objective="binary:logistic", max_depth=6, eta=0.1, grow_policy=grow,
+              max_leaves=L)
+    ob = O.Booster(X, y, **kw)
+    gb = G.Booster(c, dev(X), dev(y), base_margin=ob.base_margin, **kw)
+    _compare_tree(gb.round(keep_tree=False).to_numpy(), ob.round())  # eager round 1
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph):
+            tree = gb.round(keep_tree=False)
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(3):
+        graph.replay()
+        torch.cuda.synchronize()
+        _compare_tree(tree.to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    del graph
+    c.close()
