@@ -56,6 +56,9 @@ def parse():
                     help="lossguide: priority-queue growth (P:65) with --max-leaves")
     ap.add_argument("--max-leaves", type=int, default=None,
                     help="lossguide leaf budget (default 2^max_depth of the config)")
+    ap.add_argument("--comm", action="store_true",
+                    help="initialise torch.distributed + the NCCL communicator even for one rank "
+                         "(exercises the N > 1 code path on one GPU)")
     ap.add_argument("--max-depth", type=int, default=None,
                     help="depth limit (default: the config's; lossguide default 16)")
     a = ap.parse_args()
@@ -158,12 +161,12 @@ def run_ours(a, world, rank, local):
         beta = 0.0
     else:
         s = torch.tensor([float(np.sum(y.astype(np.float64))), float(len(y))], dtype=torch.float64)
-        if world > 1:
+        if a.dist:
             s = s.to(dev)
             dist.all_reduce(s)
         beta = float(s[0] / s[1])
     ctx = G.Context(local)
-    if world > 1:
+    if a.dist:
         ctx.comm_init_from_torch()
     kw = dict(max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
               eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
@@ -172,12 +175,12 @@ def run_ours(a, world, rank, local):
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if world > 1:
+        if a.dist:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        if world == 1:
+        if not a.dist:
             return v
         t = torch.tensor([v], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -421,16 +424,22 @@ def main():
     a.leaves = a.max_leaves if a.max_leaves is not None else (
         2 ** cfg0.max_depth if a.grow_policy == "lossguide" else 0)
     world, rank, local = dist_env()
-    if world > 1:
+    a.dist = world > 1 or (a.comm and a.impl == "ours")
+    if a.dist:
         import torch
         import torch.distributed as dist
+        if world == 1:  # --comm without torchrun: a one-rank group on the loopback interface
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29561")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if a.impl == "reference":
         rc = 0
         if rank == 0:
             rc = run_reference(a)
-        if world > 1:
+        if a.dist:
             import torch.distributed as dist
             dist.destroy_process_group()
         return rc
@@ -470,7 +479,7 @@ def main():
         print(line)
         if a.json_out:
             open(a.json_out, "w").write(line + "\n")
-    if world > 1:
+    if a.dist:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
