@@ -88,6 +88,12 @@ struct FeatBest {  // best candidate of one (node, feature)
     long long Lg, Lh;
 };
 
+// what the finishing block already knows about a node (skips a second node_source round trip)
+struct NodeKnown {
+    int state;  // 0 unknown, 1 present with totals Tg, Th, 2 absent
+    long long Tg, Th;
+};
+
 constexpr int PT = 2048;         // partition tile (rows): 16 warps x 128 rows
 constexpr int WROWS = PT / 16;   // rows per warp per tile
 constexpr int P_THREADS = 256;   // partition kernels: 8 warps x 4 ballot words
@@ -1889,18 +1895,19 @@ __device__ __forceinline__ void eval_warp(const EvalArgs &a, long long gw) {
 }
 
 // one block per (node, feature) = blk: the feature's best candidate into fb[blk]
-__device__ __forceinline__ void eval_block(const EvalArgs &a, long long blk) {
+__device__ __forceinline__ NodeKnown eval_block(const EvalArgs &a, long long blk) {
     const int j = (int)(blk / a.F), f = (int)(blk - (long long)j * a.F);
     NodeHist src;
     long long Tg, Th;
-    if (!node_source(a, j, src, Tg, Th)) return;                    // block-uniform
-    if (a.lg && a.lg[a.first + j].depth >= a.p.max_depth) return;  // a leaf: not evaluated
+    if (!node_source(a, j, src, Tg, Th)) return NodeKnown{2, 0, 0};               // block-uniform
+    if (a.lg && a.lg[a.first + j].depth >= a.p.max_depth) return NodeKnown{1, Tg, Th};  // a leaf
     const int sg = a.scale[0], sh = a.scale[1];
     const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
     const double e = ddiv(dmul(G, G), dadd(H, a.p.lambda));
     const int b0 = __ldg(a.cut_ptr + f), nbf = __ldg(a.cut_ptr + f + 1) - b0;
     const FeatBest b = eval_feature_blk(src, b0, nbf, Tg, Th, sg, sh, e, a.p);
     if (threadIdx.x == 0) a.fb[blk] = b;
+    return NodeKnown{1, Tg, Th};
 }
 
 __global__ void __launch_bounds__(E_THREADS) eval_feat_kernel(EvalArgs a) {
@@ -1927,22 +1934,15 @@ __device__ __forceinline__ void write_leaf(const TreeDev &t, int k, long long Tg
     t.weight[k] = leaf_weight(Tg, Th, sg, sh, p.lambda, p.eta);
 }
 
-__device__ __forceinline__ int feature_of_bin(const int32_t *__restrict__ cut_ptr, int F, int gbin) {
-    int lo = 0, hi = F - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(cut_ptr + mid) <= gbin) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
 
 // block-wide canonical argmax over the features of node j
-__device__ FeatBest reduce_node(const EvalArgs &a, int j) {
+__device__ FeatBest reduce_node(const EvalArgs &a, int j, int &feat) {
     __shared__ double s_g[E_THREADS / 32];
     __shared__ long long s_i[E_THREADS / 32], s_lg[E_THREADS / 32], s_lh[E_THREADS / 32];
+    __shared__ int s_f[E_THREADS / 32];
     double bg = 0.0;
     long long bi = LLONG_MAX, blg = 0, blh = 0;
+    int bf = -1;  // feature of the best candidate (no binary search over cut_ptr afterwards)
     for (int f = threadIdx.x; f < a.F; f += E_THREADS) {
         const FeatBest *cp = a.fb + (long long)j * a.F + f;
         FeatBest c;
@@ -1951,32 +1951,35 @@ __device__ FeatBest reduce_node(const EvalArgs &a, int j) {
         c.Lg = __ldcg(&cp->Lg);
         c.Lh = __ldcg(&cp->Lh);
         if (better(c.gain, c.idx, bg, bi)) {
-            bg = c.gain; bi = c.idx; blg = c.Lg; blh = c.Lh;
+            bg = c.gain; bi = c.idx; blg = c.Lg; blh = c.Lh; bf = f;
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
         const double og = __shfl_xor_sync(0xffffffffu, bg, o);
         const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
         const long long olg = __shfl_xor_sync(0xffffffffu, blg, o), olh = __shfl_xor_sync(0xffffffffu, blh, o);
+        const int of = __shfl_xor_sync(0xffffffffu, bf, o);
         if (better(og, oi, bg, bi)) {
-            bg = og; bi = oi; blg = olg; blh = olh;
+            bg = og; bi = oi; blg = olg; blh = olh; bf = of;
         }
     }
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        s_g[w] = bg; s_i[w] = bi; s_lg[w] = blg; s_lh[w] = blh;
+        s_g[w] = bg; s_i[w] = bi; s_lg[w] = blg; s_lh[w] = blh; s_f[w] = bf;
     }
     __syncthreads();
     FeatBest r;
     r.gain = s_g[0]; r.idx = s_i[0]; r.Lg = s_lg[0]; r.Lh = s_lh[0];
+    feat = s_f[0];
     for (int i = 1; i < E_THREADS / 32; ++i)
         if (better(s_g[i], s_i[i], r.gain, r.idx)) {
-            r.gain = s_g[i]; r.idx = s_i[i]; r.Lg = s_lg[i]; r.Lh = s_lh[i];
+            r.gain = s_g[i]; r.idx = s_i[i]; r.Lg = s_lg[i]; r.Lh = s_lh[i]; feat = s_f[i];
         }
     return r;
 }
 
-__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j);
+
+__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j, NodeKnown kn);
 __device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s);
 
 // Tree mode, one launch per level / loss-guided step: warp per (node, feature) evaluation; the
@@ -1986,12 +1989,13 @@ __device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s);
 // before the counter it is published by, and the finisher fences before reading.
 // nodes fin[0..nfin) were completed by this block: reduce them; count them; the block that
 // completes the level plans / pops the next step
-__device__ void eval_finish(const EvalArgs &a, const TreeDev &t, const int *fin, int nfin) {
+__device__ void eval_finish(const EvalArgs &a, const TreeDev &t, const int *fin, int nfin,
+                            const NodeKnown *known) {
     __shared__ bool s_last;
     __threadfence();
     for (int i = 0; i < nfin; ++i) {
         const int j = fin[i];
-        eval_final_body(a, t, j);
+        eval_final_body(a, t, j, known ? known[i] : NodeKnown{0, 0, 0});
         __syncthreads();
         if (threadIdx.x == 0) a.node_done[j] = 0;
     }
@@ -2032,7 +2036,7 @@ __global__ void __launch_bounds__(E_THREADS) eval_tree_kernel(EvalArgs a, TreeDe
     }
     __syncthreads();
     if (s_nfin == 0) return;
-    eval_finish(a, t, s_fin, s_nfin);
+    eval_finish(a, t, s_fin, s_nfin, nullptr);
 }
 
 // block per (node, feature); the block completing a node's last feature reduces the node
@@ -2040,7 +2044,7 @@ __global__ void __launch_bounds__(E_THREADS) eval_tree_blk_kernel(EvalArgs a, Tr
     __shared__ int s_fin[1];
     __shared__ int s_nfin;
     const long long blk = blockIdx.x;
-    eval_block(a, blk);
+    const NodeKnown kn = eval_block(a, blk);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2050,14 +2054,14 @@ __global__ void __launch_bounds__(E_THREADS) eval_tree_blk_kernel(EvalArgs a, Tr
     }
     __syncthreads();
     if (s_nfin == 0) return;
-    eval_finish(a, t, s_fin, 1);
+    eval_finish(a, t, s_fin, 1, &kn);
 }
 
-__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j) {
+__device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j, NodeKnown kn) {
     const int k = a.first + j;
     NodeHist src;
-    long long Tg, Th;
-    const bool exists = node_source(a, j, src, Tg, Th);
+    long long Tg = kn.Tg, Th = kn.Th;
+    const bool exists = kn.state == 0 ? node_source(a, j, src, Tg, Th) : kn.state == 1;
     if (!exists) {
         if (threadIdx.x == 0) a.nodes[k].state = GBM_NODE_ABSENT;
         return;
@@ -2073,7 +2077,8 @@ __device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j) {
         }
         return;
     }
-    const FeatBest b = reduce_node(a, j);
+    int f;
+    const FeatBest b = reduce_node(a, j, f);
     if (threadIdx.x != 0) return;
     NodeDev &nd = a.nodes[k];
     nd.Tg = Tg;
@@ -2088,7 +2093,6 @@ __device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j) {
         return;
     }
     const int gbin = (int)(b.idx >> 1), dl = (b.idx & 1) == 0;
-    const int f = feature_of_bin(a.cut_ptr, a.F, gbin);
     const int bb = gbin - __ldg(a.cut_ptr + f);
     if (a.lg) {  // loss-guided: a leaf until lg_select_kernel pops it (R25)
         t.kind[k] = GBM_NODE_LEAF;
@@ -2130,7 +2134,8 @@ __global__ void __launch_bounds__(E_THREADS) eval_out_kernel(EvalArgs a, int8_t 
                                                              int32_t *bin_d, int8_t *dl_d, double *gain_d,
                                                              long long *child_d) {
     const int j = blockIdx.x;
-    const FeatBest b = reduce_node(a, j);
+    int bf;
+    const FeatBest b = reduce_node(a, j, bf);
     if (threadIdx.x != 0) return;
     const long long Tg = a.totals_direct[2 * j], Th = a.totals_direct[2 * j + 1];
     const bool found = b.idx != LLONG_MAX;
@@ -2140,7 +2145,7 @@ __global__ void __launch_bounds__(E_THREADS) eval_out_kernel(EvalArgs a, int8_t 
     if (found) {
         const int gbin = (int)(b.idx >> 1);
         dl = (b.idx & 1) == 0;
-        f = feature_of_bin(a.cut_ptr, a.F, gbin);
+        f = bf;
         bb = gbin - __ldg(a.cut_ptr + f);
     }
     feature_d[j] = f;
