@@ -104,9 +104,14 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   one block per (node, feature), one bin per thread (2); 0 (default) = warps when there are
  *   at least 16 per SM, else blocks.
  * GBM_OPT_LEAF_WALK: final-level leaf assignment of a depth-wise tree: 0 (default) rows of whole
- *   words staged through shared memory in row order; 1 the feature-major symbol copy. */
+ *   words staged through shared memory in row order; 1 the feature-major symbol copy.
+ * GBM_OPT_EVAL_SCREEN: 1 EvaluateSplit computes the exact gain (two IEEE divisions) only for
+ *   candidates that pass an approximate screen proven never to drop the exact argmax or a tie
+ *   with it (tree.cu, screen_score); 0 (default: measured faster, the evaluation is bound by
+ *   memory and latency, not by the divisions) evaluates every candidate exactly.  Results are
+ *   identical either way. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
-       GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6 };
+       GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

@@ -300,6 +300,7 @@ class Context:
     GROUP_UNITS = 4
     EVAL_WARP = 5
     LEAF_WALK = 6
+    EVAL_SCREEN = 7
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

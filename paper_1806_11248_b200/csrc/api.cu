@@ -274,6 +274,10 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->eval_warp = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_EVAL_SCREEN) {
+        ctx->eval_screen = value != 0;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_LEAF_WALK) {
         if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_LEAF_WALK: 0 auto, 1 feature-major copy");
         ctx->walk_mode = (int)value;

@@ -122,6 +122,7 @@ constexpr int DUMMY_BINS = 32;   // scratch bins: padding features of the byte p
 struct EvalParams {
     double eta, lambda, gamma, mcw;
     int max_depth;
+    int screen;  // 1: exact evaluation only of candidates that pass the approximate screen
 };
 
 // ============================================================== shared-memory histogram
@@ -1597,6 +1598,58 @@ __device__ __forceinline__ void eval_candidate(long long Pg, long long Ph, long 
     }
 }
 
+// Exact-preserving screen.  Every candidate's gain is a monotone non-decreasing function of
+// s = GL^2/(HL+lambda) + GR^2/(HR+lambda) (R8: d = a + c, d -= e, d *= 0.5, gain = d - gamma, each
+// correctly rounded), so the canonical argmax -- and every candidate whose gain can tie with it --
+// lies among the candidates whose s is within rounding of the largest s.  s~ below is s computed
+// with a Newton-refined hardware reciprocal (relative error < 2^-38 from a >= 2^-10 seed, two
+// non-negative terms), and a candidate is evaluated exactly iff s~ >= (1 - 2^-16) max s~: the
+// exact best is never screened out, while almost every other candidate skips its two IEEE
+// divisions.  Returns -1 for an invalid candidate (same validity test as eval_candidate).
+__device__ __forceinline__ double rcp_refined(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double r = fma(-x, y, 1.0);
+    return fma(y, r, y);
+}
+__device__ __forceinline__ double screen_score(long long Pg, long long Ph, long long Mg, long long Mh, long long Tg,
+                                               long long Th, int sg, int sh, const EvalParams &p, int dli) {
+    const bool dl = dli == 0;
+    const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
+    const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
+    const double GR = fixed_to_double(Tg - Lg, sg), HR = fixed_to_double(Th - Lh, sh);
+    const double xl = dadd(HL, p.lambda), xr = dadd(HR, p.lambda);
+    if (!(HL >= p.mcw && HR >= p.mcw && xl > 0.0 && xr > 0.0)) return -1.0;
+    return dadd(dmul(dmul(GL, GL), rcp_refined(xl)), dmul(dmul(GR, GR), rcp_refined(xr)));
+}
+constexpr double SCREEN_KEEP = 1.0 - 0x1p-16;
+
+// one default direction of one candidate, exactly (R8 op order)
+__device__ __forceinline__ void eval_candidate_dl(long long Pg, long long Ph, long long Mg, long long Mh, long long Tg,
+                                                  long long Th, int sg, int sh, double e, const EvalParams &p,
+                                                  long long bin_global, int dli, FeatBest &best) {
+    const bool dl = dli == 0;
+    const long long Lg = Pg + (dl ? Mg : 0), Lh = Ph + (dl ? Mh : 0);
+    const double GL = fixed_to_double(Lg, sg), HL = fixed_to_double(Lh, sh);
+    const double GR = fixed_to_double(Tg - Lg, sg), HR = fixed_to_double(Th - Lh, sh);
+    if (!(HL >= p.mcw && HR >= p.mcw && dadd(HL, p.lambda) > 0.0 && dadd(HR, p.lambda) > 0.0)) return;
+    double aa = dmul(GL, GL);
+    aa = ddiv(aa, dadd(HL, p.lambda));
+    double cc = dmul(GR, GR);
+    cc = ddiv(cc, dadd(HR, p.lambda));
+    double d = dadd(aa, cc);
+    d = dsub(d, e);
+    d = dmul(0.5, d);
+    const double gain = dsub(d, p.gamma);
+    const long long idx = bin_global * 2 + dli;
+    if (better(gain, idx, best.gain, best.idx)) {
+        best.gain = gain;
+        best.idx = idx;
+        best.Lg = Lg;
+        best.Lh = Lh;
+    }
+}
+
 // Best candidate of feature f of one node, computed by one warp (valid in every lane).
 // Register-blocked: lane owns KB consecutive bins of each 32*KB-bin chunk, so all histogram
 // loads of a chunk are in flight together; the prefix is a per-lane serial scan plus one warp
@@ -1672,13 +1725,46 @@ __device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long
             Mg = Tg - __shfl_sync(0xffffffffu, xg, 31);
             Mh = Th - __shfl_sync(0xffffffffu, xh, 31);
         }
-        long long Pg = cg + xg - lg, Ph = ch + xh - lh;
+        const long long Pg0 = cg + xg - lg, Ph0 = ch + xh - lh;
+        if (p.screen) {
+            const int n_dl = (Mg == 0 && Mh == 0) ? 1 : 2;  // (see eval_candidate)
+            double sc[KB][2];
+            double smax = -1.0;
+            long long Pg = Pg0, Ph = Ph0;
 #pragma unroll
-        for (int i = 0; i < KB; ++i) {
-            const int b = c + lane * KB + i;
-            Pg += vg[i];
-            Ph += vh[i];
-            if (b < nbf) eval_candidate(Pg, Ph, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), best);
+            for (int i = 0; i < KB; ++i) {
+                const int b = c + lane * KB + i;
+                Pg += vg[i];
+                Ph += vh[i];
+#pragma unroll
+                for (int dli = 0; dli < 2; ++dli) {
+                    sc[i][dli] = (b < nbf && dli < n_dl) ? screen_score(Pg, Ph, Mg, Mh, Tg, Th, sg, sh, p, dli) : -1.0;
+                    smax = fmax(smax, sc[i][dli]);
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+            const double thr = smax * SCREEN_KEEP;
+            Pg = Pg0;
+            Ph = Ph0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+                const int b = c + lane * KB + i;
+                Pg += vg[i];
+                Ph += vh[i];
+#pragma unroll
+                for (int dli = 0; dli < 2; ++dli)
+                    if (sc[i][dli] >= 0.0 && sc[i][dli] >= thr)
+                        eval_candidate_dl(Pg, Ph, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), dli, best);
+            }
+        } else {
+            long long Pg = Pg0, Ph = Ph0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+                const int b = c + lane * KB + i;
+                Pg += vg[i];
+                Ph += vh[i];
+                if (b < nbf) eval_candidate(Pg, Ph, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), best);
+            }
         }
         cg += __shfl_sync(0xffffffffu, xg, 31);
         ch += __shfl_sync(0xffffffffu, xh, 31);
@@ -1798,7 +1884,30 @@ __device__ FeatBest eval_feature_blk(const NodeHist &src, int b0, int nbf, long 
             Mg = Tg - tg;
             Mh = Th - th;
         }
-        if (b < nbf) eval_candidate(cg + vg, ch + vh, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), best);
+        if (p.screen) {
+            __shared__ double s_max[EWPB];
+            const int n_dl = (Mg == 0 && Mh == 0) ? 1 : 2;
+            double sc[2];
+            double smax = -1.0;
+#pragma unroll
+            for (int dli = 0; dli < 2; ++dli) {
+                sc[dli] = (b < nbf && dli < n_dl) ? screen_score(cg + vg, ch + vh, Mg, Mh, Tg, Th, sg, sh, p, dli) : -1.0;
+                smax = fmax(smax, sc[dli]);
+            }
+            for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+            if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = smax;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < EWPB; ++i) smax = fmax(smax, s_max[i]);
+            __syncthreads();
+            const double thr = smax * SCREEN_KEEP;
+#pragma unroll
+            for (int dli = 0; dli < 2; ++dli)
+                if (sc[dli] >= 0.0 && sc[dli] >= thr)
+                    eval_candidate_dl(cg + vg, ch + vh, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), dli, best);
+        } else if (b < nbf) {
+            eval_candidate(cg + vg, ch + vh, Mg, Mh, Tg, Th, sg, sh, e, p, (long long)(b0 + b), best);
+        }
         cg += tg;
         ch += th;
     }
@@ -2601,14 +2710,16 @@ static int check_qm(const gbm_qmatrix *qm) {
     return GBM_OK;
 }
 
-static EvalArgs eval_args_base(const gbm_qmatrix *q, const int32_t *scale_d, const gbm_params *prm) {
+static EvalArgs eval_args_base(const gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *scale_d,
+                               const gbm_params *prm) {
     EvalArgs a = {};
     a.F = q->n_features;
     a.TB = q->cut_ptr_h[q->n_features];
     a.cut_ptr = q->cut_ptr_d;
     a.cut_values = q->cut_values_d;
     a.scale = scale_d;
-    a.p = EvalParams{prm->eta, prm->lambda, prm->gamma, prm->min_child_weight, prm->max_depth};
+    a.p = EvalParams{prm->eta, prm->lambda, prm->gamma, prm->min_child_weight, prm->max_depth,
+                     ctx->eval_screen ? 1 : 0};
     return a;
 }
 
@@ -2746,7 +2857,7 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
         ProfScope ps(ctx, PC_ALLREDUCE, s, (double)(hist_unit + 2) * 8);
         GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
     }
-    EvalArgs ea = eval_args_base(q, scale_d, prm);
+    EvalArgs ea = eval_args_base(ctx, q, scale_d, prm);
     ea.nodes = nodes;
     ea.hist_root = hist_root;
     ea.hist_build = hist_build;
@@ -2956,7 +3067,7 @@ int gbm_evaluate_splits(gbm_ctx *ctx, const gbm_qmatrix *q, const int64_t *hist_
                 GBM_E_ARG, "gbm_evaluate_splits: bad arguments");
     if (n_nodes == 0) return GBM_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    EvalArgs a = eval_args_base(q, scale_d, prm);
+    EvalArgs a = eval_args_base(ctx, q, scale_d, prm);
     a.n_nodes = n_nodes;
     a.hist_direct = reinterpret_cast<const long long *>(hist_d);
     a.totals_direct = reinterpret_cast<const long long *>(totals_d);
@@ -3178,7 +3289,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
         GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
     }
     GBM_CUDA(cudaMemsetAsync(done, 0, (1 + (size_t)max_par) * sizeof(unsigned), s));
-    EvalArgs ea = eval_args_base(q, scale_d, prm);
+    EvalArgs ea = eval_args_base(ctx, q, scale_d, prm);
     ea.nodes = nodes;
     ea.hist_root = hist_root;
     ea.hist_build = hist_build;

@@ -212,6 +212,48 @@ def test_evaluate_parity(ctx, G, seed, eval_warp):
     ctx.set_option(ctx.EVAL_WARP, 0)
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("seed", range(6))
+def test_evaluate_screen_is_exact_on_near_ties(ctx, G, seed, kernel):
+    """The approximate screen (GBM_OPT_EVAL_SCREEN) never changes a result: histograms built to
+    have many exact ties and near ties (duplicated features, +-1 perturbations, coarse counts),
+    with and without missing mass; screened == unscreened == oracle, bit for bit."""
+    rng = np.random.default_rng(500 + seed)
+    F, nb = 12, 64
+    cut_ptr = np.arange(F + 1, dtype=np.int32) * nb
+    base = rng.integers(-40, 41, (nb, 2)) * (1 << 10)
+    base[:, 1] = np.abs(base[:, 1]) + (1 << 12)
+    nodes = []
+    for j in range(5):
+        H = np.concatenate([base for _ in range(F)]).astype(np.int64)
+        for f in range(F):  # near ties: tiny perturbations of a few bins
+            k = rng.integers(0, nb, 3)
+            H[f * nb + k, 0] += rng.integers(-1, 2, 3)
+        T = H.sum(0)
+        if j % 2:  # missing mass
+            T = T + np.array([rng.integers(-5000, 5000), rng.integers(0, 5000)])
+        nodes.append((H, T))
+    hist, tot = dev(np.stack([h for h, _ in nodes])), dev(np.stack([t for _, t in nodes]))
+    qm = G.QMatrix(torch.zeros(4, dtype=torch.int32, device="cuda"), 1, F, 8, 32, 256,
+                   torch.zeros(F * nb, dtype=torch.float32, device="cuda"), dev(cut_ptr), cut_ptr)
+    sc = dev(np.array([20, 20], np.int32))
+    ctx.set_option(ctx.EVAL_WARP, kernel)
+    outs = []
+    for screen in (0, 1):
+        ctx.set_option(ctx.EVAL_SCREEN, screen)
+        o = ctx.evaluate_splits(qm, hist, tot, sc, reg_lambda=1.0, gamma=0.0, min_child_weight=0.0)
+        outs.append({k: v.cpu().numpy() for k, v in o.items()})
+    ctx.set_option(ctx.EVAL_SCREEN, 0)
+    ctx.set_option(ctx.EVAL_WARP, 0)
+    for k in outs[0]:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k], err_msg=k)
+    for j, (H, T) in enumerate(nodes):
+        r = O.evaluate_split(H, cut_ptr, T[0], T[1], [20, 20], 1.0, 0.0, 0.0)
+        assert outs[1]["gain"][j] == r["gain"] and bool(outs[1]["split"][j]) == r["split"]
+        if r["feature"] >= 0:
+            assert (outs[1]["feature"][j], outs[1]["bin"][j]) == (r["feature"], r["bin"])
+
+
 # ------------------------------------------------------------------ a5: RepartitionInstances
 @pytest.mark.parametrize("n_sel", [0, 1, 31, 1024, 1025, 70_001])
 def test_repartition_parity(ctx, G, n_sel):
