@@ -88,9 +88,9 @@ def ncu_traffic(config):
     p = os.path.join(ROOT, "profiles", f"ncu_hist_{config}.json")
     try:
         d = json.load(open(p))
-        return d.get("dram_bytes_per_launch"), d.get("source")
+        return d.get("dram_bytes_per_launch"), d.get("source"), d.get("l1tex_pct_of_peak_active_mean")
     except Exception:
-        return None, None
+        return None, None, None
 
 
 class Clocks:
@@ -257,7 +257,7 @@ def run_ours(a, world, rank, local):
     hist_launches = (prof["hist_root"]["launches"] + prof["hist_level"]["launches"]) // ms_div
     peak, peak_src = measured_peak()
     achieved = hist_bytes / (hist_ms * 1e-3) / 1e9 if hist_ms > 0 else 0.0
-    traffic, traffic_src = ncu_traffic(a.config)
+    traffic, traffic_src, l1_pct = ncu_traffic(a.config)
     roofline = {"bound": "hbm", "kernel": "hist_kernel (root + level launches)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -266,7 +266,12 @@ def run_ours(a, world, rank, local):
                 "peak_source": peak_src, "traffic_source": traffic_src,
                 "timing": ("CUDA-event nodes inside the replayed graph (last replay)" if use_graph
                            else "CUDA events around every launch of the timed region"),
-                "share_of_step": round(hist_ms / (ms_total / a.steps), 4) if ms_total else None}
+                "share_of_step": round(hist_ms / (ms_total / a.steps), 4) if ms_total else None,
+                # what actually binds it: shared-memory atomics on the L1/TEX data
+                # pipe -- the committed ncu capture's L1/TEX utilisation of these launches
+                "binding_unit": {"unit": "L1/TEX data pipe (shared-memory ATOMS)",
+                                 "pct_of_peak": round(l1_pct, 1) if l1_pct else None,
+                                 "source": traffic_src}}
     # ---- per-stage breakdown: a separate eager window with every launch timed
     ctx.profile(True)
     n_st = min(20, a.steps)

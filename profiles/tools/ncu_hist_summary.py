@@ -20,8 +20,15 @@ def tob(s):
     v,u=s.split(' ',1); v=float(v.replace(',',''))
     return v*{'byte':1,'Kbyte':1e3,'Mbyte':1e6,'Gbyte':1e9}[u.strip()]
 tr=[tob(d['rd'])+tob(d['wr']) for d in out]
+def tof(x):
+    try: return float(x.split(' ')[0].replace(',',''))
+    except Exception: return None
+l1=[tof(d['l1']) for d in out]
 summary={"source":f"ncu --set full (profiles/{tag}_ncu_hist_summary.md): bench.py --steps 3 --warmup 3, Higgs 11M x 28, one round = root + 5 level launches",
-         "dram_bytes_per_launch": sum(tr)/len(tr), "launches": [ {"kernel":d['kernel'], "dram_bytes": t} for d,t in zip(out,tr)]}
+         "dram_bytes_per_launch": sum(tr)/len(tr),
+         "l1tex_pct_of_peak_active_mean": sum(v for v in l1 if v is not None)/max(1,len([v for v in l1 if v is not None])),
+         "launches": [ {"kernel":d['kernel'], "dram_bytes": t, "l1tex_pct_active": l, "smem_atom_wavefronts": tof(d['aw']),
+                        "smem_atom_bank_conflicts": tof(d['ac'])} for d,t,l in zip(out,tr,l1)]}
 json.dump(summary, open('profiles/ncu_hist_higgs.json','w'), indent=1)
 lines=[f"# {tag} ncu --set full: histogram kernels, one boosting round (Higgs-shaped 11M x 28, depth 6)","",
 "Capture: `ncu --set full --clock-control none --import-source on -k regex:\"hist_range|part_hist\" -s 6 -c 6`",
