@@ -576,3 +576,24 @@ def test_graph_captured_rounds_with_communicator(G, grow):
         np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
     del graph
     c.close()
+
+
+def test_build_tree_argument_errors(ctx, G):
+    """gbm_build_tree's documented argument errors (GBM_E_ARG = -1): bad growth policy, leaf
+    budget out of range, loss-guided tree without left_child, depth-wise depth > 16."""
+    X, y = W.generate("tiny")
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=16, objective="reg:squarederror", max_depth=3)
+    q, sc = ctx.gradients("reg:squarederror", gb.margin, gb.y)
+    cases = [dict(grow_policy=7, max_depth=3), dict(grow_policy="lossguide", max_leaves=0, max_depth=3),
+             dict(grow_policy="lossguide", max_leaves=70000, max_depth=3), dict(max_depth=17)]
+    for kw in cases:
+        with pytest.raises(G.GbmError) as e:
+            ctx.build_tree(gb.qm, q, sc, objective="reg:squarederror", **kw)
+        assert e.value.code == -1, kw
+    t = G.Tree(3, "cuda", 4)
+    t.arrays["left_child"] = torch.empty(0, dtype=torch.int32, device="cuda")  # null pointer
+    with pytest.raises(G.GbmError) as e:
+        ctx.build_tree(gb.qm, q, sc, objective="reg:squarederror", max_depth=3,
+                       grow_policy="lossguide", max_leaves=4, tree=t)
+    assert e.value.code == -1
+    ctx.check()
