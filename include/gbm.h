@@ -109,9 +109,13 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   candidates that pass an approximate screen proven never to drop the exact argmax or a tie
  *   with it (tree.cu, screen_score); 0 (default: measured faster, the evaluation is bound by
  *   memory and latency, not by the divisions) evaluates every candidate exactly.  Results are
- *   identical either way. */
+ *   identical either way.
+ * GBM_OPT_SEGMENT_HIST: with several shared-memory feature groups (wide data): 2 = each level
+ *   is partitioned once and the built children's row segments are histogrammed group by group;
+ *   1 = the fused kernel repeats the partition in every group; 0 (default) = 2 for symbols
+ *   wider or narrower than a byte, else 1 (measured). */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
-       GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7 };
+       GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

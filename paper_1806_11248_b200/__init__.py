@@ -301,6 +301,7 @@ class Context:
     EVAL_WARP = 5
     LEAF_WALK = 6
     EVAL_SCREEN = 7
+    SEGMENT_HIST = 8
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

@@ -274,6 +274,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->eval_warp = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_SEGMENT_HIST) {
+        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_SEGMENT_HIST: 0 auto, 1 off, 2 on");
+        ctx->seg_hist = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_EVAL_SCREEN) {
         ctx->eval_screen = value != 0;
         return GBM_OK;

@@ -516,6 +516,7 @@ struct FusedArgs {
     unsigned long long *rows_ctr;  // profiling: algorithmic BITS moved (see below)
     int bits_parent_row;           // split symbol + ridx read, per scanned parent row
     int bits_built_row;            // packed row + qpair, per row of the built child
+    int no_hist;                   // partition only (flags + left counts): hist_seg_kernel follows
 };
 
 // Warp-independent: each warp owns 64 rows of every tile of the item (no block barrier
@@ -561,8 +562,10 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
         }
         const Group grp = a.groups[g];
         SmemHist h{smem, grp.bin_hi - grp.bin_lo, a.hstride};
-        smem_zero<WIDE>(h);
-        load_group(qm, grp, a.cut_ptr, s_off);
+        if (!a.no_hist) {
+            smem_zero<WIDE>(h);
+            load_group(qm, grp, a.cut_ptr, s_off);
+        }
         __syncthreads();
         // lane -> (row slot, unit) of the group; units per row Ug <= 32 (plan_hist)
         const int Ug = grp.u_hi - grp.u_lo;
@@ -592,6 +595,7 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
         const long long sw = qm.stride >> 5;
         const uint32_t mask = (1u << qm.bits) - 1u;
         unsigned long long bits_acc = 0;
+        const bool no_hist = a.no_hist != 0;
         for (int t = t0; t < t1; ++t) {
             const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
             // (A) partition flags for the warp's 128 rows (4 per lane)
@@ -628,10 +632,11 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
                 if (a.rows_ctr) {
                     const long long nv = max(0ll, min((long long)WROWS, seg_end - base));
                     bits_acc += (unsigned long long)nv * a.bits_parent_row +
-                                (unsigned long long)nbuild * a.bits_built_row;
+                                (a.no_hist ? 0ull : (unsigned long long)nbuild * a.bits_built_row);
                 }
             }
             __syncwarp();
+            if (no_hist) continue;  // partition only
             // (B) histogram of the listed rows
             if (BYTE && agg) {  // warp-uniform loop (aggregated slots use warp intrinsics)
                 for (int rb = 0; rb < nbuild; rb += 4 * rpp) {
@@ -722,6 +727,60 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
             __syncwarp();
         }
         if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
+        __syncthreads();
+        if (!no_hist) smem_flush<WIDE>(h, a.hist + ((long long)j * a.TB + grp.bin_lo) * 2);
+        __syncthreads();
+    }
+}
+
+// ============================================================== segment histograms
+// With several shared-memory feature groups (wide data: Epsilon 63, Bosch ~40, YearMSD 3) the
+// fused kernel would repeat the partition of every parent row once per group.  Instead the level
+// is partitioned once (fused kernel with no_hist), scanned and scattered, and the built
+// children's contiguous entry segments are then histogrammed group by group.
+struct SegArgs {
+    QM qm;
+    const NodeDev *nodes;
+    int first, n_par;
+    const void *ridx;         // the level's scattered entries (EntryOf<CARRY>)
+    const int2 *qpair;
+    const int *seg_base;      // [n_par + 1] first chunk of each parent's built child
+    const int *n_items;       // chunks x groups
+    int chunk, n_groups;
+    const Group *groups;
+    const int32_t *cut_ptr;
+    unsigned long long *hist;  // [n_par][TB][2]
+    long long TB;
+    int hstride;
+    unsigned long long *rows_ctr;
+};
+
+template <bool WIDE, bool BYTE, bool SENT, bool CARRY>
+__global__ void __launch_bounds__(H_THREADS, GBM_HR_MINB) hist_seg_kernel(SegArgs a) {
+    using E = typename EntryOf<CARRY>::T;
+    extern __shared__ int smem[];
+    __shared__ int s_off[2049];
+    const QM &qm = a.qm;
+    const E *rin = static_cast<const E *>(a.ridx);
+    const int n_items = *a.n_items;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int ch = it / a.n_groups, g = it - ch * a.n_groups;
+        const int j = find_parent(a.seg_base, a.n_par, ch);
+        const int k = a.first + j;
+        const NodeDev cd = a.nodes[a.nodes[k].build_left ? 2 * k + 1 : 2 * k + 2];
+        const long long start = cd.start + (long long)(ch - a.seg_base[j]) * a.chunk;
+        const int len = (int)min((long long)a.chunk, cd.start + cd.count - start);
+        const Group grp = a.groups[g];
+        SmemHist h{smem, grp.bin_hi - grp.bin_lo, a.hstride};
+        if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)len);
+        smem_zero<WIDE>(h);
+        load_group(qm, grp, a.cut_ptr, s_off);
+        __syncthreads();
+        ByteLane L = BYTE ? byte_lane(qm, grp, s_off, h.nb) : ByteLane{};
+        long long tg = 0, th = 0;
+        const E *rp = rin + start;
+        accumulate<WIDE, BYTE, SENT>(qm, grp, s_off, h, a.qpair, [&](int r) { return row_of(rp[r]); }, len, L,
+                                     &tg, &th, false);
         __syncthreads();
         smem_flush<WIDE>(h, a.hist + ((long long)j * a.TB + grp.bin_lo) * 2);
         __syncthreads();
@@ -1474,6 +1533,33 @@ __global__ void __launch_bounds__(1024) part_scan_kernel(NodeDev *__restrict__ n
         Lc->count = carry;
         Rc->start = nd.start + carry;
         Rc->count = nd.count - carry;
+    }
+}
+
+__global__ void __launch_bounds__(1024) seg_plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
+                                                        int chunk, int n_groups, int *__restrict__ seg_base,
+                                                        int *__restrict__ n_items) {
+    __shared__ long long sm32[32];
+    long long carry = 0;
+    for (int c = 0; c < n_par; c += blockDim.x) {
+        const int j = c + threadIdx.x;
+        long long nc = 0;
+        if (j < n_par) {
+            const int k = first + j;
+            const NodeDev nd = nodes[k];
+            if (nd.state == GBM_NODE_SPLIT) {
+                const long long cnt = nodes[nd.build_left ? 2 * k + 1 : 2 * k + 2].count;
+                nc = (cnt + chunk - 1) / chunk;
+            }
+        }
+        long long tot;
+        const long long ex = carry + block_exscan(nc, &tot, sm32);
+        if (j < n_par) seg_base[j] = (int)ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        seg_base[n_par] = (int)carry;
+        n_items[0] = (int)carry * n_groups;
     }
 }
 
@@ -2442,6 +2528,11 @@ static int setup_kernels(gbm_ctx *ctx, HistPlan &hp) {
     if constexpr (!W)
         GBM_CUDA(cudaFuncSetAttribute(part_hist_kernel<W, B, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       hp.smem_bytes));
+    GBM_CUDA(cudaFuncSetAttribute(hist_seg_kernel<W, B, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  hp.smem_bytes));
+    if constexpr (!W)
+        GBM_CUDA(cudaFuncSetAttribute(hist_seg_kernel<W, B, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      hp.smem_bytes));
     int o1 = 0, o2 = 0;
     GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_range_kernel<W, B, S>, H_THREADS, hp.smem_bytes));
     if constexpr (!W)
@@ -2622,6 +2713,18 @@ static int launch_fused(gbm_ctx *ctx, const HistPlan &hp, FusedArgs a, cudaStrea
         else part_hist_kernel<W, B, S, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
     } else {
         part_hist_kernel<W, B, S, false><<<hp.blocks_fused, H_THREADS, hp.smem_bytes, s>>>(a);
+    }
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+
+template <bool W, bool B, bool S>
+static int launch_seg(gbm_ctx *ctx, const HistPlan &hp, SegArgs a, cudaStream_t s, bool carry) {
+    if constexpr (!W) {
+        if (carry) hist_seg_kernel<W, B, S, true><<<hp.blocks_range, H_THREADS, hp.smem_bytes, s>>>(a);
+        else hist_seg_kernel<W, B, S, false><<<hp.blocks_range, H_THREADS, hp.smem_bytes, s>>>(a);
+    } else {
+        hist_seg_kernel<W, B, S, false><<<hp.blocks_range, H_THREADS, hp.smem_bytes, s>>>(a);
     }
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
@@ -3214,6 +3317,7 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     need += 2 * slots * hist_unit * 8 + 512;                          // level hists
     need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 512;
     need += (1 + (size_t)max_par) * sizeof(unsigned) + 256;           // eval counters
+    need += ((size_t)max_par + 1) * 4 + 8 + 512;                      // segment plan
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
@@ -3233,6 +3337,8 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     long long *hist_lvl[2] = {A.take<long long>(slots * hist_unit), A.take<long long>(slots * hist_unit)};
     FeatBest *fb = A.take<FeatBest>((size_t)std::max(1, 1 << std::max(0, D - 1)) * F);
     unsigned *done = A.take<unsigned>(1 + (size_t)max_par);  // [0] nodes completed, [1..] warps per node
+    int *seg_base = A.take<int>((size_t)max_par + 1);
+    int *seg_items = A.take<int>(2);
 
     GBM_TRY(upload_groups(ctx, hp, groups, cgroups, A, s));
     const TreeDev t = tree_dev(tree);
@@ -3296,11 +3402,18 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     ea.fb = fb;
     // tiles per fused work item: about 4 items per resident block at the widest level (items are
     // claimed dynamically; measured on Higgs: 4 tiles 0.79 ms, 8 tiles 0.84, 16 tiles 0.99 / round)
+    // several feature groups: partition each level once, then histogram the built segments per
+    // group (hist_seg_kernel) instead of re-partitioning every parent row in every group.
+    // Measured: a gain for the generic (non-byte) symbol path (Bosch 4.00 vs 4.20 ms/round), not
+    // for byte symbols (Epsilon 4.71 vs 4.57, YearMSD 0.540 vs 0.533), so auto = generic only.
+    const bool seg_mode = !hp.col && G > 1 &&
+                          (ctx->seg_hist == 2 || (ctx->seg_hist == 0 && !hp.byte_path));
+    const int Gf = seg_mode ? 1 : G;  // groups of the fused launch
     const long long tiles_all = (n + PT - 1) / PT;
     const long long target = 4ll * hp.blocks_fused;
     const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
-        1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
-    ea.plan_groups = G;
+        1, std::min<long long>(RUN_MAX, (tiles_all * Gf + target - 1) / target));
+    ea.plan_groups = Gf;
     ea.plan_run = run_tiles;
     ea.tile_base = tile_base_b[1];  // the root's evaluation plans level 1
     ea.run_base = run_base_b[1];
@@ -3323,7 +3436,8 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
     FusedArgs fa = {};
     fa.qm = qm;
     fa.nodes = nodes;
-    fa.n_groups = G;
+    fa.n_groups = Gf;
+    fa.no_hist = seg_mode ? 1 : 0;
     fa.run_tiles = run_tiles;
     fa.flags = flags;
     fa.tile_left = tile_left;
@@ -3416,9 +3530,10 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             }
         }
         // side stream: scan + scatter of this level, concurrent with the allreduce and (after the
-        // scan: the plan of level l+1 needs the children's counts) the evaluation
-        GBM_TRY(fork_side(ctx, s));
-        cudaStream_t ss = ctx->side;
+        // scan: the plan of level l+1 needs the children's counts) the evaluation.  In segment
+        // mode the histograms need the scattered entries: everything stays on s.
+        if (!seg_mode) GBM_TRY(fork_side(ctx, s));
+        cudaStream_t ss = seg_mode ? s : ctx->side;
         {
             ProfScope ps(ctx, PC_PART_SCAN, ss);
             part_scan_kernel<<<n_par, 1024, 0, ss>>>(nodes, first, tile_base, tile_left, tile_off, nullptr);
@@ -3438,6 +3553,31 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
                     reinterpret_cast<uint32_t *>(rout), nullptr, rc);
         }
         GBM_CUDA(cudaGetLastError());
+        if (seg_mode) {  // the built children's segments, group by group
+            const long long half = (n / 2 + 2ll * hp.blocks_range - 1) / (2ll * hp.blocks_range);
+            const int seg_chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, half * G));
+            seg_plan_kernel<<<1, 1024, 0, s>>>(nodes, first, n_par, seg_chunk, G, seg_base, seg_items);
+            SegArgs sa = {};
+            sa.qm = qm;
+            sa.nodes = nodes;
+            sa.first = first;
+            sa.n_par = n_par;
+            sa.ridx = rout;
+            sa.qpair = reinterpret_cast<const int2 *>(qpair_d);
+            sa.seg_base = seg_base;
+            sa.n_items = seg_items;
+            sa.chunk = seg_chunk;
+            sa.n_groups = G;
+            sa.groups = groups;
+            sa.cut_ptr = q->cut_ptr_d;
+            sa.hist = reinterpret_cast<unsigned long long *>(hist_build);
+            sa.TB = std::max<long long>(TB, 1);
+            sa.hstride = hp.hstride;
+            int slot;
+            sa.rows_ctr = prof_rows_slot(ctx, &slot);
+            ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, row_bytes + 8.0 + esz);
+            GBM_TRY(GBM_DISPATCH(hp, launch_seg, ctx, hp, sa, s, hp.carry));
+        }
         {  // AllReduceHistograms
             ProfScope ps(ctx, PC_ALLREDUCE, s, (double)n_par * hist_unit * 8);
             GBM_TRY(allreduce_i64(ctx, hist_build, (size_t)n_par * hist_unit, s));
@@ -3452,12 +3592,12 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             ea.tile_base = tile_base_b[(l + 1) & 1];
             ea.run_base = run_base_b[(l + 1) & 1];
             ea.n_items = n_items_b[(l + 1) & 1];
-            GBM_CUDA(cudaStreamWaitEvent(s, ctx->ev_scan, 0));
+            if (!seg_mode) GBM_CUDA(cudaStreamWaitEvent(s, ctx->ev_scan, 0));
             {
                 ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
                 GBM_TRY(launch_eval_tree(ctx, ea, t, s));
             }
-            GBM_TRY(wait_on(s, ctx->ev_join, ctx->side));  // join: the next level reads the scatter
+            if (!seg_mode) GBM_TRY(wait_on(s, ctx->ev_join, ctx->side));  // join: the next level reads the scatter
         }
     }
     return GBM_OK;

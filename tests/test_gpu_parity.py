@@ -597,3 +597,24 @@ def test_build_tree_argument_errors(ctx, G):
                        grow_policy="lossguide", max_leaves=4, tree=t)
     assert e.value.code == -1
     ctx.check()
+
+
+@pytest.mark.parametrize("seg", [1, 2])
+@pytest.mark.parametrize("cfg,n,missing,carry", [("yearmsd", 30_000, 0.0, 0), ("bosch", 12_000, 0.0, 1),
+                                                 ("epsilon", 6_000, 0.02, 0)])
+def test_segment_histogram_modes(ctx, G, cfg, n, missing, carry, seg):
+    """Wide data (several shared-memory feature groups): levels partitioned once + per-group
+    segment histograms (GBM_OPT_SEGMENT_HIST 2) and the per-group fused kernel (1)."""
+    ctx.set_option(ctx.SEGMENT_HIST, seg)
+    ctx.set_option(ctx.CARRY_GRADIENTS, carry)
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective,
+                   max_depth=c.max_depth, base_margin=ob.base_margin)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.SEGMENT_HIST, 0)
+    ctx.set_option(ctx.CARRY_GRADIENTS, 0)
