@@ -88,6 +88,9 @@ typedef struct {
 } gbm_prof_entry;
 GBM_API int gbm_profile_enable(gbm_ctx *ctx, int enable);
 GBM_API int gbm_profile_read(gbm_ctx *ctx, gbm_prof_entry *out, int32_t cap, int32_t *n_out);
+/* Zero the device counters of algorithmic bytes but keep the timing records (e.g. of the event
+ * nodes of a captured CUDA graph): start a measurement window after warm-up replays. */
+GBM_API int gbm_profile_zero_rows(gbm_ctx *ctx);
 GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
 
 /* Tuning options (do not change results, only which kernels compute them).

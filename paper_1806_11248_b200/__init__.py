@@ -71,6 +71,7 @@ EXPORTS = {
     "gbm_profile_read": (C.c_int, [C.c_void_p, C.POINTER(_ProfEntry), C.c_int32,
                                    C.POINTER(C.c_int32)]),
     "gbm_launch_count": (C.c_int64, [C.c_void_p]),
+    "gbm_profile_zero_rows": (C.c_int, [C.c_void_p]),
     "gbm_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     "gbm_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "gbm_comm_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
@@ -284,6 +285,10 @@ class Context:
                 v |= 1 << self.PROFILE_CATEGORIES.index(name)
             assert v > 1, "pick at least one category other than grad_max alone"
         _call("gbm_profile_enable", self.h, v)
+
+    def profile_zero_rows(self):
+        """Zero the algorithmic-byte counters, keep the timing records (graph event nodes)."""
+        _call("gbm_profile_zero_rows", self.h)
 
     def profile_read(self) -> dict:
         """Per-kernel {launches, ms, bytes, rows} since the last read (synchronises)."""

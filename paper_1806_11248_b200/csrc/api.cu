@@ -250,6 +250,14 @@ int gbm_profile_read(gbm_ctx *ctx, gbm_prof_entry *out, int32_t cap, int32_t *n_
     return GBM_OK;
 }
 
+int gbm_profile_zero_rows(gbm_ctx *ctx) {
+    GBM_TRY(ctx_enter(ctx));
+    Prof &p = ctx->prof;
+    GBM_CUDA(cudaDeviceSynchronize());
+    if (p.rows_dev) GBM_CUDA(cudaMemset(p.rows_dev, 0, sizeof(unsigned long long) * p.rows_cap));
+    return GBM_OK;
+}
+
 int64_t gbm_launch_count(gbm_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
 int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
