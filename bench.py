@@ -287,7 +287,8 @@ def run_ours(a, world, rank, local):
     hist_launches = (prof["hist_root"]["launches"] + prof["hist_level"]["launches"]) // ms_div
     peak, peak_src = measured_peak()
     achieved = hist_bytes / (hist_ms * 1e-3) / 1e9 if hist_ms > 0 else 0.0
-    traffic, traffic_src, l1_pct = ncu_traffic(a.config)
+    # the committed ncu capture is of the depth-wise bench command: attach it only to that line
+    traffic, traffic_src, l1_pct = ncu_traffic(a.config) if a.grow_policy == "depthwise" else (None, None, None)
     roofline = {"bound": "hbm", "kernel": "hist_kernel (root + level launches)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
