@@ -1101,7 +1101,10 @@ __device__ __forceinline__ void cs_batch_any(const QM &qm, CsWarp &st, int *hs, 
     cs_batch(qm, st, hs, u_lo, Wg, Fg, R, copy, nrows, rowf, qf);
 }
 
-template <bool IDENT>
+// R1: every group has more than 16 features (one row per warp instruction, compile-time row
+// pitch); a separate instantiation so the other path's code generation is not affected
+// (Airline, 13 features: root 2.69 vs 3.13 ms when the R1 variants are not in the same kernel).
+template <bool IDENT, bool R1>
 __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArgs a) {
     extern __shared__ int smem[];
     CsWarp *stage = reinterpret_cast<CsWarp *>(smem + 2 * COLB_STRIDE);
@@ -1126,8 +1129,10 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArg
                 const long long r = b0 + i;
                 return IDENT ? (uint32_t)r : __ldg(a.ridx + r);
             };
-            cs_batch_any(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, nrows, rowf,
-                         [&](int i) { return __ldg(a.qpair + rowf(i)); });
+            if (R1) cs_batch_any(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, nrows, rowf,
+                                 [&](int i) { return __ldg(a.qpair + rowf(i)); });
+            else cs_batch(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, nrows, rowf,
+                          [&](int i) { return __ldg(a.qpair + rowf(i)); });
         }
         __syncthreads();
         col_flush<false>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist);
@@ -2561,6 +2566,7 @@ struct HistPlan {
     bool carry = false;   // level entries carry the gradient pairs (grad_bits <= 15)
     bool col = false;     // bank-column kernels (every feature has <= rows bins)
     bool staged = false;  // staged bank-column kernels (layout 3: byte symbols, narrow)
+    bool cs_r1 = false;   // staged: every group has > 16 features (the one-row-per-instruction kernel)
     std::vector<ColGroup> cgroups;
     int cstride = 0;      // col: words per channel (rows * 32)
     int hstride = 0;      // words per smem channel
@@ -2651,12 +2657,16 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
                 c.f_hi = std::min(qm.F, 4 * (int)((long long)nu * (g + 1) / ng));
                 hp.cgroups.push_back(c);
             }
-            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
-            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            hp.cs_r1 = true;
+            for (auto &c : hp.cgroups) hp.cs_r1 = hp.cs_r1 && c.f_hi - c.f_lo > 16;
+            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             int o1 = 0, o2 = 0;
-            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_cs_range_kernel<true>, H_THREADS, hp.smem_bytes));
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_cs_range_kernel<true, true>, H_THREADS, hp.smem_bytes));
             GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_cs_kernel<false>, H_THREADS, hp.smem_bytes));
             if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "staged column kernels cannot be resident");
             hp.blocks_range = o1 * ctx->sm_count;
@@ -2784,8 +2794,13 @@ static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int gri
     if (hp.staged) {
         if (ca.totals) sum_qpair_kernel<<<std::min<long long>((ca.n_sel + 255) / 256, 148 * 8), 256, 0, s>>>(
             ca.qpair, ca.n_sel, ca.totals);
-        if (ca.ridx) hist_cs_range_kernel<false><<<grid, H_THREADS, sm, s>>>(ca);
-        else hist_cs_range_kernel<true><<<grid, H_THREADS, sm, s>>>(ca);
+        if (hp.cs_r1) {
+            if (ca.ridx) hist_cs_range_kernel<false, true><<<grid, H_THREADS, sm, s>>>(ca);
+            else hist_cs_range_kernel<true, true><<<grid, H_THREADS, sm, s>>>(ca);
+        } else {
+            if (ca.ridx) hist_cs_range_kernel<false, false><<<grid, H_THREADS, sm, s>>>(ca);
+            else hist_cs_range_kernel<true, false><<<grid, H_THREADS, sm, s>>>(ca);
+        }
         return;
     }
     if (hp.byte_path) {
