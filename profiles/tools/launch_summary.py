@@ -34,7 +34,8 @@ L = [f"# launch list summary (ncu --metrics gpu__time_duration.sum --clock-contr
      "| kernel | launches | us/round | share of round |", "|---|---|---|---|"]
 for k, (c, us) in sorted(per_round.items(), key=lambda x: -x[1][1]):
     L.append(f"| {k} | {c} | {us / rounds:.1f} | {100 * us / rounds / tot:.1f}% |")
-hist = sum(us for k, (c, us) in per_round.items() if "hist_range" in k or "part_hist" in k) / rounds
+hist = sum(us for k, (c, us) in per_round.items()
+           if "hist_range" in k or "hist_cs_range" in k or "part_hist" in k) / rounds
 L += ["", f"Histogram kernels (root + fused level launches): {100 * hist / tot:.1f}% of the round.", "",
       "One-time kernels (cuts, packing, transpose, predict, torch):", "",
       "| kernel | launches | total us |", "|---|---|---|"]

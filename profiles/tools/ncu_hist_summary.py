@@ -31,7 +31,7 @@ summary={"source":f"ncu --set full (profiles/{tag}_ncu_hist_summary.md): bench.p
                         "smem_atom_bank_conflicts": tof(d['ac'])} for d,t,l in zip(out,tr,l1)]}
 json.dump(summary, open('profiles/ncu_hist_higgs.json','w'), indent=1)
 lines=[f"# {tag} ncu --set full: histogram kernels, one boosting round (Higgs-shaped 11M x 28, depth 6)","",
-"Capture: `ncu --set full --clock-control none --import-source on -k regex:\"hist_range|part_hist\" -s 6 -c 6`",
+"Capture: `ncu --set full --clock-control none --import-source on -k regex:\"hist_cs_range|hist_range|part_hist\" -s 6 -c 6`",
 "on `python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline` (round 2: root + levels 1..5).  The .ncu-rep",
 "stays in gpurun_out/ (scratch); this table is the committed summary.","",
 "| launch | kernel | time | DRAM read | DRAM write | DRAM % of peak | L1/TEX % (active) | smem atom wavefronts | of which bank conflicts | warp instr | regs | dyn smem |",
