@@ -1296,7 +1296,7 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
 }
 
 // fused partition + staged bank-column histogram (GBM_OPT_HIST_LAYOUT = 3)
-template <bool CARRY>
+template <bool CARRY, bool R1>
 __global__ void __launch_bounds__(H_THREADS, 2) part_hist_cs_kernel(ColFusedArgs a) {
     using E = typename EntryOf<CARRY>::T;
     extern __shared__ int smem[];
@@ -1375,9 +1375,12 @@ __global__ void __launch_bounds__(H_THREADS, 2) part_hist_cs_kernel(ColFusedArgs
             }
             __syncwarp();
             for (int b0 = 0; b0 < nbuild; b0 += 32)
-                cs_batch_any(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, min(32, nbuild - b0),
-                             [&](int i) { return row_of(wrows[b0 + i]); },
-                             [&](int i) { return entry_q(wrows[b0 + i], a.qpair); });
+                if (R1) cs_batch_any(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, min(32, nbuild - b0),
+                                     [&](int i) { return row_of(wrows[b0 + i]); },
+                                     [&](int i) { return entry_q(wrows[b0 + i], a.qpair); });
+                else cs_batch(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, min(32, nbuild - b0),
+                              [&](int i) { return row_of(wrows[b0 + i]); },
+                              [&](int i) { return entry_q(wrows[b0 + i], a.qpair); });
             __syncwarp();
         }
         if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
@@ -2663,11 +2666,13 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
             GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
-            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
-            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_cs_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             int o1 = 0, o2 = 0;
             GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_cs_range_kernel<true, true>, H_THREADS, hp.smem_bytes));
-            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_cs_kernel<false>, H_THREADS, hp.smem_bytes));
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, part_hist_cs_kernel<false, true>, H_THREADS, hp.smem_bytes));
             if (o1 < 1 || o2 < 1) return fail(GBM_E_ARG, "staged column kernels cannot be resident");
             hp.blocks_range = o1 * ctx->sm_count;
             hp.blocks_fused = o2 * ctx->sm_count;
@@ -2827,8 +2832,13 @@ static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int gri
 static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStream_t s) {
     const int g = hp.blocks_fused, sm = hp.smem_bytes;
     if (hp.staged) {
-        if (hp.carry) part_hist_cs_kernel<true><<<g, H_THREADS, sm, s>>>(ca);
-        else part_hist_cs_kernel<false><<<g, H_THREADS, sm, s>>>(ca);
+        if (hp.cs_r1) {
+            if (hp.carry) part_hist_cs_kernel<true, true><<<g, H_THREADS, sm, s>>>(ca);
+            else part_hist_cs_kernel<false, true><<<g, H_THREADS, sm, s>>>(ca);
+        } else {
+            if (hp.carry) part_hist_cs_kernel<true, false><<<g, H_THREADS, sm, s>>>(ca);
+            else part_hist_cs_kernel<false, false><<<g, H_THREADS, sm, s>>>(ca);
+        }
         return;
     }
     if (hp.wide) {
