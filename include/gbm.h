@@ -95,8 +95,10 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
 
 /* Tuning options (do not change results, only which kernels compute them).
  * GBM_OPT_HIST_LAYOUT: shared-memory histogram layout of BuildPartialHistograms --
- *   0 auto (= compact), 1 compact (random bins, bank conflicts), 2 bank-column (feature per
- *   lane, conflict-free; falls back to compact when the bins do not fit).
+ *   0 auto (staged bank-column root for large matrices, compact levels), 1 compact (random
+ *   bins, bank conflicts), 2 bank-column (feature per lane, conflict-free; falls back to
+ *   compact when the bins do not fit), 3 staged bank-column everywhere, 4 staged root whatever
+ *   the size + compact levels.
  * GBM_OPT_CARRY_GRADIENTS: 0 (default) level passes gather qpair by row; 1 the row-index
  *   entries of every level carry the row's gradient pair (grad_bits <= 15; 8-byte entries).
  * GBM_OPT_RUN_TILES: 2048-row tiles per work item of the fused level kernel (0 = auto).

@@ -263,7 +263,9 @@ int64_t gbm_launch_count(gbm_ctx *ctx) { return ctx ? ctx->launches : 0; }
 int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
     if (!ctx) return fail(GBM_E_ARG, "null context");
     if (option == GBM_OPT_HIST_LAYOUT) {
-        if (value < 0 || value > 3) return fail(GBM_E_ARG, "GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 column, 3 staged column");
+        if (value < 0 || value > 4)
+            return fail(GBM_E_ARG, "GBM_OPT_HIST_LAYOUT: 0 auto, 1 compact, 2 column, 3 staged column, "
+                                   "4 staged root + compact levels");
         ctx->hist_layout = (int)value;
         return GBM_OK;
     }

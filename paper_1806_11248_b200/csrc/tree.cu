@@ -1140,6 +1140,70 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArg
     }
 }
 
+// Generic symbol widths (9..15 bits, e.g. 256 bins + the missing symbol): the same staged
+// bank-column root, lane f extracting its symbol from the staged row's words; missing symbols
+// are skipped (their mass is total - sum, R7).  Groups of <= 32 features at any bit offset.
+constexpr int CSG_WMAX = 16;  // words per staged row: 32 features x 15 bits + misalignment
+struct CsgWarp {
+    uint32_t w[32 * CSG_WMAX + 1];  // + 1: the last symbol's word pair never reads past the end
+    int2 q[32];
+};
+
+template <bool IDENT>
+__global__ void __launch_bounds__(H_THREADS, 2) hist_csg_range_kernel(ColRangeArgs a) {
+    extern __shared__ int smem[];
+    CsgWarp *stage = reinterpret_cast<CsgWarp *>(smem + 2 * COLB_STRIDE);
+    const QM &qm = a.qm;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = H_THREADS / 32;
+    CsgWarp &st = stage[wid];
+    const long long sw = qm.stride >> 5;
+    const uint32_t mask = (1u << qm.bits) - 1u;
+    const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int g = it % a.n_groups;
+        const long long start = (long long)(it / a.n_groups) * a.chunk;
+        const long long end = min(a.n_sel, start + a.chunk);
+        const ColGroup cg = a.groups[g];
+        for (int i = threadIdx.x; i < 2 * COLB_STRIDE; i += H_THREADS) smem[i] = 0;
+        if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)(end - start));
+        __syncthreads();
+        const int Fg = cg.f_hi - cg.f_lo;
+        const long long bit_lo = (long long)cg.f_lo * qm.bits;
+        const int w_lo = (int)(bit_lo >> 5);
+        const int Wg = (int)((((long long)cg.f_hi * qm.bits + 31) >> 5) - w_lo);
+        const int bp = (int)(bit_lo - 32ll * w_lo) + lane * qm.bits;  // my symbol's bit in the staged row
+        const int wi = bp >> 5, off = bp & 31;
+        int *hg = smem + lane, *hh = smem + COLB_STRIDE + lane;
+        for (long long b0 = start + (long long)wid * 32; b0 < end; b0 += NW * 32) {
+            const int nrows = (int)min(32ll, end - b0);
+            auto rowf = [&](int i) -> uint32_t { return IDENT ? (uint32_t)(b0 + i) : __ldg(a.ridx + b0 + i); };
+            st.q[lane] = lane < nrows ? __ldg(a.qpair + rowf(lane)) : make_int2(0, 0);
+            for (int idx = lane; idx < 32 * Wg; idx += 32) {
+                const int i = idx / Wg, w = idx - i * Wg;
+                st.w[idx] = i < nrows ? __ldg(qm.P + (long long)rowf(i) * sw + w_lo + w) : 0u;
+            }
+            __syncwarp();
+            if (lane < Fg) {
+                for (int i = 0; i < nrows; ++i) {
+                    const uint32_t *rw = st.w + i * Wg + wi;
+                    const uint64_t v = (uint64_t)rw[0] | ((uint64_t)rw[1] << 32);
+                    const int sym = (int)((uint32_t)(v >> off) & mask);
+                    if (sym != qm.B) {
+                        const int2 q = st.q[i];
+                        atomicAdd(hg + (sym << 5), q.x);
+                        atomicAdd(hh + (sym << 5), q.y);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        col_flush<false>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist);
+        __syncthreads();
+    }
+}
+
 struct ColFusedArgs {
     QM qm;
     const NodeDev *nodes;
@@ -2799,6 +2863,11 @@ static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int gri
     if (hp.staged) {
         if (ca.totals) sum_qpair_kernel<<<std::min<long long>((ca.n_sel + 255) / 256, 148 * 8), 256, 0, s>>>(
             ca.qpair, ca.n_sel, ca.totals);
+        if (!hp.byte_path) {  // generic symbol widths
+            if (ca.ridx) hist_csg_range_kernel<false><<<grid, H_THREADS, sm, s>>>(ca);
+            else hist_csg_range_kernel<true><<<grid, H_THREADS, sm, s>>>(ca);
+            return;
+        }
         if (hp.cs_r1) {
             if (ca.ridx) hist_cs_range_kernel<false, true><<<grid, H_THREADS, sm, s>>>(ca);
             else hist_cs_range_kernel<true, true><<<grid, H_THREADS, sm, s>>>(ca);
@@ -2960,12 +3029,56 @@ static int upload_groups(gbm_ctx *ctx, const HistPlan &hp, Group *groups, ColGro
 // 1.07, Airline 3.09 vs 3.73; rounds -3 %, -6 %, -3 %), while the level passes gather rows and
 // stay compact (staged levels: Higgs 1.17 vs 0.92 ms).  Auto layout only; byte symbols, narrow
 // fixed point, word-aligned rows, at least 10^8 (row, feature) updates.
+// Staged root for generic symbol widths (9..15 bits): groups of <= 32 features, every feature's
+// present symbols < 256 (one column of COLB_STRIDE rows), word-aligned rows.
+static bool plan_root_staged_generic(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, long long n, HistPlan &hr) {
+    if (q->bits < 9 || q->bits > 15 || qm.stride % 32 != 0) return false;
+    for (int f = 0; f < q->n_features; ++f)
+        if (q->cut_ptr_h[f + 1] - q->cut_ptr_h[f] > 256) return false;
+    hr = HistPlan();
+    hr.col = hr.staged = true;
+    hr.byte_path = false;
+    hr.cstride = COLB_STRIDE;
+    hr.smem_bytes = 2 * COLB_STRIDE * 4 + (H_THREADS / 32) * (int)sizeof(CsgWarp);
+    const int ng = (q->n_features + 31) / 32;
+    for (int g = 0; g < ng; ++g) {
+        ColGroup c;
+        c.f_lo = (int)((long long)q->n_features * g / ng);
+        c.f_hi = (int)((long long)q->n_features * (g + 1) / ng);
+        hr.cgroups.push_back(c);
+    }
+    if (cudaFuncSetAttribute(hist_csg_range_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hr.smem_bytes) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(hist_csg_range_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hr.smem_bytes) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    int o1 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, hist_csg_range_kernel<true>, H_THREADS, hr.smem_bytes) !=
+            cudaSuccess || o1 < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    hr.blocks_range = o1 * ctx->sm_count;
+    const long long G = (long long)hr.cgroups.size();
+    const long long per = (n + 2ll * hr.blocks_range - 1) / (2ll * hr.blocks_range) * G;
+    hr.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per));
+    return true;
+}
+
 static bool plan_root_staged(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, const HistPlan &hp, int grad_bits,
                              long long n, HistPlan &hr) {
-    if (hp.col || ctx->hist_layout != 0 || q->bits != 8 || grad_bits > 15 || qm.stride % 32 != 0 || n <= 0)
+    if (hp.col || (ctx->hist_layout != 0 && ctx->hist_layout != 4) || grad_bits > 15 || qm.stride % 32 != 0 ||
+        n <= 0)
         return false;
+    const bool forced = ctx->hist_layout == 4;
+    if (q->bits != 8) {
+        if (!forced && (double)n * q->n_features < 1e8) return false;
+        return plan_root_staged_generic(ctx, q, qm, n, hr);
+    }
     // small (L2-resident) matrices keep the compact root: YearMSD 515K x 90 0.565 vs 0.540 ms/round
-    if ((double)n * q->n_features < 1e8) return false;
+    if (!forced && (double)n * q->n_features < 1e8) return false;
     if (plan_hist(ctx, q, qm, false, n, hr, grad_bits, true, true) != GBM_OK) return false;  // compact root
     return hr.col && hr.staged;
 }

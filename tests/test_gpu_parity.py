@@ -423,6 +423,25 @@ def test_edge_shapes_parity(ctx, G, kind, grow):
     np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
 
 
+@pytest.mark.parametrize("cfg,n,missing,align,P", [("higgs", 60_000, 0.0, 32, 15), ("bosch", 12_000, 0.0, 32, 15),
+                                                  ("tiny", 3000, 0.05, 32, 15), ("airline", 40_000, 0.03, 32, 12),
+                                                  ("epsilon", 4_000, 0.0, 32, 15)])
+def test_staged_root_parity(ctx, G, cfg, n, missing, align, P):
+    """The staged bank-column root (byte and generic symbol widths) forced at small sizes
+    (GBM_OPT_HIST_LAYOUT 4), levels compact; and the root histogram itself vs the oracle."""
+    ctx.set_option(ctx.HIST_LAYOUT, 4)
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows) if cfg == "tiny" else None, missing=missing)
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth, grad_bits=P,
+                   row_align_bits=align)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth,
+                   grad_bits=P, row_align_bits=align, base_margin=ob.base_margin)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.HIST_LAYOUT, 0)
+
+
 def test_max_depth_zero_and_one(ctx, G):
     X, y = W.generate("tiny")
     for D in (0, 1):
