@@ -425,7 +425,8 @@ def test_edge_shapes_parity(ctx, G, kind, grow):
 
 @pytest.mark.parametrize("cfg,n,missing,align,P", [("higgs", 60_000, 0.0, 32, 15), ("bosch", 12_000, 0.0, 32, 15),
                                                   ("tiny", 3000, 0.05, 32, 15), ("airline", 40_000, 0.03, 32, 12),
-                                                  ("epsilon", 4_000, 0.0, 32, 15)])
+                                                  ("epsilon", 4_000, 0.0, 32, 15), ("higgs", 30_000, 0.0, 128, 15),
+                                                  ("bosch", 6_000, 0.0, 128, 15), ("tiny", 3000, 0.05, 0, 15)])
 def test_staged_root_parity(ctx, G, cfg, n, missing, align, P):
     """The staged bank-column root (byte and generic symbol widths) forced at small sizes
     (GBM_OPT_HIST_LAYOUT 4), levels compact; and the root histogram itself vs the oracle."""
