@@ -1107,13 +1107,16 @@ __device__ __forceinline__ void cs_batch_any(const QM &qm, CsWarp &st, int *hs, 
 template <bool IDENT, bool R1>
 __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArgs a) {
     extern __shared__ int smem[];
+    __shared__ long long s_red[2 * H_THREADS / 32];
     CsWarp *stage = reinterpret_cast<CsWarp *>(smem + 2 * COLB_STRIDE);
     const QM &qm = a.qm;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int NW = H_THREADS / 32;
+    long long tg = 0, th = 0;
     const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int g = it % a.n_groups;
+        const bool tot = a.totals && g == 0;
         const long long start = (long long)(it / a.n_groups) * a.chunk;
         const long long end = min(a.n_sel, start + a.chunk);
         const ColGroup cg = a.groups[g];
@@ -1133,6 +1136,15 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArg
                                  [&](int i) { return __ldg(a.qpair + rowf(i)); });
             else cs_batch(qm, stage[wid], smem, u_lo, Wg, Fg, R, copy, nrows, rowf,
                           [&](int i) { return __ldg(a.qpair + rowf(i)); });
+            if (tot) {  // the node totals from the staged pairs (rows past nrows are staged as 0)
+                const int2 q = stage[wid].q[lane];
+                tg += q.x;
+                th += q.y;
+            }
+        }
+        if (tot) {
+            block_totals(tg, th, s_red, a.totals);
+            tg = th = 0;
         }
         __syncthreads();
         col_flush<false>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist);
@@ -1157,11 +1169,14 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_csg_range_kernel(ColRangeAr
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int NW = H_THREADS / 32;
     CsgWarp &st = stage[wid];
+    __shared__ long long s_red[2 * H_THREADS / 32];
+    long long tg = 0, th = 0;
     const long long sw = qm.stride >> 5;
     const uint32_t mask = (1u << qm.bits) - 1u;
     const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int g = it % a.n_groups;
+        const bool tot = a.totals && g == 0;
         const long long start = (long long)(it / a.n_groups) * a.chunk;
         const long long end = min(a.n_sel, start + a.chunk);
         const ColGroup cg = a.groups[g];
@@ -1179,6 +1194,10 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_csg_range_kernel(ColRangeAr
             const int nrows = (int)min(32ll, end - b0);
             auto rowf = [&](int i) -> uint32_t { return IDENT ? (uint32_t)(b0 + i) : __ldg(a.ridx + b0 + i); };
             st.q[lane] = lane < nrows ? __ldg(a.qpair + rowf(lane)) : make_int2(0, 0);
+            if (tot) {
+                tg += st.q[lane].x;
+                th += st.q[lane].y;
+            }
             for (int idx = lane; idx < 32 * Wg; idx += 32) {
                 const int i = idx / Wg, w = idx - i * Wg;
                 st.w[idx] = i < nrows ? __ldg(qm.P + (long long)rowf(i) * sw + w_lo + w) : 0u;
@@ -1197,6 +1216,10 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_csg_range_kernel(ColRangeAr
                 }
             }
             __syncwarp();
+        }
+        if (tot) {
+            block_totals(tg, th, s_red, a.totals);
+            tg = th = 0;
         }
         __syncthreads();
         col_flush<false>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist);
@@ -2860,9 +2883,7 @@ static int launch_seg(gbm_ctx *ctx, const HistPlan &hp, SegArgs a, cudaStream_t 
 
 static void launch_col_range(const HistPlan &hp, const ColRangeArgs &ca, int grid, cudaStream_t s) {
     const int sm = hp.smem_bytes;
-    if (hp.staged) {
-        if (ca.totals) sum_qpair_kernel<<<std::min<long long>((ca.n_sel + 255) / 256, 148 * 8), 256, 0, s>>>(
-            ca.qpair, ca.n_sel, ca.totals);
+    if (hp.staged) {  // (the staged kernels reduce the totals from their staged pairs)
         if (!hp.byte_path) {  // generic symbol widths
             if (ca.ridx) hist_csg_range_kernel<false><<<grid, H_THREADS, sm, s>>>(ca);
             else hist_csg_range_kernel<true><<<grid, H_THREADS, sm, s>>>(ca);
