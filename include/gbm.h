@@ -268,6 +268,35 @@ GBM_API int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *qm, const int32_t *q
                    const int32_t *scale_d, const gbm_params *params, const gbm_tree *tree,
                    int32_t *row_leaf_d, void *stream);
 
+/* gbm_build_tree_fused: gbm_build_tree followed by gbm_update_margins and by pass 1 of the NEXT
+ * round's gbm_gradients (Eq. 1-2 for the updated margins: the per-row sigmoid for the logistic
+ * objective and this rank's max|g|, max|h|), fused into the final leaf assignment when the tree
+ * is depth-wise and its rows are staged (else run as separate kernels).  Results are identical
+ * to gbm_build_tree + gbm_update_margins + gbm_gradients; the next round then calls
+ * gbm_gradients_from_stats instead of gbm_gradients.  All buffers are caller-owned:
+ *   margin_d  fp64 [n_rows], updated in place     label_d  fp32 [n_rows]
+ *   sig_d     fp64 [n_rows] (logistic; unused for squared error)
+ *   maxbits_d uint64 [2]: this rank's maxima as bit patterns of non-negative doubles
+ * Label-domain violations latch GBM_E_LABEL as in gbm_gradients. */
+typedef struct {
+    double *margin_d;
+    const float *label_d;
+    int32_t objective;
+    int32_t reserved;
+    double *sig_d;
+    uint64_t *maxbits_d;
+} gbm_epilogue;
+GBM_API int gbm_build_tree_fused(gbm_ctx *ctx, const gbm_qmatrix *qm, const int32_t *qpair_d,
+                         const int32_t *scale_d, const gbm_params *params, const gbm_tree *tree,
+                         int32_t *row_leaf_d, const gbm_epilogue *epilogue, void *stream);
+/* gbm_gradients_from_stats: pass 2 of gbm_gradients from the statistics of the previous
+ * gbm_build_tree_fused (same margins and labels): the collective max over ranks (C1) and the
+ * fixed-point quantisation (R14).  Same outputs as gbm_gradients. */
+GBM_API int gbm_gradients_from_stats(gbm_ctx *ctx, int32_t objective, int32_t grad_bits,
+                             const double *margin_d, const float *label_d, int64_t n_rows,
+                             const double *sig_d, uint64_t *maxbits_d, int32_t *qpair_d,
+                             int32_t *scale_d, void *stream);
+
 /* ---- the steps of Algorithm 1, exposed one by one (used by the parity tests) ---------- */
 /* BuildPartialHistograms: hist_d int64 [TB][2] (overwritten) = sum over the listed
  * rows of (q_g, q_h) into bin cut_ptr[f] + symbol for every non-missing symbol.  rows_d

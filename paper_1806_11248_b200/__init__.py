@@ -55,6 +55,11 @@ class _Tree(C.Structure):
                                           "gain", "weight", "sum_qg", "sum_qh", "left_child")]
 
 
+class _Epilogue(C.Structure):
+    _fields_ = [("margin_d", C.c_void_p), ("label_d", C.c_void_p), ("objective", C.c_int32),
+                ("reserved", C.c_int32), ("sig_d", C.c_void_p), ("maxbits_d", C.c_void_p)]
+
+
 class _ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
                 ("bytes", C.c_double), ("rows", C.c_double)]
@@ -92,6 +97,12 @@ EXPORTS = {
                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gbm_build_tree": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_void_p,
                                  C.POINTER(_Params), C.POINTER(_Tree), C.c_void_p, C.c_void_p]),
+    "gbm_build_tree_fused": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_void_p,
+                                       C.POINTER(_Params), C.POINTER(_Tree), C.c_void_p,
+                                       C.POINTER(_Epilogue), C.c_void_p]),
+    "gbm_gradients_from_stats": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]),
     "gbm_build_histogram": (C.c_int, [C.c_void_p, C.POINTER(_QM), C.c_void_p, C.c_int32,
                                       C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "gbm_allreduce_histograms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
@@ -384,7 +395,7 @@ class Context:
     def build_tree(self, qm: QMatrix, qpair, scale, *, objective, max_depth, eta=0.3,
                    reg_lambda=1.0, gamma=0.0, min_child_weight=1.0,
                    grad_bits=DEFAULT_GRAD_BITS, tree: Tree | None = None, row_leaf=None,
-                   grow_policy="depthwise", max_leaves=0):
+                   grow_policy="depthwise", max_leaves=0, epilogue=None):
         lossguide = GROW_POLICIES.get(grow_policy, grow_policy) == 1
         tree = tree if tree is not None else Tree(max_depth, self.dev,
                                                   max_leaves if lossguide else 0)
@@ -393,9 +404,26 @@ class Context:
         prm = _params(objective, max_depth, eta, reg_lambda, gamma, min_child_weight, grad_bits,
                       grow_policy, max_leaves)
         qc, tc = qm.c(), tree.c()
-        _call("gbm_build_tree", self.h, C.byref(qc), _p(qpair), _p(scale), C.byref(prm),
-              C.byref(tc), _p(rl), _stream())
+        if epilogue is None:
+            _call("gbm_build_tree", self.h, C.byref(qc), _p(qpair), _p(scale), C.byref(prm),
+                  C.byref(tc), _p(rl), _stream())
+        else:  # fused: margin update + the next round's gradient statistics
+            margin, label, sig, maxbits = epilogue
+            ep = _Epilogue(margin.data_ptr(), label.data_ptr(), OBJECTIVES.get(objective, objective), 0,
+                           sig.data_ptr() if sig is not None else None, maxbits.data_ptr())
+            _call("gbm_build_tree_fused", self.h, C.byref(qc), _p(qpair), _p(scale), C.byref(prm),
+                  C.byref(tc), _p(rl), C.byref(ep), _stream())
         return tree, rl
+
+    def gradients_from_stats(self, objective, margin, label, sig, maxbits,
+                             grad_bits=DEFAULT_GRAD_BITS, out=None, scale=None):
+        """Pass 2 of gradients() from the statistics of the previous build_tree(epilogue=...)."""
+        n = margin.shape[0]
+        q = out if out is not None else torch.empty((n, 2), dtype=torch.int32, device=self.dev)
+        sc = scale if scale is not None else torch.empty(2, dtype=torch.int32, device=self.dev)
+        _call("gbm_gradients_from_stats", self.h, OBJECTIVES.get(objective, objective), grad_bits,
+              _p(margin), _p(label), n, _p(sig), _p(maxbits), _p(q), _p(sc), _stream())
+        return q, sc
 
     def build_histogram(self, qm: QMatrix, qpair, grad_bits, rows=None):
         TB = qm.n_bins_total
@@ -487,7 +515,8 @@ class Booster:
     def __init__(self, ctx: Context, X: torch.Tensor, y: torch.Tensor, *, max_bins: int,
                  objective: str, max_depth: int, eta=0.3, reg_lambda=1.0, gamma=0.0,
                  min_child_weight=1.0, grad_bits=DEFAULT_GRAD_BITS, row_align_bits=32,
-                 base_margin=0.0, cuts=None, colsym=True, grow_policy="depthwise", max_leaves=0):
+                 base_margin=0.0, cuts=None, colsym=True, grow_policy="depthwise", max_leaves=0,
+                 fused=True):
         self.ctx, self.y = ctx, y
         self.objective, self.max_depth, self.grad_bits = objective, max_depth, grad_bits
         self.kw = dict(eta=eta, reg_lambda=reg_lambda, gamma=gamma,
@@ -501,15 +530,33 @@ class Booster:
         self.scale = torch.empty(2, dtype=torch.int32, device=ctx.dev)
         self.row_leaf = torch.empty(n, dtype=torch.int32, device=ctx.dev)
         self.trees: list[Tree] = []
+        # fused rounds: the tree build also updates the margins and computes the next round's
+        # gradient statistics (gbm_build_tree_fused / gbm_gradients_from_stats)
+        self.fused = fused
+        lg = OBJECTIVES.get(objective, objective) == 1
+        self.sig = torch.empty(max(n, 1), dtype=torch.float64, device=ctx.dev) if fused and lg else None
+        self.maxbits = torch.zeros(2, dtype=torch.int64, device=ctx.dev) if fused else None
+        self.stats_valid = False
 
     def round(self, keep_tree=True) -> Tree:
         c = self.ctx
-        c.gradients(self.objective, self.margin, self.y, self.grad_bits, out=self.qpair,
-                    scale=self.scale)
-        tree, _ = c.build_tree(self.qm, self.qpair, self.scale, objective=self.objective,
-                               max_depth=self.max_depth, grad_bits=self.grad_bits,
-                               row_leaf=self.row_leaf, **self.kw)
-        c.update_margins(tree["weight"], self.row_leaf, self.margin)
+        if self.fused and self.stats_valid:
+            c.gradients_from_stats(self.objective, self.margin, self.y, self.sig, self.maxbits,
+                                   self.grad_bits, out=self.qpair, scale=self.scale)
+        else:
+            c.gradients(self.objective, self.margin, self.y, self.grad_bits, out=self.qpair,
+                        scale=self.scale)
+        if self.fused:
+            tree, _ = c.build_tree(self.qm, self.qpair, self.scale, objective=self.objective,
+                                   max_depth=self.max_depth, grad_bits=self.grad_bits,
+                                   row_leaf=self.row_leaf,
+                                   epilogue=(self.margin, self.y, self.sig, self.maxbits), **self.kw)
+            self.stats_valid = True
+        else:
+            tree, _ = c.build_tree(self.qm, self.qpair, self.scale, objective=self.objective,
+                                   max_depth=self.max_depth, grad_bits=self.grad_bits,
+                                   row_leaf=self.row_leaf, **self.kw)
+            c.update_margins(tree["weight"], self.row_leaf, self.margin)
         if keep_tree:
             self.trees.append(tree)
         return tree

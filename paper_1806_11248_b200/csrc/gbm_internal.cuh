@@ -124,6 +124,12 @@ namespace gbm {
 
 int ctx_enter(gbm_ctx *ctx);  // cudaSetDevice + argument check
 
+// gradients.cu helpers used by the tree builder's fused epilogue fallback
+int grad_pass1(gbm_ctx *ctx, int objective, const double *margin_d, const float *label_d, long long n_rows,
+               unsigned long long *maxbits, double *sig, cudaStream_t s);
+int update_margins_launch(gbm_ctx *ctx, const double *weight_d, const int32_t *row_leaf_d, long long n_rows,
+                          double *margin_d, cudaStream_t s);
+
 // device row counter for the next profiled launch (nullptr when profiling is off)
 unsigned long long *prof_rows_slot(gbm_ctx *ctx, int *slot);
 
@@ -216,5 +222,48 @@ __device__ __forceinline__ double fixed_to_double(long long v, int s) {
 }
 
 __host__ __device__ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- Eq. 1-2 with the canonical sigmoid (R19): shared by gradients.cu and the fused epilogue of
+// the tree builder (tree.cu)
+static __constant__ double DE_C[14] = {
+    0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5,
+    0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
+    0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};
+
+// det_exp(t), t <= 0
+__device__ __forceinline__ double det_exp(double t) {
+    if (t < -745.0) return 0.0;
+    double k = rint(dmul(t, 0x1.71547652b82fep+0));
+    double r = fma(-k, 0x1.62e42feep-1, t);
+    r = fma(-k, 0x1.a39ef35793c76p-33, r);
+    double p = DE_C[13];
+#pragma unroll
+    for (int i = 12; i >= 0; --i) p = fma(p, r, DE_C[i]);
+    return ldexp_exact(p, (int)k);
+}
+
+__device__ __forceinline__ double sigmoid(double x) {
+    if (x >= 0.0) {
+        double e = det_exp(-x);
+        return ddiv(1.0, dadd(1.0, e));
+    }
+    double e = det_exp(x);
+    return ddiv(e, dadd(1.0, e));
+}
+
+// Eq. 1-2 (logistic, from s = sigmoid(margin)) / squared error
+__device__ __forceinline__ void grad_hess_s(int obj, double m_or_s, float yl, double &g, double &h) {
+    const double y = (double)yl;
+    if (obj == GBM_SQUARED_ERROR) {
+        g = dsub(m_or_s, y);
+        h = 1.0;
+        return;
+    }
+    const double s = m_or_s;
+    g = dsub(s, y);
+    h = dmul(s, dsub(1.0, s));
+}
+
 
 }  // namespace gbm

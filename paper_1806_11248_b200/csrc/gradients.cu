@@ -10,46 +10,6 @@
 
 namespace gbm {
 
-__constant__ double DE_C[14] = {
-    0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5,
-    0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
-    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
-    0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};
-
-// det_exp(t), t <= 0
-__device__ __forceinline__ double det_exp(double t) {
-    if (t < -745.0) return 0.0;
-    double k = rint(dmul(t, 0x1.71547652b82fep+0));
-    double r = fma(-k, 0x1.62e42feep-1, t);
-    r = fma(-k, 0x1.a39ef35793c76p-33, r);
-    double p = DE_C[13];
-#pragma unroll
-    for (int i = 12; i >= 0; --i) p = fma(p, r, DE_C[i]);
-    return ldexp_exact(p, (int)k);
-}
-
-__device__ __forceinline__ double sigmoid(double x) {
-    if (x >= 0.0) {
-        double e = det_exp(-x);
-        return ddiv(1.0, dadd(1.0, e));
-    }
-    double e = det_exp(x);
-    return ddiv(e, dadd(1.0, e));
-}
-
-// Eq. 1-2 (logistic, from s = sigmoid(margin)) / squared error
-__device__ __forceinline__ void grad_hess_s(int obj, double m_or_s, float yl, double &g, double &h) {
-    const double y = (double)yl;
-    if (obj == GBM_SQUARED_ERROR) {
-        g = dsub(m_or_s, y);
-        h = 1.0;
-        return;
-    }
-    const double s = m_or_s;
-    g = dsub(s, y);
-    h = dmul(s, dsub(1.0, s));
-}
-
 constexpr int G_THREADS = 256;
 constexpr int GU = 4;  // rows in flight per thread in the streaming kernels
 
@@ -209,6 +169,64 @@ using namespace gbm;
 
 extern "C" {
 
+}  // extern "C"
+
+namespace gbm {
+// pass 1 of gbm_gradients into caller-provided statistics (maxbits zeroed here)
+int grad_pass1(gbm_ctx *ctx, int objective, const double *margin_d, const float *label_d, long long n_rows,
+               unsigned long long *maxbits, double *sig, cudaStream_t s) {
+    GBM_CUDA(cudaMemsetAsync(maxbits, 0, 16, s));
+    if (n_rows > 0) {
+        ProfScope ps(ctx, PC_GRAD_MAX, s, (double)n_rows * 12);
+        grad_max_kernel<<<grid_for(n_rows, G_THREADS, ctx->sm_count), G_THREADS, 0, s>>>(
+            objective, margin_d, label_d, n_rows, maxbits, sig, ctx->dev_err);
+        GBM_CUDA(cudaGetLastError());
+    }
+    return GBM_OK;
+}
+// pass 2: C1 (global max over ranks) and the fixed-point quantisation
+static int grad_pass2(gbm_ctx *ctx, int objective, int grad_bits, const double *margin_d, const float *label_d,
+                      long long n_rows, unsigned long long *maxbits, const double *sig, int32_t *qpair_d,
+                      int32_t *scale_d, cudaStream_t s) {
+    if (ctx->comm) {  // C1: global max of |g|, |h| (exact, order-free)
+        ProfScope ps(ctx, PC_ALLREDUCE, s, 16.0);
+        GBM_NCCL(ncclAllReduce(maxbits, maxbits, 2, ncclUint64, ncclMax, ctx->comm, s));
+    }
+    {
+        ProfScope ps(ctx, PC_GRAD_QUANT, s, (double)n_rows * 20);
+        grad_quant_kernel<<<grid_for(n_rows, G_THREADS, ctx->sm_count), G_THREADS, 0, s>>>(
+            objective, grad_bits, margin_d, label_d, n_rows, maxbits, sig, reinterpret_cast<int2 *>(qpair_d), scale_d);
+    }
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+int update_margins_launch(gbm_ctx *ctx, const double *weight_d, const int32_t *row_leaf_d, long long n_rows,
+                          double *margin_d, cudaStream_t s) {
+    if (n_rows == 0) return GBM_OK;
+    ProfScope ps(ctx, PC_MARGINS, s, (double)n_rows * 20);
+    update_margins_kernel<<<grid_for(n_rows, 256, ctx->sm_count), 256, 0, s>>>(weight_d, row_leaf_d, n_rows, margin_d);
+    GBM_CUDA(cudaGetLastError());
+    return GBM_OK;
+}
+}  // namespace gbm
+
+extern "C" {
+
+int gbm_gradients_from_stats(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const double *margin_d,
+                             const float *label_d, int64_t n_rows, const double *sig_d, uint64_t *maxbits_d,
+                             int32_t *qpair_d, int32_t *scale_d, void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    GBM_REQUIRE(objective == GBM_SQUARED_ERROR || objective == GBM_LOGISTIC, GBM_E_ARG,
+                "gbm_gradients_from_stats: unknown objective");
+    GBM_REQUIRE(grad_bits >= 1 && grad_bits <= 30, GBM_E_ARG, "gbm_gradients_from_stats: grad_bits in 1..30");
+    GBM_REQUIRE(n_rows > 0 || (ctx->comm && ctx->nranks > 1), GBM_E_EMPTY, "gbm_gradients_from_stats: zero rows");
+    GBM_REQUIRE(((margin_d && label_d && qpair_d) || n_rows == 0) && scale_d && maxbits_d &&
+                    (objective != GBM_LOGISTIC || sig_d || n_rows == 0),
+                GBM_E_ARG, "gbm_gradients_from_stats: null pointer");
+    return grad_pass2(ctx, objective, grad_bits, margin_d, label_d, n_rows,
+                      reinterpret_cast<unsigned long long *>(maxbits_d), sig_d, qpair_d, scale_d, (cudaStream_t)stream);
+}
+
 int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const double *margin_d,
                   const float *label_d, int64_t n_rows, int32_t *qpair_d, int32_t *scale_d,
                   void *stream) {
@@ -224,23 +242,8 @@ int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const doub
     GBM_TRY(ctx->arena.reserve(512 + (lg ? (size_t)n_rows * 8 : 0)));
     unsigned long long *maxbits = ctx->arena.take<unsigned long long>(2);
     double *sig = lg ? ctx->arena.take<double>((size_t)std::max<int64_t>(n_rows, 1)) : nullptr;
-    GBM_CUDA(cudaMemsetAsync(maxbits, 0, 16, s));
-    int grid = grid_for(n_rows, G_THREADS, ctx->sm_count);
-    if (n_rows > 0) {
-        ProfScope ps(ctx, PC_GRAD_MAX, s, (double)n_rows * 12);
-        grad_max_kernel<<<grid, G_THREADS, 0, s>>>(objective, margin_d, label_d, n_rows, maxbits, sig, ctx->dev_err);
-    }
-    if (ctx->comm) {  // C1: global max of |g|, |h| (exact, order-free)
-        ProfScope ps(ctx, PC_ALLREDUCE, s, 16.0);
-        GBM_NCCL(ncclAllReduce(maxbits, maxbits, 2, ncclUint64, ncclMax, ctx->comm, s));
-    }
-    {
-        ProfScope ps(ctx, PC_GRAD_QUANT, s, (double)n_rows * 20);
-        grad_quant_kernel<<<grid, G_THREADS, 0, s>>>(objective, grad_bits, margin_d, label_d, n_rows, maxbits, sig,
-                                                     reinterpret_cast<int2 *>(qpair_d), scale_d);
-    }
-    GBM_CUDA(cudaGetLastError());
-    return GBM_OK;
+    GBM_TRY(grad_pass1(ctx, objective, margin_d, label_d, n_rows, maxbits, sig, s));
+    return grad_pass2(ctx, objective, grad_bits, margin_d, label_d, n_rows, maxbits, sig, qpair_d, scale_d, s);
 }
 
 int gbm_update_margins(gbm_ctx *ctx, const double *weight_d, const int32_t *row_leaf_d,

@@ -1527,13 +1527,26 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_kernel(QM qm, const in
 // into shared memory (row pitch W|1 words: conflict-free), then each lane walks its row from
 // registers.  Moves exactly the packed bytes once, in row order (vs a 32-byte sector per level
 // and row for the feature-major gathers of leaf_walk_kernel once the rows' nodes diverge).
-template <int W>
+// Fused epilogue of gbm_build_tree_fused: with each row's leaf, margin += weight[leaf]
+// (gbm_update_margins) and Eq. 1-2 for the new margin (pass 1 of the next gbm_gradients: the
+// logistic sigmoid into sig, this rank's max|g|, max|h|), in the same op order as those entries.
+struct WalkEpi {
+    double *margin;
+    const float *label;
+    int objective;
+    double *sig;
+    unsigned long long *maxbits;
+    uint32_t *dev_err;
+    const double *weight;
+};
+
+template <int W, bool EPI>
 __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, const int8_t *__restrict__ kind,
                                                                      const int32_t *__restrict__ feature,
                                                                      const int32_t *__restrict__ bin,
                                                                      const int8_t *__restrict__ dl, int n_internal,
                                                                      int depth, long long n,
-                                                                     int32_t *__restrict__ row_leaf) {
+                                                                     int32_t *__restrict__ row_leaf, WalkEpi ep) {
     constexpr int PW = W | 1;
     extern __shared__ int s_tree[];
     __shared__ uint32_t s_rows[WALK_THREADS / 32][32 * PW];
@@ -1545,6 +1558,8 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *sr = s_rows[wid];
+    double mg = 0.0, mh = 0.0;  // (EPI)
+    bool bad = false;
     const long long n_chunks = (n + 31) / 32;
     const long long cstep = (long long)gridDim.x * (WALK_THREADS / 32);
     uint32_t v[W];
@@ -1582,9 +1597,36 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
                 const bool left = sym == qm.B ? ((fk >> 20) & 1) : (sym <= s_b[k]);
                 k = left ? 2 * k + 1 : 2 * k + 2;
             }
-            row_leaf[c * 32 + lane] = k;
+            const long long r = c * 32 + lane;
+            row_leaf[r] = k;
+            if (EPI) {
+                const double m = dadd(ep.margin[r], __ldg(ep.weight + k));
+                ep.margin[r] = m;
+                const float yl = __ldg(ep.label + r);
+                double v = m;
+                if (ep.objective == GBM_LOGISTIC) {
+                    v = sigmoid(m);
+                    ep.sig[r] = v;
+                    bad |= !(yl == 0.0f || yl == 1.0f);
+                }
+                double g, hh;
+                grad_hess_s(ep.objective, v, yl, g, hh);
+                mg = fmax(mg, fabs(g));
+                mh = fmax(mh, fabs(hh));
+            }
         }
         __syncwarp();
+    }
+    if (EPI) {
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(ep.dev_err, DERR_LABEL);
+        for (int o = 16; o > 0; o >>= 1) {
+            mg = fmax(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+            mh = fmax(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+        }
+        if (lane == 0) {  // non-negative doubles order like their bit patterns
+            atomicMax(ep.maxbits + 0, (unsigned long long)__double_as_longlong(mg));
+            atomicMax(ep.maxbits + 1, (unsigned long long)__double_as_longlong(mh));
+        }
     }
 }
 
@@ -2945,9 +2987,18 @@ static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStr
 
 template <int W>
 static void launch_walk_reg(int grid, size_t sm, cudaStream_t s, const QM &qm, const TreeDev &t, int n_int, int D,
-                            long long n, int32_t *rl) {
-    if (sm > 16 * 1024) cudaFuncSetAttribute(leaf_walk_stg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    leaf_walk_stg_kernel<W><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl);
+                            long long n, int32_t *rl, const WalkEpi *epi) {
+    if (epi) {
+        if (sm > 16 * 1024)
+            cudaFuncSetAttribute(leaf_walk_stg_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        leaf_walk_stg_kernel<W, true><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
+                                                                     n_int, D, n, rl, *epi);
+    } else {
+        if (sm > 16 * 1024)
+            cudaFuncSetAttribute(leaf_walk_stg_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        leaf_walk_stg_kernel<W, false><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
+                                                                      n_int, D, n, rl, WalkEpi{});
+    }
 
 }
 
@@ -3526,8 +3577,13 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     return GBM_OK;
 }
 
-int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
-                   const gbm_params *prm, const gbm_tree *tree, int32_t *row_leaf_d, void *stream) {
+}  // extern "C"
+
+// gbm_build_tree / gbm_build_tree_fused: ep (nullable) is fused into the final walk when the
+// staged walk applies (*ep_done = true); otherwise the caller runs it as separate kernels.
+static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
+                           const gbm_params *prm, const gbm_tree *tree, int32_t *row_leaf_d, void *stream,
+                           const gbm_epilogue *ep, bool *ep_done) {
     GBM_TRY(ctx_enter(ctx));
     GBM_TRY(check_qm(q));
     GBM_REQUIRE(prm && tree && scale_d && row_leaf_d && qpair_d, GBM_E_ARG, "gbm_build_tree: null argument");
@@ -3738,8 +3794,17 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             if (n > 0 && sm > 64 * 1024) {
                 leaf_walk_global_kernel<<<grid, WALK_THREADS, 0, s>>>(qm, t, D, n, row_leaf_d);
             } else if (n > 0 && W >= 1 && W <= 16 && ctx->walk_mode != 1) {
+                WalkEpi wepi_v = {};
+                const WalkEpi *wepi = nullptr;
+                if (ep) {  // margin update + next round's gradient statistics in the same pass
+                    GBM_CUDA(cudaMemsetAsync(ep->maxbits_d, 0, 16, s));
+                    wepi_v = WalkEpi{ep->margin_d, ep->label_d, ep->objective, ep->sig_d,
+                                     reinterpret_cast<unsigned long long *>(ep->maxbits_d), ctx->dev_err, t.weight};
+                    wepi = &wepi_v;
+                    *ep_done = true;
+                }
                 switch (W) {
-#define GBM_WALK(w) case w: launch_walk_reg<w>(grid, sm, s, qm, t, n_internal, D, n, row_leaf_d); break;
+#define GBM_WALK(w) case w: launch_walk_reg<w>(grid, sm, s, qm, t, n_internal, D, n, row_leaf_d, wepi); break;
                     GBM_WALK(1) GBM_WALK(2) GBM_WALK(3) GBM_WALK(4) GBM_WALK(5) GBM_WALK(6) GBM_WALK(7) GBM_WALK(8)
                     GBM_WALK(9) GBM_WALK(10) GBM_WALK(11) GBM_WALK(12) GBM_WALK(13) GBM_WALK(14) GBM_WALK(15)
                     GBM_WALK(16)
@@ -3867,6 +3932,33 @@ int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, c
             }
             if (!seg_mode) GBM_TRY(wait_on(s, ctx->ev_join, ctx->side));  // join: the next level reads the scatter
         }
+    }
+    return GBM_OK;
+}
+
+extern "C" {
+
+int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
+                   const gbm_params *prm, const gbm_tree *tree, int32_t *row_leaf_d, void *stream) {
+    bool done = false;
+    return build_tree_impl(ctx, q, qpair_d, scale_d, prm, tree, row_leaf_d, stream, nullptr, &done);
+}
+
+int gbm_build_tree_fused(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
+                         const gbm_params *prm, const gbm_tree *tree, int32_t *row_leaf_d,
+                         const gbm_epilogue *ep, void *stream) {
+    GBM_REQUIRE(ep && (ep->objective == GBM_SQUARED_ERROR || ep->objective == GBM_LOGISTIC), GBM_E_ARG,
+                "gbm_build_tree_fused: bad epilogue");
+    GBM_REQUIRE(q && ((ep->margin_d && ep->label_d) || q->n_rows == 0) && ep->maxbits_d &&
+                    (ep->objective != GBM_LOGISTIC || ep->sig_d || q->n_rows == 0),
+                GBM_E_ARG, "gbm_build_tree_fused: null epilogue buffer");
+    bool done = false;
+    GBM_TRY(build_tree_impl(ctx, q, qpair_d, scale_d, prm, tree, row_leaf_d, stream, ep, &done));
+    if (!done) {  // the separate kernels of gbm_update_margins and pass 1 of gbm_gradients
+        cudaStream_t s = (cudaStream_t)stream;
+        GBM_TRY(update_margins_launch(ctx, tree->weight, row_leaf_d, q->n_rows, ep->margin_d, s));
+        GBM_TRY(grad_pass1(ctx, ep->objective, ep->margin_d, ep->label_d, q->n_rows,
+                           reinterpret_cast<unsigned long long *>(ep->maxbits_d), ep->sig_d, s));
     }
     return GBM_OK;
 }

@@ -638,3 +638,25 @@ def test_segment_histogram_modes(ctx, G, cfg, n, missing, carry, seg):
         np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
     ctx.set_option(ctx.SEGMENT_HIST, 0)
     ctx.set_option(ctx.CARRY_GRADIENTS, 0)
+
+
+@pytest.mark.parametrize("cfg,obj_override,D", [("higgs", None, 6), ("tiny", None, 3), ("yearmsd", None, 6),
+                                                ("tiny", None, 0), ("bosch", None, 4)])
+def test_fused_round_equals_separate_calls(ctx, G, cfg, obj_override, D):
+    """gbm_build_tree_fused + gbm_gradients_from_stats (the default Booster round) against
+    gbm_gradients + gbm_build_tree + gbm_update_margins, and both against the oracle."""
+    c = W.CONFIGS[cfg]
+    n = min(c.n_rows, 40_000)
+    X, y = W.generate(cfg, 0, n, missing=0.02 if cfg == "tiny" else 0.0)
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=D)
+    kw = dict(max_bins=c.max_bins, objective=c.objective, max_depth=D, base_margin=ob.base_margin)
+    gf = G.Booster(ctx, dev(X), dev(y), fused=True, **kw)
+    gs = G.Booster(ctx, dev(X), dev(y), fused=False, **kw)
+    for _ in range(3):
+        ot = ob.round()
+        tf, ts = gf.round().to_numpy(), gs.round().to_numpy()
+        _compare_tree(tf, ot)
+        _compare_tree(ts, ot)
+        np.testing.assert_array_equal(gf.qpair.cpu().numpy(), ob.last["qpair"])
+        np.testing.assert_array_equal(gf.margin.cpu().numpy(), ob.margin)
+        np.testing.assert_array_equal(gs.margin.cpu().numpy(), ob.margin)
