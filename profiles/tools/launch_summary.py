@@ -2,8 +2,8 @@
 bench.py into a markdown table of per-round kernel time and shares.
 
 usage: python profiles/tools/launch_summary.py LAUNCHES.csv OUT.md "command line" [bench_ms_per_round]
-A boosting round is counted by its grad_max_kernel launch; one-time kernels (cuts, packing,
-transpose, predict, torch copies) are listed separately."""
+A boosting round is counted by its init_tree_kernel launch (one per tree); one-time kernels
+(cuts, packing, transpose, predict, torch copies) are listed separately."""
 import collections
 import csv
 import sys
@@ -19,7 +19,7 @@ for r in rows[1:]:
     name = r[ki].split("(")[0].replace("void ", "")
     agg[name][0] += 1
     agg[name][1] += float(r[vi].replace(",", "")) * scale[r[ui]]
-rounds = max(c for k, (c, _) in agg.items() if "grad_max_kernel" in k)
+rounds = max(c for k, (c, _) in agg.items() if "init_tree_kernel" in k)
 ONE_TIME = ("keys_kernel", "sort_", "scan_rows", "runs_count", "select", "cutptr", "tag",
             "write_cuts", "quantise", "pack_kernel", "transpose", "predict", "at::", "init_")
 per_round = {k: v for k, v in agg.items() if not any(t in k for t in ONE_TIME) or "init_tree" in k}
