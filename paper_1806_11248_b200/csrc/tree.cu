@@ -71,12 +71,6 @@ struct TreeDev {
     int32_t *left_child;  // optional for depth-wise trees
 };
 
-struct RangeItem {  // rows [start, start+len) of a row source, one feature group
-    int slot, group;
-    long long start;
-    int len, pad;
-};
-
 struct Group {
     int u_lo, u_hi;      // units [u_lo, u_hi) of a row (a unit = S consecutive features)
     int bin_lo, bin_hi;  // global bins of the group's features
