@@ -118,9 +118,13 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  * GBM_OPT_SEGMENT_HIST: with several shared-memory feature groups (wide data): 2 = each level
  *   is partitioned once and the built children's row segments are histogrammed group by group;
  *   1 = the fused kernel repeats the partition in every group; 0 (default) = 2 for symbols
- *   wider or narrower than a byte, else 1 (measured). */
+ *   wider or narrower than a byte, else 1 (measured).
+ * GBM_OPT_TMA_ROWS: 1 (default) the staged root kernel fetches whole 32-row batches with TMA bulk
+ *   copies (cp.async.bulk + mbarrier, double-buffered) when one group covers every word of a
+ *   row; 0 = per-lane loads. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
-       GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8 };
+       GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
+       GBM_OPT_TMA_ROWS = 10 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

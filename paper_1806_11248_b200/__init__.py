@@ -318,6 +318,7 @@ class Context:
     LEAF_WALK = 6
     EVAL_SCREEN = 7
     SEGMENT_HIST = 8
+    TMA_ROWS = 10
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

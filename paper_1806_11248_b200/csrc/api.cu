@@ -289,6 +289,10 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->seg_hist = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_TMA_ROWS) {
+        ctx->stage_tma = value != 0;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_EVAL_SCREEN) {
         ctx->eval_screen = value != 0;
         return GBM_OK;

@@ -112,6 +112,7 @@ struct gbm_ctx {
     int eval_warp = 0;             // GBM_OPT_EVAL_WARP (0 auto, 1 warp per feature, 2 block)
     int eval_screen = 0;           // GBM_OPT_EVAL_SCREEN (1 on, 0 every candidate exactly)
     int seg_hist = 0;              // GBM_OPT_SEGMENT_HIST (0 auto, 1 off, 2 on)
+    int stage_tma = 1;             // staged root: TMA bulk row copies (GBM_OPT_TMA_ROWS)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     // second stream of gbm_build_tree: the partition scatter of a level overlaps the allreduce

@@ -865,6 +865,7 @@ __device__ __forceinline__ ColLane col_lane(const QM &qm, const ColGroup &cg) {
 }
 
 struct ColRangeArgs {
+    int tma;  // staged root: TMA bulk copies of whole rows (set by the host when applicable)
     QM qm;
     const int2 *qpair;
     const uint32_t *ridx;        // null = identity rows
@@ -1016,6 +1017,21 @@ struct CsWarp {
 };
 
 // Stage rows row_i (i < 32, valid_i) of group words [u_lo, u_lo+Wg) and their pairs; then add.
+// accumulate a staged batch (R rows per warp instruction, lane = copy * Fg + feature)
+__device__ __forceinline__ void cs_consume(const CsWarp &st, int *hs, int Wg, int Fg, int R, int copy, int nrows) {
+    const int lane = threadIdx.x & 31;
+    const uint8_t *sb = reinterpret_cast<const uint8_t *>(st.w);
+    const int col = lane % Fg;  // byte of the feature within the staged row
+    const int rowbytes = Wg * 4;
+#pragma unroll 4
+    for (int i0 = 0; i0 < nrows; i0 += R) {
+        const int i = min(i0 + copy, 31);
+        const int sym = sb[i * rowbytes + col];
+        const int2 q = (i0 + copy < nrows) ? st.q[i] : make_int2(0, 0);
+        col_add_b<false>(hs, (sym << 5) + lane, q);
+    }
+}
+
 template <class RowF, class QF>
 __device__ __forceinline__ void cs_batch(const QM &qm, CsWarp &st, int *hs, int u_lo, int Wg, int Fg, int R, int copy,
                                          int nrows, RowF rowf, QF qf) {
@@ -1033,16 +1049,7 @@ __device__ __forceinline__ void cs_batch(const QM &qm, CsWarp &st, int *hs, int 
         st.w[idx] = i < nrows ? __ldg(qm.P + (long long)rowf(i) * sw + u_lo + w) : 0u;
     }
     __syncwarp();
-    const uint8_t *sb = reinterpret_cast<const uint8_t *>(st.w);
-    const int col = lane % Fg;  // byte of the feature within the staged row
-    const int rowbytes = Wg * 4;
-#pragma unroll 4
-    for (int i0 = 0; i0 < nrows; i0 += R) {
-        const int i = min(i0 + copy, 31);
-        const int sym = sb[i * rowbytes + col];
-        const int2 q = (i0 + copy < nrows) ? st.q[i] : make_int2(0, 0);
-        col_add_b<false>(hs, (sym << 5) + lane, q);
-    }
+    cs_consume(st, hs, Wg, Fg, R, copy, nrows);
     __syncwarp();
 }
 
@@ -1050,6 +1057,22 @@ __device__ __forceinline__ void cs_batch(const QM &qm, CsWarp &st, int *hs, int 
 // each staged row into its own bank column.  Compile-time row pitch, no per-row bounds logic
 // (rows past nrows are staged as symbol 0 with a zero pair: adds of 0), the pair broadcast from
 // shared memory -- about 5 instructions and 4 conflict-free wavefronts per row.
+template <int WG>
+__device__ __forceinline__ void cs_consume_r1(const CsWarp &st, int *hs, int Fg) {
+    const int lane = threadIdx.x & 31;
+    const uint8_t *sb = reinterpret_cast<const uint8_t *>(st.w) + lane;
+    int *hg = hs + lane, *hh = hs + COLB_STRIDE + lane;
+    if (lane < Fg) {
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            const int sym = sb[i * WG * 4];
+            const int2 q = st.q[i];
+            atomicAdd(hg + (sym << 5), q.x);
+            atomicAdd(hh + (sym << 5), q.y);
+        }
+    }
+}
+
 template <int WG, class RowF, class QF>
 __device__ __forceinline__ void cs_batch_r1(const QM &qm, CsWarp &st, int *hs, int u_lo, int Fg, int nrows, RowF rowf,
                                             QF qf) {
@@ -1066,17 +1089,7 @@ __device__ __forceinline__ void cs_batch_r1(const QM &qm, CsWarp &st, int *hs, i
 #pragma unroll
     for (int k = 0; k < WG; ++k) st.w[lane + 32 * k] = v[k];
     __syncwarp();
-    const uint8_t *sb = reinterpret_cast<const uint8_t *>(st.w) + lane;
-    int *hg = hs + lane, *hh = hs + COLB_STRIDE + lane;
-    if (lane < Fg) {
-#pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-            const int sym = sb[i * WG * 4];
-            const int2 q = st.q[i];
-            atomicAdd(hg + (sym << 5), q.x);
-            atomicAdd(hh + (sym << 5), q.y);
-        }
-    }
+    cs_consume_r1<WG>(st, hs, Fg);
     __syncwarp();
 }
 
@@ -1095,6 +1108,31 @@ __device__ __forceinline__ void cs_batch_any(const QM &qm, CsWarp &st, int *hs, 
     cs_batch(qm, st, hs, u_lo, Wg, Fg, R, copy, nrows, rowf, qf);
 }
 
+// ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier)
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // R1: every group has more than 16 features (one row per warp instruction, compile-time row
 // pitch); a separate instantiation so the other path's code generation is not affected
 // (Airline, 13 features: root 2.69 vs 3.13 ms when the R1 variants are not in the same kernel).
@@ -1102,11 +1140,25 @@ template <bool IDENT, bool R1>
 __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArgs a) {
     extern __shared__ int smem[];
     __shared__ long long s_red[2 * H_THREADS / 32];
+    __shared__ uint64_t s_bar[2 * H_THREADS / 32];  // per warp: one mbarrier per staging buffer
     CsWarp *stage = reinterpret_cast<CsWarp *>(smem + 2 * COLB_STRIDE);
     const QM &qm = a.qm;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int NW = H_THREADS / 32;
     long long tg = 0, th = 0;
+    const long long sw_row = qm.stride >> 5;
+    // whole contiguous rows (identity rows, one group covering every word): TMA bulk copies of
+    // 32-row batches into two staging buffers per warp, the next batch in flight while the
+    // current one is accumulated
+    const bool tma = IDENT && a.n_groups == 1 && a.tma;
+    uint64_t *bar = s_bar + 2 * wid;
+    unsigned uses0 = 0, uses1 = 0;  // completed phases per barrier
+    if (tma && lane == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     const int n_items = (int)(((a.n_sel + a.chunk - 1) / a.chunk) * a.n_groups);
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int g = it % a.n_groups;
@@ -1120,7 +1172,46 @@ __global__ void __launch_bounds__(H_THREADS, 2) hist_cs_range_kernel(ColRangeArg
         const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
         const int copy = min(lane / Fg, R - 1);
         const int u_lo = cg.f_lo >> 2, Wg = ((cg.f_hi + 3) >> 2) - u_lo;
-        for (long long b0 = start + (long long)wid * 32; b0 < end; b0 += NW * 32) {
+        long long b_first = start + (long long)wid * 32;
+        if (tma && Wg == sw_row) {
+            const long long first_b = b_first;
+            const int n_full = first_b + 32 <= end ? (int)((end - first_b - 32) / (NW * 32)) + 1 : 0;
+            const unsigned bytes_w = 32u * Wg * 4u;
+            auto issue = [&](int i) {  // lane 0: batch i into buffer i & 1
+                const long long b0 = first_b + (long long)i * NW * 32;
+                CsWarp *buf = stage + (i & 1) * NW + wid;
+                uint64_t *br = bar + (i & 1);
+                fence_proxy_async();  // the buffer's previous generic reads precede the TMA writes
+                mbar_arrive_expect_tx(br, bytes_w + 256u);
+                bulk_g2s(buf->w, qm.P + b0 * sw_row, bytes_w, br);
+                bulk_g2s(buf->q, a.qpair + b0, 256u, br);
+            };
+            if (n_full > 0 && lane == 0) issue(0);
+            for (int i = 0; i < n_full; ++i) {
+                if (i + 1 < n_full && lane == 0) issue(i + 1);
+                const unsigned par = (i & 1) ? (uses1++ & 1u) : (uses0++ & 1u);
+                mbar_wait(bar + (i & 1), par);
+                const CsWarp &st = stage[(i & 1) * NW + wid];
+                if (R1) {
+                    switch (Wg) {
+                        case 5: cs_consume_r1<5>(st, smem, Fg); break;
+                        case 6: cs_consume_r1<6>(st, smem, Fg); break;
+                        case 7: cs_consume_r1<7>(st, smem, Fg); break;
+                        case 8: cs_consume_r1<8>(st, smem, Fg); break;
+                        default: cs_consume(st, smem, Wg, Fg, R, copy, 32); break;
+                    }
+                } else {
+                    cs_consume(st, smem, Wg, Fg, R, copy, 32);
+                }
+                if (tot) {
+                    tg += st.q[lane].x;
+                    th += st.q[lane].y;
+                }
+                __syncwarp();
+            }
+            b_first = first_b + (long long)n_full * NW * 32;  // the partial tail, if any, below
+        }
+        for (long long b0 = b_first; b0 < end; b0 += NW * 32) {
             const int nrows = (int)min(32ll, end - b0);
             auto rowf = [&](int i) -> uint32_t {
                 const long long r = b0 + i;
@@ -2785,6 +2876,8 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
             }
             hp.cs_r1 = true;
             for (auto &c : hp.cgroups) hp.cs_r1 = hp.cs_r1 && c.f_hi - c.f_lo > 16;
+            // one group of whole rows: the root may fetch batches by TMA into 2 buffers per warp
+            if (hp.cgroups.size() == 1) hp.smem_bytes += (H_THREADS / 32) * (int)sizeof(CsWarp);
             GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
             GBM_CUDA(cudaFuncSetAttribute(hist_cs_range_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
@@ -2801,7 +2894,7 @@ static int plan_hist(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, bool wide
             hp.blocks_fused = o2 * ctx->sm_count;
             const long long G = (long long)hp.cgroups.size();
             long long per = (rows_hint + 2ll * hp.blocks_range - 1) / (2ll * hp.blocks_range) * G;
-            hp.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per));
+            hp.chunk = (int)std::max<long long>(256, std::min<long long>(MAX_CHUNK, per)) / 32 * 32;  // 32-row batches (TMA alignment)
             return GBM_OK;
         }
         if (allow_col && channels * rows * 32 * 4 <= budget) {
@@ -3158,6 +3251,9 @@ static int launch_root_staged(gbm_ctx *ctx, const HistPlan &hr, const QM &qm, co
     ca.ridx = nullptr;
     ca.n_sel = n;
     ca.chunk = hr.chunk;
+    // TMA bulk copies need 16-byte aligned sources (row batches are 32 rows: 16-byte multiples)
+    ca.tma = (hr.cgroups.size() == 1 && reinterpret_cast<uintptr_t>(q->packed_d) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(qpair_d) % 16 == 0 && ctx->stage_tma) ? 1 : 0;
     ca.n_groups = (int)hr.cgroups.size();
     ca.groups = cg_root;
     ca.cut_ptr = q->cut_ptr_d;
