@@ -1633,12 +1633,17 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
                                                                      int depth, long long n,
                                                                      int32_t *__restrict__ row_leaf, WalkEpi ep) {
     constexpr int PW = W | 1;
-    extern __shared__ int s_tree[];
+    extern __shared__ int2 s_node[];
     __shared__ uint32_t s_rows[WALK_THREADS / 32][32 * PW];
-    int *s_f = s_tree, *s_b = s_tree + n_internal;
+    // per internal node, one 64-bit shared load per level: x = split (sign bit) | default-left
+    // << 30 | symbol crosses a word << 29 | bit offset << 16 | word index; y = split bin
     for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
-        s_f[k] = kind[k] == GBM_NODE_SPLIT ? (feature[k] | ((int)dl[k] << 20) | (1 << 21)) : 0;
-        s_b[k] = bin[k];
+        int x = 0;
+        if (kind[k] == GBM_NODE_SPLIT) {
+            const int bp = feature[k] * qm.bits, wi = bp >> 5, off = bp & 31;
+            x = (int)(1u << 31) | ((int)dl[k] << 30) | ((off + qm.bits > 32) << 29) | (off << 16) | wi;
+        }
+        s_node[k] = make_int2(x, bin[k]);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1673,13 +1678,13 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
             const uint32_t mask = (1u << qm.bits) - 1u;
             int k = 0;
             for (int d = 0; d < depth; ++d) {
-                const int fk = s_f[k];
-                if (!(fk & (1 << 21))) break;
-                const int bp = (fk & 0xfffff) * qm.bits, wi = bp >> 5, off = bp & 31;
-                uint64_t v = row[wi];
-                if (off + qm.bits > 32) v |= (uint64_t)row[wi + 1] << 32;
-                const int sym = (int)((uint32_t)(v >> off) & mask);
-                const bool left = sym == qm.B ? ((fk >> 20) & 1) : (sym <= s_b[k]);
+                const int2 nk = s_node[k];
+                if (nk.x >= 0) break;  // leaf
+                const int wi = nk.x & 0xffff, off = (nk.x >> 16) & 31;
+                uint32_t v = row[wi] >> off;
+                if (nk.x & (1 << 29)) v |= row[wi + 1] << (32 - off);  // off > 0 here
+                const int sym = (int)(v & mask);
+                const bool left = sym == qm.B ? ((nk.x >> 30) & 1) : (sym <= nk.y);
                 k = left ? 2 * k + 1 : 2 * k + 2;
             }
             const long long r = c * 32 + lane;
