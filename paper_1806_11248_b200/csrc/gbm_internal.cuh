@@ -244,13 +244,11 @@ __device__ __forceinline__ double det_exp(double t) {
     return ldexp_exact(p, (int)k);
 }
 
+// Branch-free over the sign of x (one det_exp per lane, no divergent halves in a warp): both
+// cases of R19 take e = det_exp(-|x|); the numerator is 1 for x >= 0, e otherwise.
 __device__ __forceinline__ double sigmoid(double x) {
-    if (x >= 0.0) {
-        double e = det_exp(-x);
-        return ddiv(1.0, dadd(1.0, e));
-    }
-    double e = det_exp(x);
-    return ddiv(e, dadd(1.0, e));
+    const double e = det_exp(-fabs(x));
+    return ddiv(x >= 0.0 ? 1.0 : e, dadd(1.0, e));
 }
 
 // Eq. 1-2 (logistic, from s = sigmoid(margin)) / squared error
