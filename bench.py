@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=500_000)
     ap.add_argument("--cpu-rounds", type=int, default=3)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--row-align-bits", type=int, default=32,
+                    help="packed row stride rounded up to this many bits (gbm_compress)")
     ap.add_argument("--grow-policy", default="depthwise", choices=["depthwise", "lossguide"],
                     help="lossguide: priority-queue growth (P:65) with --max-leaves")
     ap.add_argument("--max-leaves", type=int, default=None,
@@ -171,7 +173,7 @@ def run_ours(a, world, rank, local):
     kw = dict(max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
               eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
               min_child_weight=cfg.min_child_weight, grad_bits=a.grad_bits, base_margin=beta,
-              grow_policy=a.grow_policy, max_leaves=a.leaves)
+              grow_policy=a.grow_policy, max_leaves=a.leaves, row_align_bits=a.row_align_bits)
     stream = torch.cuda.current_stream()
 
     def barrier():

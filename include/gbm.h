@@ -166,7 +166,8 @@ GBM_API int gbm_quantise(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t
 GBM_API int gbm_symbol_bits(int32_t max_symbol);
 /* packed buffer size in uint32 words for the layout of gbm_compress (R3): element (r, f)
  * starts at bit r*stride + f*bits, stride = n_features*bits rounded up to row_align_bits
- * (0, 32 or 128; 0 = SPEC's continuous stream); ceil(n*stride/32) words rounded up to a
+ * (0, 32, 128 or 256; 0 = SPEC's continuous stream; 256 = one 32-byte DRAM sector, so a
+ * gathered row of <= 32 bytes touches one sector); ceil(n*stride/32) words rounded up to a
  * multiple of 4, plus 4 zero words.  Returns a negative GBM_E_* on bad arguments. */
 GBM_API int64_t gbm_packed_words(int64_t n_rows, int32_t n_features, int32_t bits,
                          int32_t row_align_bits);
@@ -193,7 +194,7 @@ typedef struct {
     int64_t n_rows;            /* rows of this shard                                       */
     int32_t n_features;
     int32_t bits;              /* symbol width                                             */
-    int32_t row_align_bits;    /* 0, 32 or 128                                             */
+    int32_t row_align_bits;    /* 0, 32, 128 or 256                                        */
     int32_t max_bins;          /* B; the missing sentinel symbol                           */
     const float *cut_values_d; /* fp32 [TB]                                                */
     const int32_t *cut_ptr_d;  /* int32 [F+1]                                              */

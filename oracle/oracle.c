@@ -167,7 +167,7 @@ int64_t oracle_packed_words(int64_t n, int32_t F, int32_t bits, int32_t row_alig
 {
     if (n < 0 || F <= 0 || bits < 1 || bits > 16)
         return OR_E_ARG;
-    if (row_align_bits != 0 && row_align_bits != 32 && row_align_bits != 128)
+    if (row_align_bits != 0 && row_align_bits != 32 && row_align_bits != 128 && row_align_bits != 256)
         return OR_E_ARG;
     int64_t total_bits = n * row_stride_bits(F, bits, row_align_bits);
     int64_t w = (total_bits + 31) / 32;

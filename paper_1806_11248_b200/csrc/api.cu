@@ -319,8 +319,8 @@ int gbm_symbol_bits(int32_t max_symbol) {
 int64_t gbm_packed_words(int64_t n_rows, int32_t n_features, int32_t bits, int32_t row_align_bits) {
     if (n_rows < 0 || n_features <= 0 || bits < 1 || bits > 16)
         return fail(GBM_E_ARG, "gbm_packed_words: bad sizes");
-    if (row_align_bits != 0 && row_align_bits != 32 && row_align_bits != 128)
-        return fail(GBM_E_ARG, "gbm_packed_words: row_align_bits must be 0, 32 or 128");
+    if (row_align_bits != 0 && row_align_bits != 32 && row_align_bits != 128 && row_align_bits != 256)
+        return fail(GBM_E_ARG, "gbm_packed_words: row_align_bits must be 0, 32, 128 or 256");
     long long total = n_rows * row_stride_bits(n_features, bits, row_align_bits);
     long long w = (total + 31) / 32;
     w = (w + 3) / 4 * 4;

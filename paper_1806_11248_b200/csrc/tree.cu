@@ -3115,8 +3115,9 @@ static int check_qm(const gbm_qmatrix *qm) {
     GBM_REQUIRE(qm->n_features > 0 && qm->bits >= 1 && qm->bits <= 16 && qm->max_bins >= 2 &&
                     qm->max_bins <= 65535 && qm->n_rows >= 0 && qm->n_rows < (1ll << 31),
                 GBM_E_ARG, "qmatrix: bad sizes");
-    GBM_REQUIRE(qm->row_align_bits == 0 || qm->row_align_bits == 32 || qm->row_align_bits == 128, GBM_E_ARG,
-                "qmatrix: row_align_bits must be 0, 32 or 128");
+    GBM_REQUIRE(qm->row_align_bits == 0 || qm->row_align_bits == 32 || qm->row_align_bits == 128 ||
+                    qm->row_align_bits == 256, GBM_E_ARG,
+                "qmatrix: row_align_bits must be 0, 32, 128 or 256");
     return GBM_OK;
 }
 

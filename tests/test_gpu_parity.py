@@ -94,7 +94,7 @@ def test_quantise_parity(ctx, missing):
 
 
 @pytest.mark.parametrize("bits", [1, 2, 3, 4, 5, 7, 8, 9, 11, 13, 16])
-@pytest.mark.parametrize("align", [0, 32, 128])
+@pytest.mark.parametrize("align", [0, 32, 128, 256])
 def test_compress_parity(ctx, bits, align):
     rng = np.random.default_rng(bits * 7 + align)
     n, F = 3001, 13
@@ -290,6 +290,7 @@ TREE_CASES = [
     ("higgs", 100_000, 0.0, 32, 15, 3, None),
     ("higgs", 100_000, 0.0, 32, 16, 2, None),
     ("higgs", 50_000, 0.02, 128, 30, 2, None),
+    ("higgs", 40_000, 0.0, 256, 15, 2, None),   # sector-aligned rows (28 -> 32 bytes)
     ("airline", 120_000, 0.0, 32, 15, 2, None),
     ("airline", 60_000, 0.03, 0, 12, 2, None),
     ("bosch", 12_000, 0.0, 32, 15, 2, None),   # ~81% missing: 9-bit symbols, default directions

@@ -158,7 +158,7 @@ def test_pack_equals_numpy_packbits(bits):
     assert words.size % 4 == 0 and words.size >= (sym.size * bits + 31) // 32 + 4
 
 
-@pytest.mark.parametrize("align", [32, 128])
+@pytest.mark.parametrize("align", [32, 128, 256])
 def test_pack_row_alignment_is_per_row_packbits(align):
     rng = np.random.default_rng(align)
     bits, F = 9, 5
