@@ -1865,6 +1865,15 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
         const int lt = t - tile_base[j];
         if (rows_ctr && threadIdx.x == 0)
             atomicAdd(rows_ctr, (unsigned long long)min((long long)PT, nd.count - (long long)lt * PT));
+        // every load of the tile is issued before the block scan (one exposed DRAM latency)
+        const long long off = tile_off[t];
+        E rows[WPW];
+#pragma unroll
+        for (int s = 0; s < WPW; ++s) {
+            const long long pin = (long long)lt * PT + wid * (WPW * 32) + s * 32 + lane;
+            if (pin < nd.count) rows[s] = ridx_in ? ridx_in[nd.start + pin] : make_entry<CARRY>((uint32_t)(nd.start + pin), qpair);
+            else rows[s] = E{};
+        }
         // one flag word per lane (lanes >= WPW idle), warp-scan of the popcounts
         const uint32_t myw = lane < WPW ? __ldg(flags + (long long)t * (PT / 32) + wid * WPW + lane) : 0u;
         if (lane < WPW) wpre[wid * WPW + lane] = __popc(myw);
@@ -1882,15 +1891,7 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
             wpre[2 * lane + 1] = x - v + v0;
         }
         __syncthreads();
-        const long long off = tile_off[t];
         const uint32_t ltm = (1u << lane) - 1u;
-        E rows[WPW];
-#pragma unroll
-        for (int s = 0; s < WPW; ++s) {
-            const long long pin = (long long)lt * PT + wid * (WPW * 32) + s * 32 + lane;
-            if (pin < nd.count) rows[s] = ridx_in ? ridx_in[nd.start + pin] : make_entry<CARRY>((uint32_t)(nd.start + pin), qpair);
-            else rows[s] = E{};
-        }
 #pragma unroll
         for (int s = 0; s < WPW; ++s) {
             const uint32_t w = __shfl_sync(0xffffffffu, myw, s);
