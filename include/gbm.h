@@ -121,10 +121,17 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   wider or narrower than a byte, else 1 (measured).
  * GBM_OPT_TMA_ROWS: 1 (default) the staged root kernel fetches whole 32-row batches with TMA bulk
  *   copies (cp.async.bulk + mbarrier, double-buffered) when one group covers every word of a
- *   row; 0 = per-lane loads. */
+ *   row; 0 = per-lane loads.
+ * GBM_OPT_ROW_DECIDE: depth-wise levels 1..D-1 of RepartitionInstances: 2 = a row-order
+ *   pass walks every row's staged packed row down the tree built so far and writes its
+ *   go-left decision at its parent as one bit per row (n/8 bytes, L2-resident), which the fused
+ *   partition + histogram kernel then reads instead of gathering the split symbol from DRAM;
+ *   applies to rows of whole words (<= 16 words) and max_depth <= 12; 0 (default) and 1 = the
+ *   split symbol is gathered per row (measured faster: the extra streaming pass costs more than
+ *   the gathers it removes).  Same decisions either way. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
        GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
-       GBM_OPT_TMA_ROWS = 10 };
+       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

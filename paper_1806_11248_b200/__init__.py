@@ -285,7 +285,8 @@ class Context:
     # ------------------------------------------------------------ instrumentation
     PROFILE_CATEGORIES = ("grad_max", "grad_quant", "hist_root", "hist_level", "part_count", "part_scan",
                           "part_scatter", "part_final", "evaluate", "allreduce", "update_margins",
-                          "init_tree", "predict", "cuts", "quantise_compress", "eval_final", "plan")
+                          "init_tree", "predict", "cuts", "quantise_compress", "eval_final", "plan",
+                          "part_decide")
 
     def profile(self, enable: bool = True, only=None):
         """Start (reset) / stop in-library event timing; `only` = category names to record."""
@@ -319,6 +320,7 @@ class Context:
     EVAL_SCREEN = 7
     SEGMENT_HIST = 8
     TMA_ROWS = 10
+    ROW_DECIDE = 11
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

@@ -49,7 +49,7 @@ int Arena::reserve(size_t bytes) {
 const char *const PROF_NAMES[PC_N] = {
     "grad_max", "grad_quant", "hist_root", "hist_level", "part_count", "part_scan",
     "part_scatter", "part_final", "evaluate", "allreduce", "update_margins", "init_tree",
-    "predict", "cuts", "quantise_compress", "eval_final", "plan"};
+    "predict", "cuts", "quantise_compress", "eval_final", "plan", "part_decide"};
 
 // Under stream capture an event record must be an EXTERNAL event node to be timed after replays.
 static void record(cudaEvent_t e, cudaStream_t s) {
@@ -300,6 +300,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
     if (option == GBM_OPT_LEAF_WALK) {
         if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_LEAF_WALK: 0 auto, 1 feature-major copy");
         ctx->walk_mode = (int)value;
+        return GBM_OK;
+    }
+    if (option == GBM_OPT_ROW_DECIDE) {
+        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_ROW_DECIDE: 0/1 off (default), 2 on");
+        ctx->row_decide = (int)value;
         return GBM_OK;
     }
     if (option == GBM_OPT_CARRY_GRADIENTS) {

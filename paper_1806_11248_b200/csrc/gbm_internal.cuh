@@ -71,7 +71,7 @@ struct Arena {
 enum ProfCat {
     PC_GRAD_MAX = 0, PC_GRAD_QUANT, PC_HIST_ROOT, PC_HIST_LEVEL, PC_PART_COUNT, PC_PART_SCAN,
     PC_PART_SCATTER, PC_PART_FINAL, PC_EVAL, PC_ALLREDUCE, PC_MARGINS, PC_INIT, PC_PREDICT,
-    PC_CUTS, PC_QUANT, PC_EVAL_FINAL, PC_PLAN, PC_N
+    PC_CUTS, PC_QUANT, PC_EVAL_FINAL, PC_PLAN, PC_PART_DECIDE, PC_N
 };
 extern const char *const PROF_NAMES[PC_N];
 
@@ -113,6 +113,7 @@ struct gbm_ctx {
     int eval_screen = 0;           // GBM_OPT_EVAL_SCREEN (1 on, 0 every candidate exactly)
     int seg_hist = 0;              // GBM_OPT_SEGMENT_HIST (0 auto, 1 off, 2 on)
     int stage_tma = 1;             // staged root: TMA bulk row copies (GBM_OPT_TMA_ROWS)
+    int row_decide = 0;            // GBM_OPT_ROW_DECIDE (2 on; measured slower, off by default)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     // second stream of gbm_build_tree: the partition scatter of a level overlaps the allreduce
@@ -155,6 +156,7 @@ struct QM {
     int U;             // units per row = ceil(F / S)
     const uint8_t *col;  // optional feature-major symbol copy [F][n]
     long long n;         // rows (column stride of col)
+    const uint32_t *dbits = nullptr;  // optional go-left bit per row at its parent (ROW_DECIDE)
 };
 
 inline long long row_stride_bits(int F, int bits, int row_align_bits) {

@@ -411,6 +411,7 @@ __device__ __forceinline__ int2 entry_q(uint2 e, const int2 *) {
 __device__ __forceinline__ int2 entry_q(uint32_t e, const int2 *__restrict__ qpair) { return __ldg(qpair + e); }
 
 __device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint32_t row) {
+    if (qm.dbits) return (__ldg(qm.dbits + (row >> 5)) >> (row & 31)) & 1u;  // row_decide_kernel
     const uint32_t sym = split_symbol(qm, row, nd.f);
     return (int)sym == qm.B ? (nd.dl != 0) : ((int)sym <= nd.b);
 }
@@ -1717,6 +1718,78 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
             atomicMax(ep.maxbits + 0, (unsigned long long)__double_as_longlong(mg));
             atomicMax(ep.maxbits + 1, (unsigned long long)__double_as_longlong(mh));
         }
+    }
+}
+
+// Row-order decisions of one depth-wise level (GBM_OPT_ROW_DECIDE): a warp stages 32 whole rows
+// (as leaf_walk_stg_kernel), each lane walks its row from the root through the SPLIT nodes of
+// depths < par_depth to its parent at depth par_depth and applies that parent's split -- the
+// rule of goes_left on the same symbol -- and the warp writes the 32 decisions as one
+// word (bit = goes left).  Rows whose walk ends in a leaf get 0 (never read).  Streams the packed
+// rows once (coalesced) instead of gathering a 32-byte sector per row for one symbol.
+template <int W>
+__global__ void __launch_bounds__(WALK_THREADS) row_decide_kernel(QM qm, const NodeDev *__restrict__ nodes,
+                                                                  int par_depth, long long n,
+                                                                  uint32_t *__restrict__ dbits) {
+    constexpr int PW = W | 1;
+    extern __shared__ int2 s_dnode[];  // [2^(par_depth+1) - 1] as in leaf_walk_stg_kernel
+    __shared__ uint32_t s_rows[WALK_THREADS / 32][32 * PW];
+    const int n_nodes = (2 << par_depth) - 1;
+    for (int k = threadIdx.x; k < n_nodes; k += WALK_THREADS) {
+        const NodeDev nd = nodes[k];
+        int x = 0;
+        if (nd.state == GBM_NODE_SPLIT) {
+            const int bp = nd.f * qm.bits, wi = bp >> 5, off = bp & 31;
+            x = (int)(1u << 31) | ((nd.dl != 0) << 30) | ((off + qm.bits > 32) << 29) | (off << 16) | wi;
+        }
+        s_dnode[k] = make_int2(x, nd.b);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *sr = s_rows[wid];
+    const uint32_t mask = (1u << qm.bits) - 1u;
+    const long long n_chunks = (n + 31) / 32;
+    const long long cstep = (long long)gridDim.x * (WALK_THREADS / 32);
+    uint32_t v[W];
+    auto load = [&](long long c) {
+        const uint32_t *src = qm.P + c * 32 * W;
+        const long long rows_c = c < n_chunks ? min(32ll, n - c * 32) : 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int j = lane + 32 * k;
+            v[k] = j / W < rows_c ? __ldg(src + j) : 0u;
+        }
+    };
+    long long c = blockIdx.x * (long long)(WALK_THREADS / 32) + wid;
+    if (c < n_chunks) load(c);
+    for (; c < n_chunks; c += cstep) {
+        const long long rows_here = min(32ll, n - c * 32);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int j = lane + 32 * k;
+            sr[(j / W) * PW + j % W] = v[k];
+        }
+        __syncwarp();
+        load(c + cstep);
+        bool left = false;
+        if (lane < rows_here) {
+            const uint32_t *row = sr + lane * PW;
+            int k = 0;
+            for (int d = 0; d <= par_depth; ++d) {
+                const int2 nk = s_dnode[k];
+                if (nk.x >= 0) break;  // leaf: no parent at par_depth
+                const int wi = nk.x & 0xffff, off = (nk.x >> 16) & 31;
+                uint32_t x = row[wi] >> off;
+                if (nk.x & (1 << 29)) x |= row[wi + 1] << (32 - off);
+                const int sym = (int)(x & mask);
+                const bool l = sym == qm.B ? ((nk.x >> 30) & 1) : (sym <= nk.y);
+                if (d == par_depth) left = l;
+                k = l ? 2 * k + 1 : 2 * k + 2;
+            }
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, left);
+        if (lane == 0) dbits[c] = word;
+        __syncwarp();
     }
 }
 
@@ -3736,6 +3809,12 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     need += (size_t)std::max(1, 1 << std::max(0, D - 1)) * F * sizeof(FeatBest) + 512;
     need += (1 + (size_t)max_par) * sizeof(unsigned) + 256;           // eval counters
     need += ((size_t)max_par + 1) * 4 + 8 + 512;                      // segment plan
+    // row-order decisions (GBM_OPT_ROW_DECIDE): rows of whole words, <= 16 words
+    const int dW = (qm.stride % 32 == 0) ? (int)(qm.stride / 32) : 0;
+    // measured slower end to end (the extra streaming pass costs more than the gathers it
+    // removes: Higgs 2.06 vs 1.73, Airline 24.6 vs 19.9 ms/round), so only when forced
+    const bool row_decide = D > 1 && D <= 12 && dW >= 1 && dW <= 16 && ctx->row_decide == 2;
+    if (row_decide) need += (size_t)((n + 31) / 32) * 4 + 256;
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
@@ -3758,6 +3837,7 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     unsigned *done = A.take<unsigned>(1 + (size_t)max_par);  // [0] nodes completed, [1..] warps per node
     int *seg_base = A.take<int>((size_t)max_par + 1);
     int *seg_items = A.take<int>(2);
+    uint32_t *dbits = row_decide ? A.take<uint32_t>((size_t)((n + 31) / 32)) : nullptr;
 
     GBM_TRY(upload_groups(ctx, hp, groups, cgroups, A, s, root_staged ? &hr : nullptr, cg_root));
     const TreeDev t = tree_dev(tree);
@@ -3919,7 +3999,22 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
         GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
         // RepartitionInstances + BuildPartialHistograms (fused)
         GBM_CUDA(cudaMemsetAsync(hist_build, 0, (size_t)n_par * hist_unit * 8, s));
+        if (row_decide && n > 0) {  // every row's go-left bit at its parent (depth l - 1)
+            ProfScope ps(ctx, PC_PART_DECIDE, s, (double)n * (qm.stride / 8.0 + 0.125));
+            const int grid = (int)std::max<long long>(1, std::min<long long>((n + WALK_THREADS - 1) / WALK_THREADS,
+                                                                            (long long)ctx->sm_count * 8));
+            const size_t dsm = (size_t)((2 << (l - 1)) - 1) * 8;
+            switch (dW) {
+#define GBM_DECIDE(w) case w: row_decide_kernel<w><<<grid, WALK_THREADS, dsm, s>>>(qm, nodes, l - 1, n, dbits); break;
+                GBM_DECIDE(1) GBM_DECIDE(2) GBM_DECIDE(3) GBM_DECIDE(4) GBM_DECIDE(5) GBM_DECIDE(6) GBM_DECIDE(7)
+                GBM_DECIDE(8) GBM_DECIDE(9) GBM_DECIDE(10) GBM_DECIDE(11) GBM_DECIDE(12) GBM_DECIDE(13)
+                GBM_DECIDE(14) GBM_DECIDE(15) GBM_DECIDE(16)
+#undef GBM_DECIDE
+            }
+            GBM_CUDA(cudaGetLastError());
+        }
         {
+            fa.qm.dbits = dbits;
             fa.first = first;
             fa.n_par = n_par;
             fa.ridx_in = rin;
@@ -3932,6 +4027,7 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
             if (hp.col) {
                 ColFusedArgs ca = {};
                 ca.qm = qm;
+                ca.qm.dbits = dbits;
                 ca.nodes = nodes;
                 ca.first = first;
                 ca.n_par = n_par;

@@ -329,6 +329,46 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
     ctx.set_option(ctx.CARRY_GRADIENTS, 0)
 
 
+@pytest.mark.parametrize("layout", [0, 3])
+@pytest.mark.parametrize("cfg,n,missing,align,P,depth", [
+    ("tiny", 2000, 0.05, 32, 15, 5),            # 1 word per row, missing (default directions)
+    ("higgs", 70_000, 0.0, 32, 15, None),       # 7 words
+    ("higgs", 30_000, 0.02, 256, 15, None),     # 8 words (sector-aligned)
+    ("airline", 90_000, 0.03, 32, 15, None),    # depth 8, 4 words, missing
+    ("yearmsd", 20_000, 0.0, 128, 15, 4),       # 24 words: out of range -> gathered symbols
+    ("tiny", 1999, 0.0, 32, 30, 3),             # ragged last 32-row chunk, wide gradients
+])
+def test_row_decide_rounds_parity(ctx, G, cfg, n, missing, align, P, depth, layout):
+    """GBM_OPT_ROW_DECIDE = 2: RepartitionInstances from the row-order decision bits
+    equals the oracle (trees, row_leaf, margins) -- and equals the gathered-symbol path."""
+    ctx.set_option(ctx.HIST_LAYOUT, layout)
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    D = c.max_depth if depth is None else depth
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=D, grad_bits=P,
+                   row_align_bits=align, eta=0.3, reg_lambda=1.0, gamma=0.0, mcw=1.0)
+    gbs = {}
+    for mode in (2, 1):
+        ctx.set_option(ctx.ROW_DECIDE, mode)
+        gbs[mode] = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective,
+                              max_depth=D, grad_bits=P, row_align_bits=align,
+                              base_margin=ob.base_margin, eta=0.3, reg_lambda=1.0, gamma=0.0,
+                              min_child_weight=1.0)
+    try:
+        for r in range(2):
+            ot = ob.round()
+            for mode in (2, 1):
+                ctx.set_option(ctx.ROW_DECIDE, mode)
+                gb = gbs[mode]
+                gt = gb.round().to_numpy()
+                _compare_tree(gt, ot)
+                np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+                np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    finally:
+        ctx.set_option(ctx.ROW_DECIDE, 0)
+        ctx.set_option(ctx.HIST_LAYOUT, 0)
+
+
 @pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("cfg,n,missing,grow", [("airline", 60_000, 0.03, "depthwise"),
                                                 ("bosch", 12_000, 0.0, "depthwise"),
