@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--comm", action="store_true",
                     help="initialise torch.distributed + the NCCL communicator even for one rank "
                          "(exercises the N > 1 code path on one GPU)")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
+                    help="gbm_set_option before training, e.g. RUN_TILES=4 (GBM_OPT_* of include/gbm.h)")
     ap.add_argument("--max-depth", type=int, default=None,
                     help="depth limit (default: the config's; lossguide default 16)")
     a = ap.parse_args()
@@ -168,6 +170,9 @@ def run_ours(a, world, rank, local):
             dist.all_reduce(s)
         beta = float(s[0] / s[1])
     ctx = G.Context(local)
+    for o in a.opt:
+        name, val = o.split("=", 1)
+        ctx.set_option(getattr(G.Context, name), int(val))
     if a.dist:
         ctx.comm_init_from_torch()
     kw = dict(max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
@@ -449,9 +454,10 @@ def metric_of(a):
 
 
 def policy_keys(a):
-    if a.grow_policy == "lossguide":
-        return {"grow_policy": "lossguide", "max_leaves": a.leaves}
-    return {}
+    keys = {"grow_policy": "lossguide", "max_leaves": a.leaves} if a.grow_policy == "lossguide" else {}
+    if a.opt:
+        keys["options"] = dict(o.split("=", 1) for o in a.opt)
+    return keys
 
 
 def main():
