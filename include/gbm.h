@@ -101,7 +101,8 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   the size + compact levels.
  * GBM_OPT_CARRY_GRADIENTS: 0 (default) level passes gather qpair by row; 1 the row-index
  *   entries of every level carry the row's gradient pair (grad_bits <= 15; 8-byte entries).
- * GBM_OPT_RUN_TILES: 2048-row tiles per work item of the fused level kernel (0 = auto).
+ * GBM_OPT_RUN_TILES: 2048-row tiles per work item of the fused level kernel (0 = auto, 1..31:
+ *   one int32 shared-memory flush per item must stay within 65535 rows).
  * GBM_OPT_GROUP_UNITS: at most this many packed units (S features each) per shared-memory
  *   feature group of the compact layout (0 = auto = 32; 1..32).  Smaller groups mean less
  *   shared memory per block (more resident blocks) but more passes over the row list.

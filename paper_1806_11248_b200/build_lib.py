@@ -35,16 +35,40 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object in parallel (objects cached by mtime under
+    build/), then link libgbm.so."""
     if not force and not stale():
         return LIB
     inc, libdir = nccl_dirs()
+    obj_dir = os.path.join(HERE, "build")
+    os.makedirs(obj_dir, exist_ok=True)
+    flags = [nvcc(), "-std=c++17", "-O3", "-lineinfo", "--fmad=false",
+             "-gencode", "arch=compute_100a,code=sm_100a",
+             "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-I", inc]
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
+    procs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        srcp = os.path.join(CSRC, src)
+        if (not force and os.path.exists(obj) and
+                os.path.getmtime(obj) > max(os.path.getmtime(srcp), hdr_t)):
+            continue
+        cmd = flags + ["-c", srcp, "-o", obj + f".tmp{os.getpid()}"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd, cwd=CSRC), obj))
+    failed = False
+    for p, obj in procs:
+        if p.wait() != 0:
+            failed = True
+        else:
+            os.replace(obj + f".tmp{os.getpid()}", obj)
+    if failed:
+        raise subprocess.CalledProcessError(1, "nvcc")
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), "-std=c++17", "-O3", "-lineinfo", "--fmad=false",
-           "-gencode", "arch=compute_100a,code=sm_100a",
-           "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-           "-shared", "-I", inc, "-o", tmp]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
-    cmd += ["-L", libdir, "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}"]
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs
+    cmd += ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd, cwd=CSRC)

@@ -270,7 +270,9 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         return GBM_OK;
     }
     if (option == GBM_OPT_RUN_TILES) {
-        if (value < 0 || value > 64) return fail(GBM_E_ARG, "GBM_OPT_RUN_TILES: 0 (auto) .. 64");
+        // a work item flushes its int32 shared histogram once: <= MAX_CHUNK (65535) rows per item
+        // keeps every bin sum exact (tree.cu header), so at most 31 tiles of 2048 rows
+        if (value < 0 || value > 31) return fail(GBM_E_ARG, "GBM_OPT_RUN_TILES: 0 (auto) .. 31");
         ctx->run_tiles = (int)value;
         return GBM_OK;
     }

@@ -3324,7 +3324,7 @@ static bool plan_root_staged(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, c
 
 static int launch_root_staged(gbm_ctx *ctx, const HistPlan &hr, const QM &qm, const gbm_qmatrix *q,
                               const int32_t *qpair_d, const ColGroup *cg_root, long long *hist_root,
-                              size_t hist_unit, long long n, double row_bytes, cudaStream_t s) {
+                              long long *totals, long long n, double row_bytes, cudaStream_t s) {
     ColRangeArgs ca = {};
     ca.qm = qm;
     ca.qpair = reinterpret_cast<const int2 *>(qpair_d);
@@ -3338,7 +3338,7 @@ static int launch_root_staged(gbm_ctx *ctx, const HistPlan &hr, const QM &qm, co
     ca.groups = cg_root;
     ca.cut_ptr = q->cut_ptr_d;
     ca.hist = reinterpret_cast<unsigned long long *>(hist_root);
-    ca.totals = reinterpret_cast<unsigned long long *>(hist_root + hist_unit);
+    ca.totals = reinterpret_cast<unsigned long long *>(totals);
     ca.cstride = hr.cstride;
     int slot = -1;
     ca.rows_ctr = prof_rows_slot(ctx, &slot);
@@ -3419,7 +3419,7 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     // ---- InitRoot
     GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
     if (n > 0 && TB > 0 && root_staged) {
-        GBM_TRY(launch_root_staged(ctx, hr, qm, q, qpair_d, cg_root, hist_root, hist_unit, n, row_bytes, s));
+        GBM_TRY(launch_root_staged(ctx, hr, qm, q, qpair_d, cg_root, hist_root, hist_root + hist_unit, n, row_bytes, s));
     } else if (n > 0 && TB > 0) {
         RangeArgs ra = {};
         ra.qm = qm;
@@ -3589,9 +3589,23 @@ int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair
     const QM qm = make_qm(q);
     const int TB = q->cut_ptr_h[q->n_features];
     HistPlan hp;
-    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp, grad_bits, ctx->hist_layout >= 2, ctx->hist_layout == 3));
+    // layouts 2 / 3 force the column levels; 4 = staged root + compact levels
+    GBM_TRY(plan_hist(ctx, q, qm, grad_bits > 15, n_sel, hp, grad_bits,
+                      ctx->hist_layout == 2 || ctx->hist_layout == 3, ctx->hist_layout == 3));
     GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)std::max(TB, 1) * 2 * 8, s));
     if (n_sel == 0 || TB == 0) return GBM_OK;
+    HistPlan hr;
+    if (!rows_d && plan_root_staged(ctx, q, qm, hp, grad_bits, n_sel, hr)) {
+        // the staged bank-column root of gbm_build_tree (hist_cs_range / hist_csg_range), so it can
+        // be compared bin for bin with the oracle
+        GBM_TRY(ctx->arena.reserve(hr.cgroups.size() * sizeof(ColGroup) + 512));
+        ColGroup *cgs = ctx->arena.take<ColGroup>(hr.cgroups.size());
+        long long *tot = ctx->arena.take<long long>(2);
+        GBM_CUDA(cudaMemcpyAsync(cgs, hr.cgroups.data(), hr.cgroups.size() * sizeof(ColGroup), cudaMemcpyHostToDevice, s));
+        GBM_CUDA(cudaMemsetAsync(tot, 0, 16, s));
+        return launch_root_staged(ctx, hr, qm, q, qpair_d, cgs, reinterpret_cast<long long *>(hist_d), tot, n_sel,
+                                  (double)q->n_features * q->bits / 8.0, s);
+    }
     if (hp.col) {
         GBM_TRY(ctx->arena.reserve(hp.cgroups.size() * sizeof(ColGroup) + 256));
         ColGroup *cgs = ctx->arena.take<ColGroup>(hp.cgroups.size());
@@ -3784,7 +3798,7 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     const long long cap = (1ll << (D + 1)) - 1;
     HistPlan hp;
     GBM_TRY(plan_hist(ctx, q, qm, prm->grad_bits > 15, std::max<long long>(n, 1), hp, prm->grad_bits,
-                      ctx->hist_layout >= 2, ctx->hist_layout == 3));
+                      ctx->hist_layout == 2 || ctx->hist_layout == 3, ctx->hist_layout == 3));
     const int G = hp.col ? (int)hp.cgroups.size() : (int)hp.groups.size();
     const size_t esz = hp.carry ? 8 : 4;  // bytes per level entry
     HistPlan hr;
@@ -3850,7 +3864,7 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     // ---- InitRoot: root histogram + totals, allreduce, evaluate
     GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
     if (n > 0 && TB > 0 && root_staged) {
-        GBM_TRY(launch_root_staged(ctx, hr, qm, q, qpair_d, cg_root, hist_root, hist_unit, n, row_bytes, s));
+        GBM_TRY(launch_root_staged(ctx, hr, qm, q, qpair_d, cg_root, hist_root, hist_root + hist_unit, n, row_bytes, s));
     } else if (n > 0 && TB > 0 && hp.col) {
         ColRangeArgs ca = {};
         ca.qm = qm;

@@ -329,6 +329,32 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
     ctx.set_option(ctx.CARRY_GRADIENTS, 0)
 
 
+@pytest.mark.parametrize("run_tiles", [2, 5, 8, 31])
+@pytest.mark.parametrize("cfg,n,missing,P", [("higgs", 300_000, 0.0, 15), ("airline", 250_000, 0.0, 15),
+                                             ("higgs", 200_000, 0.0, 30), ("bosch", 40_000, 0.0, 15)])
+def test_run_tiles_rounds_parity(ctx, G, cfg, n, missing, P, run_tiles):
+    """Work items of several 2048-row tiles (the auto value at 11M rows is 5): many items per
+    parent, items straddling parents, and the 31-tile maximum (one flush per <= 63488 rows)."""
+    ctx.set_option(ctx.RUN_TILES, run_tiles)
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, missing=missing)
+    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth, grad_bits=P)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth,
+                   grad_bits=P, base_margin=ob.base_margin)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.RUN_TILES, 0)
+
+
+def test_run_tiles_option_bounds(ctx, G):
+    with pytest.raises(G.GbmError):
+        ctx.set_option(ctx.RUN_TILES, 32)
+    ctx.set_option(ctx.RUN_TILES, 31)
+    ctx.set_option(ctx.RUN_TILES, 0)
+
+
 @pytest.mark.parametrize("layout", [0, 3])
 @pytest.mark.parametrize("cfg,n,missing,align,P,depth", [
     ("tiny", 2000, 0.05, 32, 15, 5),            # 1 word per row, missing (default directions)
@@ -478,9 +504,26 @@ def test_staged_root_parity(ctx, G, cfg, n, missing, align, P):
                    row_align_bits=align)
     gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth,
                    grad_bits=P, row_align_bits=align, base_margin=ob.base_margin)
+    staged = align % 32 == 0  # word-aligned rows: the staged kernels apply (else the compact root)
     for _ in range(2):
+        ctx.profile(True, only=("hist_root", "hist_level"))
         _compare_tree(gb.round().to_numpy(), ob.round())
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        if staged:  # the staged root kernel is the one that ran (it books under hist_root)
+            assert prof["hist_root"]["launches"] >= 1
         np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    # the root histogram itself, bin for bin (gbm_build_histogram takes the same staged kernel)
+    qm, v, p, s, bits, words = _qm_from_oracle(G, X, c.max_bins, align)
+    _, _, q, _ = O.gradients(c.objective, np.zeros(n), y, P)
+    ref = O.node_histogram(words, X.shape[1], bits, align, p, qm.max_bins, q, np.arange(n))
+    ctx.profile(True, only=("hist_root", "hist_level"))
+    got = ctx.build_histogram(qm, dev(q), P)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    if staged:
+        assert prof["hist_root"]["launches"] == 1 and prof["hist_level"]["launches"] == 0
     ctx.set_option(ctx.HIST_LAYOUT, 0)
 
 
