@@ -129,10 +129,18 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   partition + histogram kernel then reads instead of gathering the split symbol from DRAM;
  *   applies to rows of whole words (<= 16 words) and max_depth <= 12; 0 (default) and 1 = the
  *   split symbol is gathered per row (measured faster: the extra streaming pass costs more than
- *   the gathers it removes).  Same decisions either way. */
+ *   the gathers it removes).  Same decisions either way.
+ * GBM_OPT_LEVEL_PATH: depth-wise levels 1..D-1.  2 = records: every level streams its
+ *   parents' rows (packed row words + gradient pair, grouped by node; level 1 reads the packed
+ *   matrix and qpair) by TMA bulk copies, decides each row's side from the staged split symbol,
+ *   accumulates the smaller child into a conflict-free shared histogram, and moves every row into
+ *   its child's segment of a second buffer (2 x n x (row bytes + 8) of scratch); applies to
+ *   8-bit symbols, <= 32 features, rows of whole words.  1 = row-index lists (partition flags +
+ *   scan + scatter of row ids; packed rows and qpair gathered per level).  0 (default) = 1
+ *   (measured faster end to end).  Same trees either way. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
        GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
-       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11 };
+       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

@@ -321,6 +321,7 @@ class Context:
     SEGMENT_HIST = 8
     TMA_ROWS = 10
     ROW_DECIDE = 11
+    LEVEL_PATH = 12
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

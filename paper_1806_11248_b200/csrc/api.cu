@@ -304,6 +304,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->walk_mode = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_LEVEL_PATH) {
+        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_LEVEL_PATH: 0 auto, 1 row-index lists, 2 records");
+        ctx->level_path = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_ROW_DECIDE) {
         if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_ROW_DECIDE: 0/1 off (default), 2 on");
         ctx->row_decide = (int)value;

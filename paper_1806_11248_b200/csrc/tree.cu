@@ -29,18 +29,9 @@
 #include <climits>
 #include <vector>
 
-#include "gbm_internal.cuh"
+#include "tree_common.cuh"
 
 namespace gbm {
-
-struct NodeDev {
-    long long Tg, Th;        // node totals over all ranks (fixed point)
-    long long start, count;  // this rank's segment in the level's ridx buffer
-    int state;               // GBM_NODE_ABSENT / SPLIT / LEAF
-    int f, b, dl;            // split (state == SPLIT)
-    int build_left;          // which child's histogram is built at the next level
-    int pad;
-};
 
 // Loss-guided growth (R25-R27).  A node evaluated with a positive-gain split that may still be
 // expanded is OPEN until the step kernel selects it (then SPLIT) -- internal state only.
@@ -88,29 +79,7 @@ struct NodeKnown {
     long long Tg, Th;
 };
 
-constexpr int PT = 2048;         // partition tile (rows): 16 warps x 128 rows
-constexpr int WROWS = PT / 16;   // rows per warp per tile
-constexpr int P_THREADS = 256;   // partition kernels: 8 warps x 4 ballot words
-constexpr int H_THREADS = 512;   // histogram / fused kernels
-#ifndef GBM_PH_UNR
-#define GBM_PH_UNR 4
-#endif
-#ifndef GBM_PH_MINB
-#define GBM_PH_MINB 3
-#endif
-#ifndef GBM_HR_MINB  // root histogram kernel: 2 resident blocks (Bosch root 1.65 vs 1.86 ms at 3)
-#define GBM_HR_MINB 2
-#endif
-constexpr int PH_UNR = GBM_PH_UNR;    // rows in flight per lane in the fused level kernel's byte path
-// resident blocks the fused level kernel is compiled for: the byte path runs best with the
-// register room of 2 blocks (Higgs 1.86 vs 1.97 ms/round, Epsilon 5.09 vs 5.18), the generic path
-// with the occupancy of 3 (Bosch 4.73 vs 5.04)
-constexpr int PH_MINB = GBM_PH_MINB;
-constexpr int PH_MINB_BYTE = 2;
-constexpr int RUN_MAX = 16;      // tiles per fused work item: chosen per tree (flush amortisation
-                                 // vs. enough items for every resident block)
 constexpr int E_THREADS = 256;   // evaluation kernels
-constexpr int MAX_CHUNK = 65535; // rows per flush (exactness bound above)
 constexpr int DUMMY_BINS = 32;   // scratch bins: padding features of the byte path (symbol 0)
 
 struct EvalParams {
@@ -376,16 +345,6 @@ __global__ void __launch_bounds__(H_THREADS, GBM_HR_MINB) hist_range_kernel(Rang
 }
 
 // ============================================================== partition helpers
-__device__ __forceinline__ int find_parent(const int *__restrict__ tile_base, int n_par, int t) {
-    int lo = 0, hi = n_par - 1;  // largest j with tile_base[j] <= t
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(tile_base + mid) <= t) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
 // Row-index entries of the level buffers.  CARRY (grad_bits <= 15): the row's fixed-point
 // gradient pair travels with its index through every partition, so no level pass gathers qpair
 // (a 64-byte DRAM access per 8-byte pair).  q_g in [-2^15, 2^15] needs 17 bits, q_h in
@@ -422,7 +381,8 @@ __device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint3
 // kernel is run i / G, group i % G, resolved on the fly (find_parent over run_base).
 // Works for any block size that is a multiple of 32 (<= 1024).
 __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_par, int n_groups, int run_tiles,
-                           int *__restrict__ tile_base, int *__restrict__ run_base, int *__restrict__ n_items) {
+                           int *__restrict__ tile_base, int *__restrict__ run_base, int *__restrict__ n_items,
+                           bool split_only = false) {
     __shared__ long long sm32[32];
     __shared__ long long carry;
     if (threadIdx.x == 0) carry = 0;
@@ -433,7 +393,7 @@ __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_p
         long long nt = 0, nr = 0;
         if (j < n_par) {
             const NodeDev nd = nodes[first + j];
-            if (nd.state != GBM_NODE_ABSENT && nd.count > 0) {
+            if (nd.count > 0 && (split_only ? nd.state == GBM_NODE_SPLIT : nd.state != GBM_NODE_ABSENT)) {
                 nt = (nd.count + PT - 1) / PT;
                 nr = (nt + run_tiles - 1) / run_tiles;
             }
@@ -470,15 +430,6 @@ __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_p
         n_items[0] = (int)(carry & 0xffffffff) * n_groups;
         n_items[1] = 0;  // dynamic work counter of the fused kernel
     }
-}
-
-// Dynamic work distribution: the block claims the next item from counter[0]; n_items[0] items.
-__device__ __forceinline__ int claim_item(int *counter) {
-    __shared__ int s_item;
-    __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
-    __syncthreads();
-    return s_item;
 }
 
 __global__ void __launch_bounds__(1024) plan_kernel(const NodeDev *__restrict__ nodes, int first, int n_par,
@@ -792,26 +743,8 @@ __global__ void __launch_bounds__(H_THREADS, GBM_HR_MINB) hist_seg_kernel(SegArg
 // a feature-major source staged by TMA to pay off.
 // A group holds Fg <= 32 features; a warp processes R = 32/Fg rows per step: lane = copy*Fg +
 // feature, the R copies of a feature live in different columns and are merged by the flush.
-struct ColGroup {
-    int f_lo, f_hi;  // features [f_lo, f_hi), Fg <= 32
-};
-
 // byte symbols: every feature has <= 256 bins, the channel stride is the constant 256*32 words
-constexpr int COLB_STRIDE = 256 * 32;
 constexpr int COLB_UR = 4;   // rows in flight per lane in the byte column kernels (16 measured slower)
-template <bool WIDE>
-__device__ __forceinline__ void col_add_b(int *hs, int word, int2 q) {
-    if (WIDE) {
-        atomicAdd(hs + word, q.x & 0x7fff);
-        atomicAdd(hs + COLB_STRIDE + word, q.y & 0x7fff);
-        atomicAdd(hs + 2 * COLB_STRIDE + word, q.x >> 15);
-        atomicAdd(hs + 3 * COLB_STRIDE + word, q.y >> 15);
-    } else {
-        atomicAdd(hs + word, q.x);
-        atomicAdd(hs + COLB_STRIDE + word, q.y);
-    }
-}
-
 template <bool WIDE>
 __device__ __forceinline__ void col_add(int *hs, int cstride, int word, int2 q) {
     if (WIDE) {
@@ -822,29 +755,6 @@ __device__ __forceinline__ void col_add(int *hs, int cstride, int word, int2 q) 
     } else {
         atomicAdd(hs + word, q.x);
         atomicAdd(hs + cstride + word, q.y);
-    }
-}
-
-template <bool WIDE>
-__device__ void col_flush(const int *hs, int cstride, const ColGroup &cg, const int32_t *__restrict__ cut_ptr,
-                          unsigned long long *dst /* slot base */) {
-    const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
-    for (int w = threadIdx.x; w < cstride; w += blockDim.x) {
-        const int b = w >> 5, col = w & 31;
-        if (col >= R * Fg) continue;
-        const int f = cg.f_lo + col % Fg;
-        const int c0 = __ldg(cut_ptr + f);
-        if (b >= __ldg(cut_ptr + f + 1) - c0) continue;
-        long long G, H;
-        if (WIDE) {
-            G = (long long)hs[2 * cstride + w] * 32768 + (long long)(unsigned)hs[w];
-            H = (long long)hs[3 * cstride + w] * 32768 + (long long)(unsigned)hs[cstride + w];
-        } else {
-            G = hs[w];
-            H = hs[cstride + w];
-        }
-        if (G) atomicAdd(dst + 2ll * (c0 + b), (unsigned long long)G);
-        if (H) atomicAdd(dst + 2ll * (c0 + b) + 1, (unsigned long long)H);
     }
 }
 
@@ -1108,31 +1018,6 @@ __device__ __forceinline__ void cs_batch_any(const QM &qm, CsWarp &st, int *hs, 
     }
     cs_batch(qm, st, hs, u_lo, Wg, Fg, R, copy, nrows, rowf, qf);
 }
-
-// ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier)
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // R1: every group has more than 16 features (one row per warp instruction, compile-time row
 // pitch); a separate instantiation so the other path's code generation is not affected
@@ -2360,6 +2245,7 @@ struct EvalArgs {
     int sel_step;
     int *tile_left;                 // loss-guided: zeroed for the popped node's tiles
     int plan_groups, plan_run;
+    int plan_split_only;            // record level path: items only for split parents
     int plan_run_min;               // loss-guided: smallest work item (tiles)
     int *tile_base, *run_base, *n_items;
     long long TB;
@@ -2560,7 +2446,8 @@ __device__ void eval_finish(const EvalArgs &a, const TreeDev &t, const int *fin,
     if (!s_last) return;
     __threadfence();
     if (a.plan_mode == 1)  // the children of this level are the next level's parents
-        plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.plan_run, a.tile_base, a.run_base, a.n_items);
+        plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.plan_run, a.tile_base, a.run_base, a.n_items,
+                   a.plan_split_only != 0);
     else if (a.plan_mode == 2)
         lg_select_block(a, t, a.sel_step);
     if (threadIdx.x == 0) *a.done = 0;
@@ -3829,9 +3716,37 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     // removes: Higgs 2.06 vs 1.73, Airline 24.6 vs 19.9 ms/round), so only when forced
     const bool row_decide = D > 1 && D <= 12 && dW >= 1 && dW <= 16 && ctx->row_decide == 2;
     if (row_decide) need += (size_t)((n + 31) / 32) * 4 + 256;
+    // records level path (records.cu): 8-bit symbols, <= 32 features, rows of whole words
+    const int RW = (qm.stride % 32 == 0) ? (int)(qm.stride / 32) : 0;
+    const bool rec_ok = D >= 2 && q->bits == 8 && F <= 32 && RW >= 1 && RW <= 8 && !row_decide;
+    // measured slower than the row-index path in the whole round on Higgs (2.17-2.25 vs 1.83 ms/round:
+    // twice the DRAM bytes per level, the block-wide reservation), so only when forced
+    const bool rec = rec_ok && ctx->level_path == 2;
+    const int RWP = rec ? rec_row_words(RW) : 0;
+    const size_t rec_rows_bytes = (size_t)std::max<long long>(n, 1) * RWP * 4 + 64;
+    const size_t rec_q_bytes = (size_t)std::max<long long>(n, 1) * 8 + 64;
+    if (rec) {
+        need -= 2 * (size_t)std::max<long long>(n, 1) * 8;                  // no ridx lists
+        need += 2 * (rec_rows_bytes + 256) + 2 * (rec_q_bytes + 256);       // two record buffers
+        need += (size_t)(2 * cap + 2) * 2 * 8 + 256;                        // cursors
+    }
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
-    char *ridx[2] = {A.take<char>(std::max<long long>(n, 1) * esz), A.take<char>(std::max<long long>(n, 1) * esz)};
+    char *ridx[2] = {nullptr, nullptr};
+    if (!rec) {
+        ridx[0] = A.take<char>(std::max<long long>(n, 1) * esz);
+        ridx[1] = A.take<char>(std::max<long long>(n, 1) * esz);
+    }
+    uint32_t *rec_rows[2] = {nullptr, nullptr};
+    int2 *rec_q[2] = {nullptr, nullptr};
+    unsigned long long *cursor = nullptr;
+    if (rec) {
+        for (int b = 0; b < 2; ++b) {
+            rec_rows[b] = reinterpret_cast<uint32_t *>(A.take<char>(rec_rows_bytes));
+            rec_q[b] = reinterpret_cast<int2 *>(A.take<char>(rec_q_bytes));
+        }
+        cursor = A.take<unsigned long long>((size_t)(2 * cap + 2) * 2);
+    }
     uint32_t *flags = A.take<uint32_t>((size_t)max_tiles * (PT / 32));
     int *tile_left = A.take<int>(max_tiles);
     int *tile_off = A.take<int>(max_tiles);
@@ -3859,6 +3774,10 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     {
         ProfScope ps(ctx, PC_INIT, s);
         init_tree_kernel<<<(int)std::min<long long>((cap + 255) / 256, 1024), 256, 0, s>>>(t, cap, nodes, n);
+    }
+    if (rec) {
+        ProfScope ps(ctx, PC_INIT, s);
+        GBM_TRY(rec_root_launch(ctx, cursor, n, s));
     }
 
     // ---- InitRoot: root histogram + totals, allreduce, evaluate
@@ -3928,8 +3847,9 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     const long long target = 4ll * hp.blocks_fused;
     const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
         1, std::min<long long>(RUN_MAX, (tiles_all * Gf + target - 1) / target));
-    ea.plan_groups = Gf;
-    ea.plan_run = run_tiles;
+    ea.plan_groups = rec ? 1 : Gf;
+    ea.plan_run = rec ? 1 : run_tiles;  // records: items of one 2048-row tile, split parents only
+    ea.plan_split_only = rec ? 1 : 0;
     ea.tile_base = tile_base_b[1];  // the root's evaluation plans level 1
     ea.run_base = run_base_b[1];
     ea.n_items = n_items_b[1];
@@ -4009,6 +3929,70 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
             }
             GBM_CUDA(cudaGetLastError());
             break;
+        }
+        if (rec) {  // records: partition + smaller-child histogram in one streaming pass
+            GBM_CUDA(cudaMemsetAsync(hist_build, 0, (size_t)n_par * hist_unit * 8, s));
+            RecLaunch L = {};
+            L.nodes = nodes;
+            L.first = first;
+            L.n_par = n_par;
+            L.tile_base = tile_base;
+            L.items_hint = (int)std::min<long long>(INT_MAX, tiles_all + n_par);
+            if (l == 1) {  // the canonical packed matrix and qpair, identity positions
+                L.in_rows = q->packed_d;
+                L.in_q = reinterpret_cast<const int2 *>(qpair_d);
+                L.in_rows_bytes = (unsigned long long)gbm_packed_words(n, F, q->bits, q->row_align_bits) * 4;
+                L.in_q_bytes = (unsigned long long)n * 8;
+            } else {
+                L.in_rows = rec_rows[(l - 1) & 1];
+                L.in_q = rec_q[(l - 1) & 1];
+                L.in_rows_bytes = rec_rows_bytes;
+                L.in_q_bytes = rec_q_bytes;
+            }
+            const bool out = l < D - 1;  // the last histogram level moves no rows (the walk follows)
+            L.out_rows = out ? rec_rows[l & 1] : nullptr;
+            L.out_q = out ? rec_q[l & 1] : nullptr;
+            L.cursor = cursor;
+            L.cut_ptr = q->cut_ptr_d;
+            L.F = F;
+            L.B = q->max_bins;
+            L.RW = RW;
+            L.RW_in = l == 1 ? RW : RWP;
+            L.wide = prm->grad_bits > 15;
+            L.hist = reinterpret_cast<unsigned long long *>(hist_build);
+            L.TB = std::max<long long>(TB, 1);
+            int slot;
+            L.rows_ctr = prof_rows_slot(ctx, &slot);
+            // algorithmic bits: per parent row the split symbol + a row-index read
+            // and write (b + 64), per row of the built child the packed row + qpair + row index
+            L.bits_parent_row = q->bits + 64;
+            L.bits_built_row = F * q->bits + 96;
+            {
+                ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
+                GBM_TRY(rec_level_launch(ctx, L, s));
+            }
+            if (out) {  // the children's segments (the next level's plan reads their counts)
+                ProfScope ps(ctx, PC_PART_SCAN, s);
+                GBM_TRY(rec_seg_launch(ctx, nodes, first, n_par, cursor, s));
+            }
+            {
+                ProfScope ps(ctx, PC_ALLREDUCE, s, (double)n_par * hist_unit * 8);
+                GBM_TRY(allreduce_i64(ctx, hist_build, (size_t)n_par * hist_unit, s));
+            }
+            ea.level = l;
+            ea.first = (1 << l) - 1;
+            ea.n_nodes = 1 << l;
+            ea.hist_prev = l == 1 ? nullptr : hist_lvl[(l - 1) & 1];
+            ea.hist_store = (l < D - 1) ? hist_lvl[l & 1] : nullptr;
+            ea.plan_mode = (l + 1 < D) ? 1 : 0;
+            ea.tile_base = tile_base_b[(l + 1) & 1];
+            ea.run_base = run_base_b[(l + 1) & 1];
+            ea.n_items = n_items_b[(l + 1) & 1];
+            {
+                ProfScope ps(ctx, PC_EVAL, s, (double)n_par * hist_unit * 8 * (2.0 + (ea.hist_store ? 2.0 : 0.0)));
+                GBM_TRY(launch_eval_tree(ctx, ea, t, s));
+            }
+            continue;
         }
         GBM_CUDA(cudaMemsetAsync(tile_left, 0, sizeof(int) * (size_t)max_tiles, s));
         // RepartitionInstances + BuildPartialHistograms (fused)

@@ -329,6 +329,41 @@ def test_training_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, depth
     ctx.set_option(ctx.CARRY_GRADIENTS, 0)
 
 
+REC_CASES = [
+    # cfg, rows, missing, align, P, max_bins override, depth override
+    ("higgs", 100_000, 0.0, 32, 15, None, None),
+    ("higgs", 70_001, 0.0, 32, 30, None, None),       # wide accumulators (4 channels)
+    ("higgs", 50_000, 0.02, 32, 15, 200, None),       # 8-bit symbols with the sentinel (200)
+    ("higgs", 40_000, 0.0, 256, 15, None, 9),         # 32-byte rows, 256 parents at the last level
+    ("airline", 120_000, 0.0, 32, 15, None, None),    # 13 features: two rows per warp step
+    ("airline", 30_000, 0.03, 128, 20, None, 4),
+    ("tiny", 2000, 0.0, 32, 15, 256, 5),              # 8 features, 8-bit symbols: four rows per step
+    ("epsilon", 3000, 0.0, 32, 15, None, 3),          # > 32 features: falls back to row-index lists
+]
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("cfg,n,missing,align,P,B,depth", REC_CASES)
+def test_record_levels_parity(ctx, G, cfg, n, missing, align, P, B, depth, path):
+    """GBM_OPT_LEVEL_PATH 2 (records: rows moved into node-grouped buffers, TMA-staged, bank-column
+    histograms) against 1 (row-index lists), both against the oracle, every tree field, the row
+    partition and the margins bit for bit."""
+    ctx.set_option(ctx.LEVEL_PATH, path)
+    c = W.CONFIGS[cfg]
+    B = B or c.max_bins
+    D = depth or c.max_depth
+    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
+    ob = O.Booster(X, y, max_bins=B, objective=c.objective, max_depth=D, grad_bits=P, row_align_bits=align,
+                   eta=0.3)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=B, objective=c.objective, max_depth=D, grad_bits=P,
+                   row_align_bits=align, base_margin=ob.base_margin, eta=0.3)
+    for _ in range(3):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.LEVEL_PATH, 0)
+
+
 @pytest.mark.parametrize("run_tiles", [2, 5, 8, 31])
 @pytest.mark.parametrize("cfg,n,missing,P", [("higgs", 300_000, 0.0, 15), ("airline", 250_000, 0.0, 15),
                                              ("higgs", 200_000, 0.0, 30), ("bosch", 40_000, 0.0, 15)])
