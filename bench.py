@@ -49,8 +49,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
-    ap.add_argument("--cpu-rows", type=int, default=500_000)
-    ap.add_argument("--cpu-rounds", type=int, default=3)
+    ap.add_argument("--cpu-rounds", type=int, default=3,
+                    help="oracle rounds of the cpu_baseline / parity leg (full rows, threaded)")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0 = the host's cores)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size oracle parity leg")
+    ap.add_argument("--no-p30", action="store_true", help="skip the grad_bits = 30 figure")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--row-align-bits", type=int, default=32,
                     help="packed row stride rounded up to this many bits (gbm_compress)")
@@ -335,6 +338,7 @@ def run_ours(a, world, rank, local):
     p1.record(stream)
     torch.cuda.synchronize()
     predict_ms = max_over_ranks(p0.elapsed_time(p1))
+    Xd_keep, yd_keep = Xd, yd
     del booster, Xd, yd, flush_buf
     torch.cuda.empty_cache()
 
@@ -378,69 +382,166 @@ def run_ours(a, world, rank, local):
                        "amortised per round"}
         del b2, Xd, yd, g2
 
-    # ---- CPU baseline: the oracle as it stands, on a bounded sample (rank 0, N=1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(a.config, min(a.cpu_rows, n), a.cpu_rounds, n, a)
-    return dict(ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages, l2=l2_note,
+    # ---- grad_bits = 30 (SURVEY §8(c) Q4's s = 30 - E): the same timed graph protocol
+    p30 = None
+    if not a.no_p30 and a.grad_bits != 30 and a.grow_policy == "depthwise":
+        p30 = time_precision(G, ctx, torch, dev, Xd_keep, yd_keep, kw, a, stream, barrier, max_over_ranks, 30)
+    del Xd_keep, yd_keep
+    torch.cuda.empty_cache()
+    # ---- CPU baseline + full-size parity: the oracle (threaded, as it stands) on the full rows
+    # of this rank's workload for R rounds, the GPU's first R rounds compared with it (rank 0, N=1)
+    cpu = parity = None
+    if rank == 0 and world == 1 and not (a.no_cpu_baseline and a.no_parity):
+        cpu, parity = cpu_baseline_and_parity(G, ctx, torch, dev, X, y, kw, a)
+    return dict(p30=p30, parity=parity, ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages, l2=l2_note,
                 one_time=one_time, clocks=clk, launches=launches, e2e=e2e, cpu=cpu,
                 predict_ms=predict_ms, allreduce_ms=allreduce_ms, grad_bits=a.grad_bits)
 
 
-def cpu_baseline(config, rows, rounds, n_full, a):
+def host_facts():
+    """Cores this process may use and the CPU model (record nproc and lscpu)."""
+    nproc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return nproc, model
+
+
+def time_precision(G, ctx, torch, dev, Xd, yd, kw, a, stream, barrier, max_over_ranks, bits):
+    """ms per round at another grad_bits (same data, cuts, graph-replay protocol as the line)."""
+    kw2 = dict(kw, grad_bits=bits)
+    b = G.Booster(ctx, Xd, yd, **kw2)
+    for _ in range(a.warmup):
+        b.round(keep_tree=False)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        b.round(keep_tree=False)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        b.round(keep_tree=False)
+    for _ in range(3):
+        g.replay()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        g.replay()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / a.steps)
+    del g, b
+    return {"grad_bits": bits, "ms_per_step": ms, "value": ms / 1e3, "unit": "s/round",
+            "note": "same workload, cuts and timed CUDA-graph protocol as the line; "
+                    "4 ATOMS per (g,h) update instead of 2 (DESIGN.md R14)"}
+
+
+def oracle_booster(X, y, cfg, a, threads):
     import oracle as O
-    cfg = W.CONFIGS[config]
-    X, y = W.generate(config, 0, rows, n_rows=max(rows, cfg.n_rows))
+    O.set_threads(threads)
     beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
-    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective,
-                  max_depth=a.depth, eta=cfg.eta, reg_lambda=cfg.reg_lambda,
-                  gamma=cfg.gamma, mcw=cfg.min_child_weight, base_margin=beta,
-                  grow_policy=a.grow_policy, max_leaves=a.leaves)
     t = time.perf_counter()
-    for _ in range(rounds):
-        b.round()
-    per = (time.perf_counter() - t) / rounds
-    return {"value": per * n_full / rows, "unit": "s/round", "cores": 1, "kind": "oracle",
-            "sample": f"{rounds} rounds on the first {rows} rows of the {config} workload, "
-                      f"{per:.3f} s/round measured, scaled x{n_full / rows:.1f} to {n_full} rows "
-                      "(histogram work is linear in rows); single-threaded C oracle, -O2"}
+    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
+                  eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
+                  mcw=cfg.min_child_weight, grad_bits=a.grad_bits, base_margin=beta,
+                  grow_policy=a.grow_policy, max_leaves=a.leaves)
+    return b, time.perf_counter() - t, beta
+
+
+def cpu_baseline_and_parity(G, ctx, torch, dev, X, y, kw, a):
+    """The oracle (C, -O2, threaded over the host's cores) on the FULL rows of the workload for
+    R rounds: its mean seconds per round is cpu_baseline (measured, not extrapolated), and the
+    GPU's first R rounds from the same X, y (cuts and packing on the GPU) are compared with it
+    field by field: cuts, packed words, every tree field, the row -> leaf map and the margins."""
+    cfg = W.CONFIGS[a.config]
+    nproc, model = host_facts()
+    T = a.cpu_threads or nproc
+    R = max(1, a.cpu_rounds)
+    ob, t_prep, beta = oracle_booster(X, y, cfg, a, T)
+    times, otrees, oleaf = [], [], []
+    for _ in range(R):
+        t = time.perf_counter()
+        otrees.append(ob.round())
+        times.append(time.perf_counter() - t)
+        oleaf.append(ob.last["row_leaf"].copy())
+    cpu = {"value": float(np.mean(times)), "unit": "s/round", "cores": T, "kind": "oracle",
+           "host": {"nproc": nproc, "cpu_model": model},
+           "sample": f"{R} oracle rounds on all {len(y)} rows of the {a.config} workload "
+                     f"(per round {', '.join(f'{t:.2f}' for t in times)} s; one-time cuts + "
+                     f"quantise + pack {t_prep:.1f} s not included), C oracle -O2, {T} threads "
+                     "(row blocks with private int64 partial histograms)"}
+    parity = None
+    if not a.no_parity:
+        import oracle as O  # noqa: F401  (the oracle is the checker here)
+        Xd = torch.from_numpy(X).to(dev)
+        yd = torch.from_numpy(y).to(dev)
+        gb = G.Booster(ctx, Xd, yd, **dict(kw, base_margin=beta))
+        qm = gb.qm
+        res = {"rows": int(len(y)), "rounds": R, "cuts": bool(
+            np.array_equal(qm.cut_ptr_h, ob.cut_ptr) and
+            np.array_equal(qm.cut_values.cpu().numpy().view(np.uint32), ob.cut_values.view(np.uint32))),
+            "packed_words": bool(np.array_equal(qm.packed.cpu().numpy().view(np.uint32), ob.words))}
+        fields = ("kind", "feature", "bin", "threshold", "default_left", "gain", "weight", "sum_qg",
+                  "sum_qh")
+        trees_ok, leaf_ok = True, True
+        for r in range(R):
+            gt = gb.round().to_numpy()
+            for k in fields:
+                ga, oa = gt[k], otrees[r][k]
+                if ga.dtype.kind == "f":
+                    ga, oa = ga.view(np.uint64 if ga.itemsize == 8 else np.uint32), \
+                        oa.view(np.uint64 if oa.itemsize == 8 else np.uint32)
+                trees_ok = trees_ok and bool(np.array_equal(ga, oa))
+            leaf_ok = leaf_ok and bool(np.array_equal(gb.row_leaf.cpu().numpy(), oleaf[r]))
+        gm = gb.margin.cpu().numpy()
+        res.update({"trees": trees_ok, "row_leaf": leaf_ok,
+                    "margins": bool(np.array_equal(gm.view(np.uint64), ob.margin.view(np.uint64))),
+                    "margins_max_rel_diff": float(np.max(np.abs(gm - ob.margin) /
+                                                         np.maximum(np.abs(ob.margin), 1e-300)))})
+        res["identical"] = all(res[k] for k in ("cuts", "packed_words", "trees", "row_leaf", "margins"))
+        res["fields"] = list(fields)
+        parity = res
+        del gb, Xd, yd
+        torch.cuda.empty_cache()
+    if a.no_cpu_baseline:
+        cpu = None
+    return cpu, parity
 
 
 def run_reference(a):
-    """Reference arm of this tier: the CPU oracle, as it stands, on the host cores."""
-    import oracle as O
+    """Reference arm of this tier: the CPU oracle, as it stands, threaded over the host's cores,
+    each step one boosting round on ALL rows of the workload (no sample, no extrapolation)."""
     cfg = W.CONFIGS[a.config]
     n = a.rows or cfg.n_rows
-    budget_s = 90.0   # whole --steps K --warmup W run (plus ~10 s of preparation)
-    per_row = 4.5e-6 * (cfg.n_features / 28.0) * (cfg.max_depth / 6.0)
-    if a.grow_policy == "lossguide":  # one partition / histogram pass per expansion
-        per_row *= max(1.0, a.leaves / 2 ** cfg.max_depth) * 2
-    rows = int(min(n, 2_000_000, max(20_000, budget_s / (a.steps + a.warmup) / per_row)))
-    X, y = W.generate(a.config, 0, rows, n_rows=max(rows, cfg.n_rows))
-    beta = 0.0 if cfg.objective == "binary:logistic" else float(np.mean(y.astype(np.float64)))
-    b = O.Booster(X, y, max_bins=cfg.max_bins, objective=cfg.objective, max_depth=a.depth,
-                  eta=cfg.eta, reg_lambda=cfg.reg_lambda, gamma=cfg.gamma,
-                  mcw=cfg.min_child_weight, base_margin=beta, grow_policy=a.grow_policy,
-                  max_leaves=a.leaves)
+    nproc, model = host_facts()
+    T = a.cpu_threads or nproc
+    X, y = W.generate(a.config, 0, n, n_rows=max(n, cfg.n_rows))
+    b, t_prep, _ = oracle_booster(X, y, cfg, a, T)
     for _ in range(a.warmup):
         b.round()
     t = time.perf_counter()
     for _ in range(a.steps):
         b.round()
     per = (time.perf_counter() - t) / a.steps
-    value = per * n / rows
-    sample = (f"each step = one oracle boosting round on the first {rows} of {n} rows "
-              f"({per:.3f} s measured), scaled x{n / rows:.1f} to the full workload")
-    out = {"metric": metric_of(a), "value": value, "unit": "s/round", "n_gpus": 0, "steps": a.steps,
-           "warmup": a.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+    sample = (f"each step = one oracle boosting round on all {n} rows of the {a.config} workload "
+              f"(C oracle -O2, {T} threads; one-time cuts + quantise + pack {t_prep:.1f} s untimed)")
+    out = {"metric": metric_of(a), "value": per, "unit": "s/round", "n_gpus": 0, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": per * 1e3, "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": a.config, "rows": n, "features": cfg.n_features,
                       "max_bins": cfg.max_bins, "max_depth": a.depth,
-                      "objective": cfg.objective, **policy_keys(a)},
-           "cpu_baseline": {"value": value, "unit": "s/round", "cores": 1, "kind": "oracle",
-                            "sample": sample},
-           "e2e": {"value": value, "unit": "s/round", "h2d_bytes_per_step": 0,
+                      "objective": cfg.objective, "grad_bits": a.grad_bits, **policy_keys(a)},
+           "cpu_baseline": {"value": per, "unit": "s/round", "cores": T, "kind": "oracle",
+                            "host": {"nproc": nproc, "cpu_model": model}, "sample": sample},
+           "e2e": {"value": per, "unit": "s/round", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
@@ -510,6 +611,8 @@ def main():
                        "l2": r["l2"]},
             "roofline": r["roofline"],
             "cpu_baseline": r["cpu"],
+            "parity": r["parity"],
+            "grad_bits_30": r["p30"],
             "e2e": r["e2e"],
             "gpu_launches": r["launches"],
             "clocks": r["clocks"],

@@ -39,7 +39,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-Wall", "-o", tmp, _SRC, "-lm"])
+                               "-fopenmp", "-fPIC", "-shared", "-Wall", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -57,6 +57,7 @@ def lib():
             i32, i64, f64, f32 = C.c_int32, C.c_int64, C.c_double, C.c_float
             sig = {
                 "oracle_symbol_bits": (C.c_int, [i32]),
+                "oracle_set_threads": (C.c_int, [i32]),
                 "oracle_cuts": (C.c_int, [_P(f32), i64, i32, i32, _P(f32), _P(i32)]),
                 "oracle_symbols": (C.c_int, [_P(f32), i64, i32, _P(f32), _P(i32), i32,
                                              _P(C.c_uint16), _P(i32)]),
@@ -112,6 +113,12 @@ def _check(code: int, where: str):
 
 
 # ---------------------------------------------------------------------------------------------
+def set_threads(t: int) -> int:
+    """Threaded mode (T row blocks with private int64 partials); returns the
+    previous thread count.  Results do not depend on T (exact sums, per-row values)."""
+    return int(lib().oracle_set_threads(int(t)))
+
+
 def symbol_bits(max_symbol: int) -> int:
     """max(1, ceil(log2(max_symbol + 1))) -- P:30 read as R1."""
     return lib().oracle_symbol_bits(int(max_symbol))

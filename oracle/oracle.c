@@ -16,6 +16,13 @@
  * "Oracle pins" and implemented in tests/test_oracle_*.py.
  *
  * Error codes mirror the C-ABI's documented values but are defined here independently.
+ *
+ * Threaded mode (SURVEY.md §8(d) "Oracle timing"): oracle_set_threads(T) runs the row loops over
+ * T contiguous row blocks (OpenMP), the per-feature sort of the cuts over features, and each
+ * BuildPartialHistograms over T row blocks with private int64 partial histograms summed in block
+ * order.  Every result is a selection, an exact integer sum or a per-row value, so T changes no
+ * output (pinned by tests/test_oracle_tree.py::test_threaded_oracle_identical).  T = 1 (default)
+ * is the plain single-thread program.
  */
 #include <math.h>
 #include <stdint.h>
@@ -29,6 +36,16 @@
 #define OR_E_LABEL (-4)
 #define OR_E_NONFINITE (-5)
 #define OR_E_NOMEM (-12)
+
+static int g_threads = 1;
+
+/* Threads of the row loops (>= 1); returns the previous value. */
+int oracle_set_threads(int32_t t)
+{
+    int old = g_threads;
+    g_threads = t < 1 ? 1 : t;
+    return old;
+}
 
 /* ------------------------------------------------------------------------------------------
  * §2.2 Data compression.  "Matrix values are compressed down to log2(max_value)
@@ -62,47 +79,77 @@ int oracle_cuts(const float *X, int64_t n, int32_t F, int32_t B, float *cut_valu
         return OR_E_EMPTY;
     if (F <= 0 || B < 2)
         return OR_E_ARG;
-    float *V = (float *)malloc(sizeof(float) * (size_t)n);
-    if (!V)
+    /* every feature's cuts into its own slot of tmp (at most B each), then concatenated */
+    float *tmp = (float *)malloc(sizeof(float) * (size_t)F * (size_t)B);
+    int32_t *cnt = (int32_t *)calloc((size_t)F, sizeof(int32_t));
+    if (!tmp || !cnt) {
+        free(tmp);
+        free(cnt);
         return OR_E_NOMEM;
-    int32_t total = 0;
-    cut_ptr[0] = 0;
-    for (int32_t f = 0; f < F; f++) {
-        int64_t m = 0;
-        for (int64_t i = 0; i < n; i++) {
-            float v = X[i * F + f];
-            if (isnan(v))
+    }
+    int err = OR_OK;
+#pragma omp parallel num_threads(g_threads)
+    {
+        float *V = (float *)malloc(sizeof(float) * (size_t)n);
+#pragma omp for schedule(dynamic, 1)
+        for (int32_t f = 0; f < F; f++) {
+            if (!V) {
+                err = OR_E_NOMEM;
                 continue;
-            if (isinf(v)) {
-                free(V);
-                return OR_E_NONFINITE;
             }
-            if (v == 0.0f)
-                v = 0.0f; /* -0.0 -> +0.0 */
-            V[m++] = v;
-        }
-        qsort(V, (size_t)m, sizeof(float), cmp_float);
-        int64_t d = 0;
-        for (int64_t i = 0; i < m; i++)
-            if (i == 0 || V[i] != V[i - 1])
-                d++;
-        if (d <= B) {
+            int64_t m = 0;
+            int bad = 0;
+            for (int64_t i = 0; i < n; i++) {
+                float v = X[i * F + f];
+                if (isnan(v))
+                    continue;
+                if (isinf(v)) {
+                    bad = 1;
+                    break;
+                }
+                if (v == 0.0f)
+                    v = 0.0f; /* -0.0 -> +0.0 */
+                V[m++] = v;
+            }
+            if (bad) {
+                err = OR_E_NONFINITE;
+                continue;
+            }
+            qsort(V, (size_t)m, sizeof(float), cmp_float);
+            int64_t d = 0;
             for (int64_t i = 0; i < m; i++)
                 if (i == 0 || V[i] != V[i - 1])
-                    cut_values[total++] = V[i];
-        } else {
-            int32_t first = total;
-            for (int64_t j = 0; j < B; j++) {
-                int64_t idx = ((j + 1) * m) / B - 1;
-                float c = V[idx];
-                if (total == first || cut_values[total - 1] != c)
-                    cut_values[total++] = c;
+                    d++;
+            float *out = tmp + (size_t)f * B;
+            int32_t c = 0;
+            if (d <= B) {
+                for (int64_t i = 0; i < m; i++)
+                    if (i == 0 || V[i] != V[i - 1])
+                        out[c++] = V[i];
+            } else {
+                for (int64_t j = 0; j < B; j++) {
+                    int64_t idx = ((j + 1) * m) / B - 1;
+                    float v = V[idx];
+                    if (c == 0 || out[c - 1] != v)
+                        out[c++] = v;
+                }
             }
+            cnt[f] = c;
         }
-        cut_ptr[f + 1] = total;
+        free(V);
     }
-    free(V);
-    return OR_OK;
+    if (err == OR_OK) {
+        int32_t total = 0;
+        cut_ptr[0] = 0;
+        for (int32_t f = 0; f < F; f++) {
+            memcpy(cut_values + total, tmp + (size_t)f * B, sizeof(float) * (size_t)cnt[f]);
+            total += cnt[f];
+            cut_ptr[f + 1] = total;
+        }
+    }
+    free(tmp);
+    free(cnt);
+    return err;
 }
 
 /* Bin of a present value: the smallest k with v <= cuts[k]; values above the last
@@ -128,22 +175,28 @@ int oracle_symbols(const float *X, int64_t n, int32_t F, const float *cut_values
     if (n <= 0)
         return OR_E_EMPTY;
     int32_t mx = 0;
+    int err = OR_OK;
+#pragma omp parallel for num_threads(g_threads) schedule(static) reduction(max : mx)
     for (int64_t i = 0; i < n; i++) {
         for (int32_t f = 0; f < F; f++) {
             float v = X[i * F + f];
             int32_t nb = cut_ptr[f + 1] - cut_ptr[f];
             int32_t s;
-            if (isinf(v))
-                return OR_E_NONFINITE;
-            if (isnan(v) || nb == 0)
+            if (isinf(v)) {
+                err = OR_E_NONFINITE;
                 s = B;
-            else
+            } else if (isnan(v) || nb == 0) {
+                s = B;
+            } else {
                 s = bin_of(v, cut_values + cut_ptr[f], nb);
+            }
             sym[i * F + f] = (uint16_t)s;
             if (s > mx)
                 mx = s;
         }
     }
+    if (err != OR_OK)
+        return err;
     *max_symbol = mx;
     return OR_OK;
 }
@@ -276,6 +329,9 @@ int oracle_gradients(int32_t objective, const double *margin, const float *label
         free(h);
         return OR_E_NOMEM;
     }
+    int bad_label = 0;
+    double Mg = 0.0, Mh = 0.0;
+#pragma omp parallel for num_threads(g_threads) schedule(static) reduction(max : Mg, Mh)
     for (int64_t i = 0; i < n; i++) {
         double y = (double)label[i];
         if (objective == 0) {
@@ -283,21 +339,23 @@ int oracle_gradients(int32_t objective, const double *margin, const float *label
             h[i] = 1.0;
         } else {
             if (!(label[i] == 0.0f || label[i] == 1.0f)) {
-                free(g);
-                free(h);
-                return OR_E_LABEL;
+                bad_label = 1;
+                g[i] = h[i] = 0.0;
+                continue;
             }
             double s = oracle_sigmoid(margin[i]);
             g[i] = s - y;
             h[i] = s * (1.0 - s);
         }
-    }
-    double Mg = 0.0, Mh = 0.0;
-    for (int64_t i = 0; i < n; i++) {
         if (fabs(g[i]) > Mg)
             Mg = fabs(g[i]);
         if (fabs(h[i]) > Mh)
             Mh = fabs(h[i]);
+    }
+    if (bad_label) {
+        free(g);
+        free(h);
+        return OR_E_LABEL;
     }
     int Eg = 0, Eh = 0;
     if (Mg > 0.0)
@@ -305,6 +363,7 @@ int oracle_gradients(int32_t objective, const double *margin, const float *label
     if (Mh > 0.0)
         (void)frexp(Mh, &Eh);
     int sg = P - Eg, sh = P - Eh;
+#pragma omp parallel for num_threads(g_threads) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         qpair[2 * i + 0] = (int32_t)rint(ldexp(g[i], sg));
         qpair[2 * i + 1] = (int32_t)rint(ldexp(h[i], sh));
@@ -346,6 +405,52 @@ int oracle_node_histogram(const uint32_t *words, int32_t F, int32_t bits, int32_
         }
     }
     return OR_OK;
+}
+
+/* AllReduceHistograms of the p_workers' partial histograms of node `node` (the rows i
+ * with pos[i] == node; worker w owns rows [w n / p, (w + 1) n / p), R18), summed in worker
+ * order.  Threaded mode splits each worker's rows over g_threads blocks, each with a private
+ * partial (parts: [g_threads][2 TB]); int64 sums are exact, so the block count is invisible.
+ * rows: scratch [n]. */
+static void reduced_histogram(const uint32_t *words, int64_t n, int32_t F, int32_t bits,
+                              int32_t row_align_bits, const int32_t *cut_ptr, int32_t B,
+                              const int32_t *qpair, const int32_t *pos, int32_t node,
+                              int32_t p_workers, int64_t *rows, int64_t *parts, int64_t *hist)
+{
+    const int32_t TB = cut_ptr[F];
+    const int T = g_threads;
+    memset(hist, 0, sizeof(int64_t) * 2 * (size_t)TB);
+    for (int32_t w = 0; w < p_workers; w++) {
+        const int64_t lo = (w * n) / p_workers, hi = ((w + 1) * n) / p_workers;
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+        for (int t = 0; t < T; t++) {
+            const int64_t b0 = lo + ((hi - lo) * t) / T, b1 = lo + ((hi - lo) * (t + 1)) / T;
+            int64_t *rr = rows + b0, m = 0;
+            for (int64_t i = b0; i < b1; i++)
+                if (pos[i] == node)
+                    rr[m++] = i;
+            oracle_node_histogram(words, F, bits, row_align_bits, cut_ptr, B, qpair, rr, m,
+                                  parts + (size_t)t * 2 * TB);
+        }
+        for (int t = 0; t < T; t++)
+            for (int32_t k = 0; k < 2 * TB; k++)
+                hist[k] += parts[(size_t)t * 2 * TB + k];
+    }
+}
+
+/* RepartitionInstances: a row of node k goes to `left` iff
+ * (symbol == sentinel ? default_left : symbol <= bin), else to `right`; rows are independent. */
+static void repartition(const uint32_t *words, int64_t n, int64_t stride, int32_t bits, int32_t B,
+                        int32_t *pos, int32_t k, const int32_t *si, int32_t left, int32_t right)
+{
+#pragma omp parallel for num_threads(g_threads) schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+        if (pos[i] != k)
+            continue;
+        uint32_t s = read_symbol(words, stride, bits, i, si[0]);
+        int go_left = ((int32_t)s == B) ? si[2] : ((int32_t)s <= si[1]);
+        pos[i] = go_left ? left : right;
+    }
 }
 
 /* EvaluateSplit (R8-R10, Q5).  For every feature f, missing mass
@@ -469,7 +574,8 @@ int oracle_build_tree(const uint32_t *words, int64_t n, int32_t F, int32_t bits,
         sum_qh[k] = 0;
     }
     int64_t *hist = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1), sizeof(int64_t));
-    int64_t *part = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1), sizeof(int64_t));
+    int64_t *part = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1) * (size_t)g_threads,
+                                      sizeof(int64_t));
     int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     entry_t *queue = (entry_t *)malloc(sizeof(entry_t) * (size_t)cap);
     if (!hist || !part || !rows || !queue) {
@@ -484,19 +590,8 @@ int oracle_build_tree(const uint32_t *words, int64_t n, int32_t F, int32_t bits,
 
     /* AllReduce of the p partial histograms of node `node` (rows with position == node). */
 #define BUILD_REDUCED_HIST(node_id)                                                              \
-    do {                                                                                         \
-        memset(hist, 0, sizeof(int64_t) * 2 * (size_t)TB);                                      \
-        for (int32_t w = 0; w < p_workers; w++) {                                                \
-            int64_t lo = (w * n) / p_workers, hi = ((w + 1) * n) / p_workers, m = 0;             \
-            for (int64_t i = lo; i < hi; i++)                                                    \
-                if (row_leaf[i] == (node_id))                                                    \
-                    rows[m++] = i;                                                               \
-            oracle_node_histogram(words, F, bits, row_align_bits, cut_ptr, B, qpair, rows, m,    \
-                                  part);                                                         \
-            for (int32_t t = 0; t < 2 * TB; t++)                                                 \
-                hist[t] += part[t];                                                              \
-        }                                                                                        \
-    } while (0)
+    reduced_histogram(words, n, F, bits, row_align_bits, cut_ptr, B, qpair, row_leaf, (node_id),   \
+                      p_workers, rows, part, hist)
 
     /* InitRoot: root totals over every worker's rows, root histogram, root split. */
     entry_t root;
@@ -537,13 +632,7 @@ int oracle_build_tree(const uint32_t *words, int64_t n, int32_t F, int32_t bits,
         /* RepartitionInstances on every worker: a row of node k goes left
          * iff (symbol == sentinel ? default_left : symbol <= bin).  Rows keep row order. */
         int32_t left = 2 * k + 1, right = 2 * k + 2;
-        for (int64_t i = 0; i < n; i++) {
-            if (row_leaf[i] != k)
-                continue;
-            uint32_t s = read_symbol(words, stride, bits, i, e.si[0]);
-            int go_left = ((int32_t)s == B) ? e.si[2] : ((int32_t)s <= e.si[1]);
-            row_leaf[i] = go_left ? left : right;
-        }
+        repartition(words, n, stride, bits, B, row_leaf, k, e.si, left, right);
         entry_t le, re;
         memset(&le, 0, sizeof(le));
         memset(&re, 0, sizeof(re));
@@ -618,7 +707,8 @@ int oracle_build_tree_lossguide(const uint32_t *words, int64_t n, int32_t F, int
         left_child[k] = -1;
     }
     int64_t *hist = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1), sizeof(int64_t));
-    int64_t *part = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1), sizeof(int64_t));
+    int64_t *part = (int64_t *)calloc(2 * (size_t)(TB > 0 ? TB : 1) * (size_t)g_threads,
+                                      sizeof(int64_t));
     int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     entry_t *queue = (entry_t *)malloc(sizeof(entry_t) * (size_t)cap);
     if (!hist || !part || !rows || !queue) {
@@ -632,19 +722,8 @@ int oracle_build_tree_lossguide(const uint32_t *words, int64_t n, int32_t F, int
         row_leaf[i] = 0;
 
 #define BUILD_REDUCED_HIST(node_id)                                                              \
-    do {                                                                                         \
-        memset(hist, 0, sizeof(int64_t) * 2 * (size_t)TB);                                      \
-        for (int32_t w = 0; w < p_workers; w++) {                                                \
-            int64_t lo = (w * n) / p_workers, hi = ((w + 1) * n) / p_workers, m = 0;             \
-            for (int64_t i = lo; i < hi; i++)                                                    \
-                if (row_leaf[i] == (node_id))                                                    \
-                    rows[m++] = i;                                                               \
-            oracle_node_histogram(words, F, bits, row_align_bits, cut_ptr, B, qpair, rows, m,    \
-                                  part);                                                         \
-            for (int32_t t = 0; t < 2 * TB; t++)                                                 \
-                hist[t] += part[t];                                                              \
-        }                                                                                        \
-    } while (0)
+    reduced_histogram(words, n, F, bits, row_align_bits, cut_ptr, B, qpair, row_leaf, (node_id),   \
+                      p_workers, rows, part, hist)
 
     entry_t root;
     memset(&root, 0, sizeof(root));
@@ -697,13 +776,7 @@ int oracle_build_tree_lossguide(const uint32_t *words, int64_t n, int32_t F, int
         threshold[k] = cut_values[cut_ptr[e.si[0]] + e.si[1]];
         gain[k] = e.gain;
         left_child[k] = left;
-        for (int64_t i = 0; i < n; i++) { /* RepartitionInstances on every worker */
-            if (row_leaf[i] != k)
-                continue;
-            uint32_t s = read_symbol(words, stride, bits, i, e.si[0]);
-            int go_left = ((int32_t)s == B) ? e.si[2] : ((int32_t)s <= e.si[1]);
-            row_leaf[i] = go_left ? left : right;
-        }
+        repartition(words, n, stride, bits, B, row_leaf, k, e.si, left, right); /* every worker */
         entry_t le, re;
         memset(&le, 0, sizeof(le));
         memset(&re, 0, sizeof(re));
@@ -741,6 +814,7 @@ int oracle_predict_linked(int32_t n_trees, int64_t cap, const int8_t *kind, cons
                           const int32_t *left_child, const double *weight, double base_margin,
                           const float *X, int64_t n, int32_t F, double *margin)
 {
+#pragma omp parallel for num_threads(g_threads) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         double m = base_margin;
         for (int32_t t = 0; t < n_trees; t++) {
@@ -762,6 +836,7 @@ int oracle_predict_linked(int32_t n_trees, int64_t cap, const int8_t *kind, cons
 int oracle_update_margins(const double *weight, const int32_t *row_leaf, int64_t n,
                           double *margin)
 {
+#pragma omp parallel for num_threads(g_threads) schedule(static)
     for (int64_t i = 0; i < n; i++)
         margin[i] = margin[i] + weight[row_leaf[i]];
     return OR_OK;
@@ -776,6 +851,7 @@ int oracle_predict(int32_t n_trees, int32_t max_depth, const int8_t *kind,
                    int32_t F, double *margin)
 {
     int64_t cap = ((int64_t)1 << (max_depth + 1)) - 1;
+#pragma omp parallel for num_threads(g_threads) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         double m = base_margin;
         for (int32_t t = 0; t < n_trees; t++) {

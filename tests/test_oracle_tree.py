@@ -314,3 +314,31 @@ def test_all_gradients_zero_root_is_leaf():
     q[:, 1] = 1
     t, rl = O.build_tree(words, 50, 3, bits, 32, v, p, 16, q, (15, 15), 3, 0.3, 1.0, 0.0, 0.0)
     assert t["kind"][0] == 2
+
+
+@pytest.mark.parametrize("grow,p", [("depthwise", 1), ("depthwise", 3), ("lossguide", 2)])
+def test_threaded_oracle_identical(grow, p):
+    """Threaded mode: T row blocks with private int64 partial histograms, summed in
+    block order, the cut sort over features, the per-row loops split -- identical cuts, symbols,
+    gradients, trees, row partitions and margins for T = 1 and T = 5."""
+    import workloads as W
+    X, y = W.generate("higgs", 0, 30_011)
+    runs = []
+    for T in (1, 5):
+        old = O.set_threads(T)
+        try:
+            b = O.Booster(X, y, max_bins=256, objective="binary:logistic",
+                          max_depth=6 if grow == "depthwise" else 10, eta=0.3, p_workers=p,
+                          grow_policy=grow, max_leaves=20 if grow == "lossguide" else 0)
+            trees = [b.round() for _ in range(2)]
+            runs.append((b.cut_values.copy(), b.cut_ptr.copy(), b.words.copy(), trees,
+                         b.last["row_leaf"].copy(), b.last["qpair"].copy(), b.margin.copy(),
+                         b.predict()))
+        finally:
+            O.set_threads(old)
+    a, c = runs
+    for i in (0, 1, 2, 4, 5, 6, 7):
+        np.testing.assert_array_equal(a[i], c[i])
+    for ta, tc in zip(a[3], c[3]):
+        for k in ta:
+            np.testing.assert_array_equal(ta[k], tc[k])
