@@ -152,6 +152,21 @@ GBM_API int gbm_comm_unique_id(uint8_t id_h[128]);
 GBM_API int gbm_comm_init(gbm_ctx *ctx, const uint8_t id_h[128], int nranks, int rank);
 GBM_API int gbm_comm_info(gbm_ctx *ctx, int *nranks_h, int *rank_h);
 
+/* Virtual ranks (test harness for the multi-rank path on ONE GPU): a gbm_vcomm joins
+ * nranks contexts of one process on one device, each driven by its own host thread and stream.
+ * gbm_comm_init_virtual attaches ctx as `rank`; afterwards every collective entry (gbm_cuts C3,
+ * gbm_gradients C1, gbm_build_tree C2 and its argument agreement) exchanges through the vcomm
+ * exactly where it would call NCCL: the callers' streams are synchronised, the ranks meet at a
+ * host barrier, rank 0 sums (int64) / takes the max / gathers the posted device buffers, and
+ * every rank copies the result back.  Results equal NCCL's (integer sums and maxima are exact).
+ * Not usable inside CUDA graph capture (GBM_E_STATE).  The vcomm is owned by the caller and
+ * must outlive its contexts' last collective call.  nranks in 1..64.
+ * Errors: GBM_E_ARG (bad nranks / rank), GBM_E_STATE (ctx already has a communicator). */
+typedef struct gbm_vcomm gbm_vcomm;
+GBM_API int gbm_vcomm_create(int nranks, gbm_vcomm **out);
+GBM_API int gbm_vcomm_destroy(gbm_vcomm *vc);
+GBM_API int gbm_comm_init_virtual(gbm_ctx *ctx, gbm_vcomm *vc, int rank);
+
 /* ---------------------------------------------------------------- §2.1 quantiles
  * gbm_cuts: exact per-feature cut points over the GLOBAL rows (collective: the ranks'
  * shards are all-gathered).  Rule R5: with V the sorted present values of a
@@ -284,7 +299,14 @@ typedef struct {
  * child's histogram, one allreduce, sibling by subtraction, evaluate both children.  Uses the
  * compact histogram layout whatever GBM_OPT_HIST_LAYOUT says.
  * row_leaf_d int32 [n_rows] receives the leaf each row ends in.
- * Asynchronous (no host synchronisation inside a tree). */
+ * Asynchronous (no host synchronisation inside a tree).
+ * Errors: GBM_E_ARG (null pointers, max_depth outside 0..16, grad_bits outside 1..30, negative
+ * lambda / gamma / min_child_weight, lossguide max_leaves outside 1..65536), GBM_E_EMPTY (zero
+ * rows on a single rank; a rank of several may hold none).  With a communicator of several
+ * ranks (outside CUDA-graph capture) the ranks first agree in one small collective: every rank
+ * returns the same code when any rank's arguments are bad, and GBM_E_MISMATCH when the
+ * ranks' n_features, total bins, symbol bits, row alignment, max_bins, max_depth, grow_policy,
+ * max_leaves or grad_bits differ -- so no rank enters a histogram allreduce its peers skip. */
 GBM_API int gbm_build_tree(gbm_ctx *ctx, const gbm_qmatrix *qm, const int32_t *qpair_d,
                    const int32_t *scale_d, const gbm_params *params, const gbm_tree *tree,
                    int32_t *row_leaf_d, void *stream);

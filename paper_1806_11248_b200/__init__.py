@@ -18,7 +18,7 @@ import torch
 
 from . import build_lib
 
-__all__ = ["GbmError", "Context", "QMatrix", "Tree", "Booster", "lib", "symbol_bits",
+__all__ = ["GbmError", "Context", "QMatrix", "Tree", "Booster", "VirtualComm", "lib", "symbol_bits",
            "packed_words", "SQUARED_ERROR", "LOGISTIC", "OBJECTIVES"]
 
 SQUARED_ERROR, LOGISTIC = 0, 1
@@ -81,6 +81,9 @@ EXPORTS = {
     "gbm_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "gbm_comm_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
     "gbm_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "gbm_vcomm_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "gbm_vcomm_destroy": (C.c_int, [C.c_void_p]),
+    "gbm_comm_init_virtual": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "gbm_cuts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
                            C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p]),
     "gbm_quantise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
@@ -272,6 +275,12 @@ class Context:
     def comm_init(self, id_bytes: bytes, nranks: int, rank: int):
         ids = (C.c_uint8 * 128)(*id_bytes)
         _call("gbm_comm_init", self.h, ids, nranks, rank)
+
+    def comm_init_virtual(self, vcomm: "VirtualComm", rank: int):
+        """Attach this context as virtual rank `rank` of `vcomm` (p ranks on one device, one
+        host thread each; the test harness of the multi-rank path, gbm.h)."""
+        _call("gbm_comm_init_virtual", self.h, vcomm.h, int(rank))
+        self._vcomm = vcomm  # keep the communicator alive while this context uses it
 
     @staticmethod
     def comm_unique_id() -> bytes:
@@ -489,6 +498,26 @@ class Context:
               _p(cat["threshold"]), _p(cat["default_left"]), _p(cat["weight"]),
               float(base_margin), _p(X), n, F, _p(out), _stream())
         return out
+
+
+class VirtualComm:
+    """An in-process communicator of `nranks` virtual ranks on one device (gbm_vcomm_create)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        _call("gbm_vcomm_create", int(nranks), C.byref(h))
+        self.h, self.nranks = h, int(nranks)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gbm_vcomm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def share_unique_id(make_id, group=None, device=None) -> bytes:

@@ -97,11 +97,6 @@ int ctx_enter(gbm_ctx *ctx) {
     return GBM_OK;
 }
 
-int allreduce_i64(gbm_ctx *ctx, long long *buf, size_t count, cudaStream_t s) {
-    if (!ctx->comm || count == 0) return GBM_OK;
-    GBM_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, ctx->comm, s));
-    return GBM_OK;
-}
 
 }  // namespace gbm
 
@@ -148,6 +143,7 @@ int gbm_ctx_destroy(gbm_ctx *ctx) {
     if (ctx->arena.base) cudaFree(ctx->arena.base);
     if (ctx->tree_arena.base) cudaFree(ctx->tree_arena.base);
     if (ctx->dev_err) cudaFree(ctx->dev_err);
+    if (ctx->agree_d) cudaFree(ctx->agree_d);
     if (ctx->prof.rows_dev) cudaFree(ctx->prof.rows_dev);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
     if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -186,7 +182,7 @@ int gbm_comm_init(gbm_ctx *ctx, const uint8_t id_h[128], int nranks, int rank) {
     GBM_TRY(ctx_enter(ctx));
     if (!id_h || nranks < 1 || rank < 0 || rank >= nranks)
         return fail(GBM_E_ARG, "gbm_comm_init: bad id / nranks / rank");
-    if (ctx->comm) return fail(GBM_E_STATE, "gbm_comm_init: communicator already initialised");
+    if (ctx->comm || ctx->vcomm) return fail(GBM_E_STATE, "gbm_comm_init: communicator already initialised");
     ncclUniqueId id;
     memcpy(&id, id_h, 128);
     GBM_NCCL(ncclCommInitRank(&ctx->comm, nranks, id, rank));

@@ -11,6 +11,8 @@
 
 #include "../../include/gbm.h"
 
+struct gbm_vcomm;  // comm.cu: in-process communicator of virtual ranks
+
 namespace gbm {
 
 // ------------------------------------------------------------------ error plumbing
@@ -99,6 +101,8 @@ struct gbm_ctx {
     int sm_count = 148;
     size_t smem_optin = 227 * 1024;
     ncclComm_t comm = nullptr;
+    gbm_vcomm *vcomm = nullptr;    // virtual ranks on one device (comm.cu), instead of NCCL
+    long long *agree_d = nullptr;  // coll_agree scratch
     int nranks = 1, rank = 0;
     uint32_t *dev_err = nullptr;   // device-latched error bits
     gbm::Arena arena;              // scratch for the current call
@@ -146,6 +150,13 @@ struct ProfScope {
     ~ProfScope();
 };
 int allreduce_i64(gbm_ctx *ctx, long long *buf, size_t count, cudaStream_t s);
+
+// ------------------------------------------------------------------ collectives (comm.cu)
+enum CollOp { COLL_SUM_I64 = 0, COLL_MAX_U64 = 1, COLL_MAX_I64 = 2 };
+bool coll_on(const gbm_ctx *ctx);  // an NCCL or virtual communicator is attached
+int coll_allreduce(gbm_ctx *ctx, void *buf, size_t count, CollOp op, cudaStream_t s);
+int coll_allgather(gbm_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank, cudaStream_t s);
+int coll_agree(gbm_ctx *ctx, int local_code, const long long *sig, int nsig, cudaStream_t s, const char *where);
 
 // ------------------------------------------------------------------ packed-matrix access
 // The layout of gbm_compress (R3): element (r, f) at stream bit r*stride + f*bits.

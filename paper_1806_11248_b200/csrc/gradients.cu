@@ -188,9 +188,9 @@ int grad_pass1(gbm_ctx *ctx, int objective, const double *margin_d, const float 
 static int grad_pass2(gbm_ctx *ctx, int objective, int grad_bits, const double *margin_d, const float *label_d,
                       long long n_rows, unsigned long long *maxbits, const double *sig, int32_t *qpair_d,
                       int32_t *scale_d, cudaStream_t s) {
-    if (ctx->comm) {  // C1: global max of |g|, |h| (exact, order-free)
+    if (coll_on(ctx)) {  // C1: global max of |g|, |h| (exact, order-free)
         ProfScope ps(ctx, PC_ALLREDUCE, s, 16.0);
-        GBM_NCCL(ncclAllReduce(maxbits, maxbits, 2, ncclUint64, ncclMax, ctx->comm, s));
+        GBM_TRY(coll_allreduce(ctx, maxbits, 2, COLL_MAX_U64, s));
     }
     {
         ProfScope ps(ctx, PC_GRAD_QUANT, s, (double)n_rows * 20);
@@ -216,13 +216,19 @@ int gbm_gradients_from_stats(gbm_ctx *ctx, int32_t objective, int32_t grad_bits,
                              const float *label_d, int64_t n_rows, const double *sig_d, uint64_t *maxbits_d,
                              int32_t *qpair_d, int32_t *scale_d, void *stream) {
     GBM_TRY(ctx_enter(ctx));
-    GBM_REQUIRE(objective == GBM_SQUARED_ERROR || objective == GBM_LOGISTIC, GBM_E_ARG,
-                "gbm_gradients_from_stats: unknown objective");
-    GBM_REQUIRE(grad_bits >= 1 && grad_bits <= 30, GBM_E_ARG, "gbm_gradients_from_stats: grad_bits in 1..30");
-    GBM_REQUIRE(n_rows > 0 || (ctx->comm && ctx->nranks > 1), GBM_E_EMPTY, "gbm_gradients_from_stats: zero rows");
-    GBM_REQUIRE(((margin_d && label_d && qpair_d) || n_rows == 0) && scale_d && maxbits_d &&
-                    (objective != GBM_LOGISTIC || sig_d || n_rows == 0),
-                GBM_E_ARG, "gbm_gradients_from_stats: null pointer");
+    auto check = [&]() -> int {
+        GBM_REQUIRE(objective == GBM_SQUARED_ERROR || objective == GBM_LOGISTIC, GBM_E_ARG,
+                    "gbm_gradients_from_stats: unknown objective");
+        GBM_REQUIRE(grad_bits >= 1 && grad_bits <= 30, GBM_E_ARG, "gbm_gradients_from_stats: grad_bits in 1..30");
+        GBM_REQUIRE(n_rows > 0 || (coll_on(ctx) && ctx->nranks > 1), GBM_E_EMPTY,
+                    "gbm_gradients_from_stats: zero rows");
+        GBM_REQUIRE(((margin_d && label_d && qpair_d) || n_rows == 0) && scale_d && maxbits_d &&
+                        (objective != GBM_LOGISTIC || sig_d || n_rows == 0),
+                    GBM_E_ARG, "gbm_gradients_from_stats: null pointer");
+        return GBM_OK;
+    };
+    const long long sig[2] = {objective, grad_bits};  // C1 follows: every rank agrees first
+    GBM_TRY(coll_agree(ctx, check(), sig, 2, (cudaStream_t)stream, "gbm_gradients_from_stats"));
     return grad_pass2(ctx, objective, grad_bits, margin_d, label_d, n_rows,
                       reinterpret_cast<unsigned long long *>(maxbits_d), sig_d, qpair_d, scale_d, (cudaStream_t)stream);
 }
@@ -231,19 +237,24 @@ int gbm_gradients(gbm_ctx *ctx, int32_t objective, int32_t grad_bits, const doub
                   const float *label_d, int64_t n_rows, int32_t *qpair_d, int32_t *scale_d,
                   void *stream) {
     GBM_TRY(ctx_enter(ctx));
-    GBM_REQUIRE(objective == GBM_SQUARED_ERROR || objective == GBM_LOGISTIC, GBM_E_ARG,
-                "gbm_gradients: unknown objective");
-    GBM_REQUIRE(grad_bits >= 1 && grad_bits <= 30, GBM_E_ARG, "gbm_gradients: grad_bits in 1..30");
-    GBM_REQUIRE(n_rows > 0 || (ctx->comm && ctx->nranks > 1), GBM_E_EMPTY, "gbm_gradients: zero rows");
-    GBM_REQUIRE((margin_d && label_d && qpair_d) || n_rows == 0, GBM_E_ARG, "gbm_gradients: null pointer");
-    GBM_REQUIRE(scale_d, GBM_E_ARG, "gbm_gradients: null scale");
+    auto check = [&]() -> int {
+        GBM_REQUIRE(objective == GBM_SQUARED_ERROR || objective == GBM_LOGISTIC, GBM_E_ARG,
+                    "gbm_gradients: unknown objective");
+        GBM_REQUIRE(grad_bits >= 1 && grad_bits <= 30, GBM_E_ARG, "gbm_gradients: grad_bits in 1..30");
+        GBM_REQUIRE(n_rows > 0 || (coll_on(ctx) && ctx->nranks > 1), GBM_E_EMPTY, "gbm_gradients: zero rows");
+        GBM_REQUIRE((margin_d && label_d && qpair_d) || n_rows == 0, GBM_E_ARG, "gbm_gradients: null pointer");
+        GBM_REQUIRE(scale_d, GBM_E_ARG, "gbm_gradients: null scale");
+        return GBM_OK;
+    };
+    const long long sig[2] = {objective, grad_bits};  // C1 follows: every rank agrees first
+    GBM_TRY(coll_agree(ctx, check(), sig, 2, (cudaStream_t)stream, "gbm_gradients"));
     cudaStream_t s = (cudaStream_t)stream;
     const bool lg = objective == GBM_LOGISTIC;
     GBM_TRY(ctx->arena.reserve(512 + (lg ? (size_t)n_rows * 8 : 0)));
     unsigned long long *maxbits = ctx->arena.take<unsigned long long>(2);
-    double *sig = lg ? ctx->arena.take<double>((size_t)std::max<int64_t>(n_rows, 1)) : nullptr;
-    GBM_TRY(grad_pass1(ctx, objective, margin_d, label_d, n_rows, maxbits, sig, s));
-    return grad_pass2(ctx, objective, grad_bits, margin_d, label_d, n_rows, maxbits, sig, qpair_d, scale_d, s);
+    double *sig_p = lg ? ctx->arena.take<double>((size_t)std::max<int64_t>(n_rows, 1)) : nullptr;
+    GBM_TRY(grad_pass1(ctx, objective, margin_d, label_d, n_rows, maxbits, sig_p, s));
+    return grad_pass2(ctx, objective, grad_bits, margin_d, label_d, n_rows, maxbits, sig_p, qpair_d, scale_d, s);
 }
 
 int gbm_update_margins(gbm_ctx *ctx, const double *weight_d, const int32_t *row_leaf_d,

@@ -440,12 +440,18 @@ int gbm_quantise_compress(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_
                           int32_t row_align_bits, uint32_t *packed_d, int64_t packed_words,
                           void *stream) {
     GBM_TRY(ctx_enter(ctx));
-    GBM_REQUIRE(n_rows > 0, GBM_E_EMPTY, "gbm_quantise_compress: zero rows");
+    // a rank of several may hold no rows (its shard of a tiny matrix): only the zero pad words
+    const bool empty_rank = n_rows == 0 && coll_on(ctx) && ctx->nranks > 1;
+    GBM_REQUIRE(n_rows > 0 || empty_rank, GBM_E_EMPTY, "gbm_quantise_compress: zero rows");
     int64_t need = gbm_packed_words(n_rows, F, bits, row_align_bits);
     if (need < 0) return (int)need;
-    GBM_REQUIRE(X_d && cv && cp && packed_d && packed_words >= need && max_bins >= 2 &&
+    GBM_REQUIRE((X_d || empty_rank) && cv && cp && packed_d && packed_words >= need && max_bins >= 2 &&
                     max_bins <= 65535,
                 GBM_E_ARG, "gbm_quantise_compress: bad arguments");
+    if (empty_rank) {
+        GBM_CUDA(cudaMemsetAsync(packed_d, 0, (size_t)packed_words * 4, (cudaStream_t)stream));
+        return GBM_OK;
+    }
     long long stride = row_stride_bits(F, bits, row_align_bits);
     ProfScope ps(ctx, PC_QUANT, (cudaStream_t)stream, (double)n_rows * F * 4 + (double)packed_words * 4);
     pack_kernel<true><<<grid_for(packed_words, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
@@ -467,26 +473,36 @@ int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t 
     long long n_total = n_rows, n_max = n_rows;
     const float *Xg = X_d;
     float *gathered = nullptr;
-    if (ctx->comm) {
+    if (coll_on(ctx)) {
         long long *tmp;
         GBM_CUDA(cudaMallocAsync((void **)&tmp, 2 * sizeof(long long), s));
         long long h2[2] = {n_rows, n_rows};
         GBM_CUDA(cudaMemcpyAsync(tmp, h2, sizeof(h2), cudaMemcpyHostToDevice, s));
-        GBM_NCCL(ncclAllReduce(tmp, tmp, 1, ncclInt64, ncclSum, ctx->comm, s));
-        GBM_NCCL(ncclAllReduce(tmp + 1, tmp + 1, 1, ncclInt64, ncclMax, ctx->comm, s));
-        GBM_CUDA(cudaMemcpyAsync(h2, tmp, sizeof(h2), cudaMemcpyDeviceToHost, s));
-        GBM_CUDA(cudaStreamSynchronize(s));
-        GBM_CUDA(cudaFreeAsync(tmp, s));
+        int rc = coll_allreduce(ctx, tmp, 1, COLL_SUM_I64, s);
+        if (rc == GBM_OK) rc = coll_allreduce(ctx, tmp + 1, 1, COLL_MAX_I64, s);
+        if (rc == GBM_OK && cudaMemcpyAsync(h2, tmp, sizeof(h2), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            rc = fail(GBM_E_CUDA, "gbm_cuts: copy of the global row counts");
+        if (rc == GBM_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = fail(GBM_E_CUDA, "gbm_cuts: sync");
+        cudaFreeAsync(tmp, s);
+        if (rc != GBM_OK) return rc;
         n_total = h2[0];
         n_max = h2[1];
         size_t slab = (size_t)n_max * F;
-        GBM_CUDA(cudaMallocAsync((void **)&gathered, slab * ctx->nranks * sizeof(float), s));
-        float *mine;
-        GBM_CUDA(cudaMallocAsync((void **)&mine, std::max<size_t>(slab, 1) * sizeof(float), s));
-        GBM_CUDA(cudaMemsetAsync(mine, 0xff, slab * sizeof(float), s));  // 0xffffffff is a NaN
-        if (n_rows) GBM_CUDA(cudaMemcpyAsync(mine, X_d, (size_t)n_rows * F * sizeof(float), cudaMemcpyDeviceToDevice, s));
-        GBM_NCCL(ncclAllGather(mine, gathered, slab, ncclFloat32, ctx->comm, s));
-        GBM_CUDA(cudaFreeAsync(mine, s));
+        float *mine = nullptr;
+        if (cudaMallocAsync((void **)&gathered, std::max<size_t>(slab, 1) * ctx->nranks * sizeof(float), s) != cudaSuccess ||
+            cudaMallocAsync((void **)&mine, std::max<size_t>(slab, 1) * sizeof(float), s) != cudaSuccess) {
+            cudaGetLastError();
+            if (gathered) cudaFreeAsync(gathered, s);
+            return fail(GBM_E_NOMEM, "gbm_cuts: cannot allocate the gathered rows");
+        }
+        cudaMemsetAsync(mine, 0xff, slab * sizeof(float), s);  // 0xffffffff is a NaN
+        if (n_rows) cudaMemcpyAsync(mine, X_d, (size_t)n_rows * F * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        rc = coll_allgather(ctx, mine, gathered, slab * sizeof(float), s);  // C3
+        cudaFreeAsync(mine, s);
+        if (rc != GBM_OK) {
+            cudaFreeAsync(gathered, s);
+            return rc;
+        }
         Xg = gathered;
         n_max = n_max * ctx->nranks;  // rows of the gathered buffer (padding rows are all-NaN)
     }

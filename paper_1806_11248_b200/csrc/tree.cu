@@ -3652,12 +3652,12 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
 
 // gbm_build_tree / gbm_build_tree_fused: ep (nullable) is fused into the final walk when the
 // staged walk applies (*ep_done = true); otherwise the caller runs it as separate kernels.
-static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
-                           const gbm_params *prm, const gbm_tree *tree, int32_t *row_leaf_d, void *stream,
-                           const gbm_epilogue *ep, bool *ep_done) {
-    GBM_TRY(ctx_enter(ctx));
+// argument checks of gbm_build_tree (local decision; build_tree_impl makes it collective)
+static int validate_tree_args(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
+                              const gbm_params *prm, const gbm_tree *tree, const int32_t *row_leaf_d) {
     GBM_TRY(check_qm(q));
-    GBM_REQUIRE(prm && tree && scale_d && row_leaf_d && qpair_d, GBM_E_ARG, "gbm_build_tree: null argument");
+    GBM_REQUIRE(prm && tree && scale_d && ((row_leaf_d && qpair_d) || q->n_rows == 0), GBM_E_ARG,
+                "gbm_build_tree: null argument");
     GBM_REQUIRE(tree->kind && tree->feature && tree->bin && tree->threshold && tree->default_left && tree->gain &&
                     tree->weight && tree->sum_qg && tree->sum_qh,
                 GBM_E_ARG, "gbm_build_tree: null tree array");
@@ -3675,7 +3675,28 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     GBM_REQUIRE(prm->lambda >= 0 && prm->gamma >= 0 && prm->min_child_weight >= 0, GBM_E_ARG,
                 "gbm_build_tree: lambda, gamma, min_child_weight must be >= 0");
     const long long n = q->n_rows;
-    GBM_REQUIRE(n > 0 || (ctx->comm && ctx->nranks > 1), GBM_E_EMPTY, "gbm_build_tree: zero rows (S:321)");
+    GBM_REQUIRE(n > 0 || (coll_on(ctx) && ctx->nranks > 1), GBM_E_EMPTY, "gbm_build_tree: zero rows (S:321)");
+    return GBM_OK;
+}
+
+static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair_d, const int32_t *scale_d,
+                           const gbm_params *prm, const gbm_tree *tree, int32_t *row_leaf_d, void *stream,
+                           const gbm_epilogue *ep, bool *ep_done) {
+    GBM_TRY(ctx_enter(ctx));
+    // every argument check decides locally; the ranks then agree (one collective) so that all of
+    // them return the same error -- or GBM_E_MISMATCH when their shapes differ -- and none enters
+    // a histogram allreduce its peers skip
+    int rc = validate_tree_args(ctx, q, qpair_d, scale_d, prm, tree, row_leaf_d);
+    long long sig[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (q && q->cut_ptr_h && prm && q->n_features > 0) {
+        const long long v[9] = {q->n_features, q->cut_ptr_h[q->n_features], q->bits, q->row_align_bits,
+                                q->max_bins, prm->max_depth, prm->grow_policy, prm->max_leaves, prm->grad_bits};
+        std::copy(v, v + 9, sig);
+    }
+    rc = coll_agree(ctx, rc, sig, 9, (cudaStream_t)stream, "gbm_build_tree");
+    if (rc != GBM_OK) return rc;
+    const long long n = q->n_rows;
+
     cudaStream_t s = (cudaStream_t)stream;
     const QM qm = make_qm(q);
     if (prm->grow_policy == GBM_GROW_LOSSGUIDE)

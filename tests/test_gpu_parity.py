@@ -539,7 +539,8 @@ def test_staged_root_parity(ctx, G, cfg, n, missing, align, P):
                    row_align_bits=align)
     gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth,
                    grad_bits=P, row_align_bits=align, base_margin=ob.base_margin)
-    staged = align % 32 == 0  # word-aligned rows: the staged kernels apply (else the compact root)
+    # word-aligned rows of 8-bit (byte) or 9..15-bit (generic) symbols: the staged kernels apply
+    staged = align % 32 == 0 and (gb.qm.bits == 8 or 9 <= gb.qm.bits <= 15)
     for _ in range(2):
         ctx.profile(True, only=("hist_root", "hist_level"))
         _compare_tree(gb.round().to_numpy(), ob.round())
@@ -664,6 +665,34 @@ def test_full_size_round_properties(ctx, G, cfg):
     tid["weight"] = np.arange(cap, dtype=np.float64)
     leaf = O.predict([tid], c.max_depth, 0.0, X[idx]).astype(np.int64)
     np.testing.assert_array_equal(leaf, rl[idx])
+
+
+@pytest.mark.parametrize("cfg,P", [("higgs", 15), ("higgs", 30)])
+def test_full_size_training_parity(ctx, G, cfg, P):
+    """BASELINE.json's Higgs-shaped 11M x 28 at full size, the headline configuration (auto
+    level plan: several 2048-row tiles per work item, several parents per level): GPU cuts,
+    packed words, and two boosting rounds -- every tree field, the row -> leaf map and the
+    margins -- bit for bit against the oracle (threaded over the host's cores; results do not
+    depend on the thread count, tests/test_oracle_tree.py::test_threaded_oracle_identical)."""
+    import os
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg)
+    old = O.set_threads(len(os.sched_getaffinity(0)))
+    try:
+        ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth,
+                       eta=c.eta, grad_bits=P)
+        gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective,
+                       max_depth=c.max_depth, eta=c.eta, grad_bits=P, base_margin=ob.base_margin)
+        np.testing.assert_array_equal(gb.qm.cut_ptr_h, ob.cut_ptr)
+        np.testing.assert_array_equal(gb.qm.cut_values.cpu().numpy().view(np.uint32),
+                                      ob.cut_values.view(np.uint32))
+        np.testing.assert_array_equal(u32(gb.qm.packed), ob.words)
+        for _ in range(2):
+            _compare_tree(gb.round().to_numpy(), ob.round())
+            np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+            np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    finally:
+        O.set_threads(old)
 
 
 def test_single_rank_communicator_paths(G):
