@@ -331,13 +331,15 @@ def run_ours(a, world, rank, local):
     booster.trees = []
     for _ in range(10):
         booster.round()
+    booster.predict(Xd)  # warm: lazy module load and the tree concatenation's allocations
     torch.cuda.synchronize()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    booster.predict(Xd)
+    for _ in range(5):
+        booster.predict(Xd)
     p1.record(stream)
     torch.cuda.synchronize()
-    predict_ms = max_over_ranks(p0.elapsed_time(p1))
+    predict_ms = max_over_ranks(p0.elapsed_time(p1) / 5)
     Xd_keep, yd_keep = Xd, yd
     del booster, Xd, yd, flush_buf
     torch.cuda.empty_cache()

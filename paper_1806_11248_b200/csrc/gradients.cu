@@ -157,6 +157,138 @@ __global__ void predict_kernel(int n_trees, long long cap, const int8_t *__restr
     }
 }
 
+// Staged prediction ("one training instance per thread ... iterating through each tree
+// sequentially", Q7): a block stages PR_ROWS rows of X with coalesced 16-byte loads into shared
+// memory (row pitch F | 1 floats: the per-thread reads of one feature fall into distinct banks) and
+// a chunk of trees as packed node records; each thread then walks its row through the chunk's
+// trees in order, adding the leaf weights to its fp64 margin in tree order (the oracle's
+// operation sequence).  Nodes: meta = (threshold bits, feature | default_left << 16 | split << 17),
+// left child (heap 2k+1, or left_child[k] for linked trees), weight.
+constexpr int PR_THREADS = 256;
+constexpr int PR_ROWS = 256;  // one row per thread
+constexpr int PR_FMAX = 64;   // features staged (wider matrices use predict_kernel)
+struct PNode {
+    uint32_t thr;   // threshold bits
+    uint32_t info;  // feature (16 bits) | default_left << 16 | split << 17
+};
+
+template <bool LINKED>
+__global__ void __launch_bounds__(PR_THREADS) predict_stg_kernel(
+    int n_trees, long long cap, int trees_per_chunk, const int8_t *__restrict__ kind,
+    const int32_t *__restrict__ feature, const float *__restrict__ thr, const int8_t *__restrict__ dl,
+    const int32_t *__restrict__ left_child, const double *__restrict__ weight, double base,
+    const float *__restrict__ X, long long n, int F, double *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char psm[];
+    const int pitch = F | 1;
+    float *xs = reinterpret_cast<float *>(psm);                                   // [PR_ROWS][pitch]
+    const size_t xs_bytes = ((size_t)PR_ROWS * pitch * 4 + 15) & ~size_t(15);
+    const int chunk_nodes = trees_per_chunk * (int)cap;
+    double *ws = reinterpret_cast<double *>(psm + xs_bytes);                      // [chunk_nodes]
+    PNode *ns = reinterpret_cast<PNode *>(ws + chunk_nodes);                      // [chunk_nodes]
+    int32_t *ls = reinterpret_cast<int32_t *>(ns + chunk_nodes);                  // [chunk_nodes] (LINKED)
+    const long long tiles = (n + PR_ROWS - 1) / PR_ROWS;
+    const bool vec = (F % 4) == 0;  // rows of whole float4s (16-byte aligned when X is)
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const long long r0 = tile * PR_ROWS;
+        const int nr = (int)min((long long)PR_ROWS, n - r0);
+        __syncthreads();  // previous tile's readers are done
+        if (vec) {
+            const float4 *src = reinterpret_cast<const float4 *>(X + r0 * F);
+            const int F4 = F / 4;
+            for (int i = threadIdx.x; i < nr * F4; i += PR_THREADS) {
+                const float4 v = __ldg(src + i);
+                const int r = i / F4, c = (i - r * F4) * 4;
+                float *d = xs + r * pitch + c;
+                d[0] = v.x;
+                d[1] = v.y;
+                d[2] = v.z;
+                d[3] = v.w;
+            }
+        } else {
+            const float *src = X + r0 * F;
+            for (int i = threadIdx.x; i < nr * F; i += PR_THREADS) {
+                const int r = i / F;
+                xs[r * pitch + (i - r * F)] = __ldg(src + i);
+            }
+        }
+        double m = base;
+        const int row = threadIdx.x;
+        const float *x = xs + row * pitch;
+        for (int t0 = 0; t0 < n_trees; t0 += trees_per_chunk) {
+            const int nt = min(trees_per_chunk, n_trees - t0);
+            if (t0 > 0 || tile == blockIdx.x || n_trees > trees_per_chunk) {
+                if (t0 > 0) __syncthreads();  // the previous chunk's walkers are done
+                const long long base_node = (long long)t0 * cap;
+                for (int i = threadIdx.x; i < nt * (int)cap; i += PR_THREADS) {
+                    const long long g = base_node + i;
+                    const int k = __ldg(kind + g);
+                    const int f = __ldg(feature + g);
+                    PNode pn;
+                    pn.thr = __float_as_uint(__ldg(thr + g));
+                    pn.info = (k == GBM_NODE_SPLIT) ? ((uint32_t)(f & 0xffff) | ((uint32_t)(__ldg(dl + g) != 0) << 16) |
+                                                       (1u << 17))
+                                                    : 0u;
+                    ns[i] = pn;
+                    ws[i] = __ldg(weight + g);
+                    if (LINKED) ls[i] = __ldg(left_child + g);
+                }
+            }
+            __syncthreads();
+            if (row < nr) {
+                for (int t = 0; t < nt; ++t) {
+                    const int o = t * (int)cap;
+                    int k = 0;
+                    PNode pn = ns[o];
+                    while (pn.info & (1u << 17)) {
+                        const int f = pn.info & 0xffff;
+                        const float v = f < F ? x[f] : __int_as_float(0x7fffffff);
+                        const bool left = isnan(v) ? ((pn.info >> 16) & 1u) : (v <= __uint_as_float(pn.thr));
+                        const int c = LINKED ? ls[o + k] : 2 * k + 1;
+                        k = left ? c : c + 1;
+                        pn = ns[o + k];
+                    }
+                    m = dadd(m, ws[o + k]);
+                }
+            }
+        }
+        if (row < nr) out[r0 + row] = m;
+    }
+}
+
+// shared bytes of predict_stg_kernel for F features and `trees` trees of capacity cap per chunk
+static size_t predict_smem(int F, long long cap, int trees, bool linked) {
+    const size_t xs = ((size_t)PR_ROWS * (F | 1) * 4 + 15) & ~size_t(15);
+    return xs + (size_t)trees * cap * (8 + sizeof(PNode) + (linked ? 4 : 0));
+}
+
+// staged launch when it applies (F <= PR_FMAX, at least one tree fits): 1 on success, 0 to fall
+// back to predict_kernel, < 0 on a CUDA error
+template <bool LINKED>
+static int launch_predict_stg(gbm_ctx *ctx, int n_trees, long long cap, const int8_t *kind, const int32_t *feature,
+                              const float *thr, const int8_t *dl, const int32_t *left_child, const double *weight,
+                              double base, const float *X, long long n, int F, double *out, cudaStream_t s) {
+    if (F > PR_FMAX || F >= 65536 || cap > (1 << 20) || reinterpret_cast<uintptr_t>(X) % 16 != 0) return 0;
+    const size_t budget = 96 * 1024;  // two blocks per SM
+    const size_t one = predict_smem(F, cap, 1, LINKED);
+    if (one > budget) return 0;
+    int tpc = (int)std::max<long long>(1, std::min<long long>(std::max(n_trees, 1),
+                                                              (long long)((budget - predict_smem(F, cap, 0, LINKED)) /
+                                                                          (cap * (8 + sizeof(PNode) + (LINKED ? 4 : 0))))));
+    const size_t sm = predict_smem(F, cap, tpc, LINKED);
+    if (cudaFuncSetAttribute(predict_stg_kernel<LINKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+        cudaSuccess)
+        return fail(GBM_E_CUDA, "predict: shared memory attribute");
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, predict_stg_kernel<LINKED>, PR_THREADS, sm) != cudaSuccess ||
+        occ < 1)
+        return 0;
+    const long long tiles = (n + PR_ROWS - 1) / PR_ROWS;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(tiles, (long long)occ * ctx->sm_count));
+    predict_stg_kernel<LINKED><<<grid, PR_THREADS, sm, s>>>(n_trees, cap, tpc, kind, feature, thr, dl, left_child,
+                                                            weight, base, X, n, F, out);
+    return cudaGetLastError() == cudaSuccess ? 1 : fail(GBM_E_CUDA, "predict_stg_kernel launch");
+}
+
 static int grid_for(long long work, int threads, int sm) {
     long long g = (work + threads - 1) / threads;
     long long cap = (long long)sm * 16;
@@ -282,9 +414,14 @@ int gbm_predict(gbm_ctx *ctx, int32_t n_trees, int32_t max_depth, const int8_t *
     if (n_rows == 0) return GBM_OK;
     long long cap = (1ll << (max_depth + 1)) - 1;
     ProfScope ps(ctx, PC_PREDICT, (cudaStream_t)stream, (double)n_rows * (4.0 * n_features + 8.0));
-    predict_kernel<false><<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
-        n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, nullptr, weight_d, base_margin, X_d,
-        n_rows, n_features, margin_d);
+    const int st = launch_predict_stg<false>(ctx, n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, nullptr,
+                                             weight_d, base_margin, X_d, n_rows, n_features, margin_d,
+                                             (cudaStream_t)stream);
+    if (st < 0) return st;
+    if (st == 0)  // wide rows: per-thread gathers of the visited features
+        predict_kernel<false><<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
+            n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, nullptr, weight_d, base_margin, X_d,
+            n_rows, n_features, margin_d);
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
@@ -302,9 +439,14 @@ int gbm_predict_linked(gbm_ctx *ctx, int32_t n_trees, int64_t cap, const int8_t 
                 GBM_E_ARG, "gbm_predict_linked: null pointer");
     if (n_rows == 0) return GBM_OK;
     ProfScope ps(ctx, PC_PREDICT, (cudaStream_t)stream, (double)n_rows * (4.0 * n_features + 8.0));
-    predict_kernel<true><<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
-        n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, left_child_d, weight_d, base_margin,
-        X_d, n_rows, n_features, margin_d);
+    const int st = launch_predict_stg<true>(ctx, n_trees, cap, kind_d, feature_d, threshold_d, default_left_d,
+                                            left_child_d, weight_d, base_margin, X_d, n_rows, n_features, margin_d,
+                                            (cudaStream_t)stream);
+    if (st < 0) return st;
+    if (st == 0)
+        predict_kernel<true><<<grid_for(n_rows, 128, ctx->sm_count), 128, 0, (cudaStream_t)stream>>>(
+            n_trees, cap, kind_d, feature_d, threshold_d, default_left_d, left_child_d, weight_d, base_margin,
+            X_d, n_rows, n_features, margin_d);
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }

@@ -808,3 +808,29 @@ def test_fused_round_equals_separate_calls(ctx, G, cfg, obj_override, D):
         np.testing.assert_array_equal(gf.qpair.cpu().numpy(), ob.last["qpair"])
         np.testing.assert_array_equal(gf.margin.cpu().numpy(), ob.margin)
         np.testing.assert_array_equal(gs.margin.cpu().numpy(), ob.margin)
+
+
+@pytest.mark.parametrize("cfg,n,rounds,grow,missing", [
+    ("higgs", 5_003, 70, "depthwise", 0.0),      # 70 trees: several tree chunks per row tile
+    ("airline", 3_001, 12, "depthwise", 0.03),   # 13 features (not whole float4s), NaNs
+    ("tiny", 700, 40, "lossguide", 0.05),        # linked trees, many chunks
+    ("epsilon", 1_500, 3, "depthwise", 0.0),     # 2000 features: the gather predictor
+])
+def test_predict_many_trees_parity(ctx, G, cfg, n, rounds, grow, missing):
+    """gbm_predict / gbm_predict_linked (Q7) after many rounds, on the training rows and
+    on fresh rows with missing values: the margins equal the oracle's predictor bit for bit (fp64
+    adds in tree order) and the staged-consistency identity predict(k trees) == margins."""
+    c = W.CONFIGS[cfg]
+    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
+    kw = dict(max_bins=c.max_bins, objective=c.objective, max_depth=(c.max_depth if grow == "depthwise" else 7),
+              eta=0.3)
+    L = 10 if grow == "lossguide" else 0
+    ob = O.Booster(X, y, grow_policy=grow, max_leaves=L, **kw)
+    gb = G.Booster(ctx, dev(X), dev(y), base_margin=ob.base_margin, grow_policy=grow, max_leaves=L, **kw)
+    for _ in range(rounds):
+        ob.round()
+        gb.round()
+    np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy().view(np.uint64), ob.margin.view(np.uint64))
+    Xt, _ = W.generate(cfg, n, n + 2_345, n_rows=max(n + 2_345, c.n_rows), missing=0.1)
+    np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy().view(np.uint64),
+                                  ob.predict(Xt).view(np.uint64))
