@@ -137,10 +137,16 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   its child's segment of a second buffer (2 x n x (row bytes + 8) of scratch); applies to
  *   8-bit symbols, <= 32 features, rows of whole words.  1 = row-index lists (partition flags +
  *   scan + scatter of row ids; packed rows and qpair gathered per level).  0 (default) = 1
- *   (measured faster end to end).  Same trees either way. */
+ *   (measured faster end to end).  Same trees either way.
+ * GBM_OPT_LEVEL_HIST: the shared-memory histogram of the row-index level kernel.  1 = compact
+ *   (bins of all features packed; lane = (row, packed word), random-bank atomics); 2 =
+ *   bank-column (lane = feature, word = bin * 32 + lane: conflict-free atomics, the row's words
+ *   moved to the feature lanes by warp shuffles; byte symbols, <= 32 features, whole-word rows);
+ *   0 (default) = 1 (measured faster: the shuffles cost more issue slots than the bank conflicts
+ *   they remove).  Same histograms either way. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
        GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
-       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12 };
+       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12, GBM_OPT_LEVEL_HIST = 13 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

@@ -331,6 +331,7 @@ class Context:
     TMA_ROWS = 10
     ROW_DECIDE = 11
     LEVEL_PATH = 12
+    LEVEL_HIST = 13
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

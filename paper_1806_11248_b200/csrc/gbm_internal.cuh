@@ -118,7 +118,8 @@ struct gbm_ctx {
     int seg_hist = 0;              // GBM_OPT_SEGMENT_HIST (0 auto, 1 off, 2 on)
     int stage_tma = 1;             // staged root: TMA bulk row copies (GBM_OPT_TMA_ROWS)
     int row_decide = 0;            // GBM_OPT_ROW_DECIDE (2 on; measured slower, off by default)
-    int level_path = 0;            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
+    int level_path = 0;
+    int level_hist = 0;            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed bank-column)            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     // second stream of gbm_build_tree: the partition scatter of a level overlaps the allreduce

@@ -679,6 +679,139 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
     }
 }
 
+// ============================================================== shuffle-fed bank-column levels
+// The fused level kernel for byte symbols with every feature in one group (F <= 32, rows of U
+// whole words): the partition phase is part_hist_kernel's; the built rows are fetched exactly as
+// there -- lane (row slot r, word w) loads word w of its row, 32 / U rows per load instruction --
+// but accumulated into the conflict-free bank-column histogram (word = bin * 32 + lane): lane
+// (copy c, feature f) takes its symbol from lane (r, f / 4) with one shuffle and the row's pair
+// with two, then adds into its own bank.  The compact layout's random-bank ATOMS cost ~3.4
+// wavefronts each (ncu: 70 % of the level kernel's atomic wavefronts were conflict replays);
+// these cost one.  The sentinel (B < 256) lands in a bin >= n_bins(f) of its column, never
+// flushed (as in the lean root kernel).
+template <bool WIDE>
+__global__ void __launch_bounds__(H_THREADS, WIDE ? 1 : 2) part_hist_sb_kernel(FusedArgs a) {
+    extern __shared__ int smem[];
+    __shared__ uint32_t s_rows[H_THREADS / 32][WROWS];
+    constexpr int CH = WIDE ? 4 : 2;
+    const QM &qm = a.qm;
+    const uint32_t *rin = static_cast<const uint32_t *>(a.ridx_in);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n_items = *a.n_items;
+    uint32_t *wrows = s_rows[wid];
+    const int F = qm.F, U = (F + 3) >> 2;        // words per row (stride == U words)
+    const int rpp = 32 / U;                      // rows per load instruction
+    const int lr = lane / U, lw = lane - lr * U; // loading role: row slot, word
+    const bool load_on = lr < rpp;
+    const int R = 32 / F;                        // rows per accumulate step (copies)
+    const int cc = lane / F, cf = lane - cc * F; // accumulating role: copy, feature
+    const bool acc_on = cc < R;
+    const int src_w = cf >> 2, sh = 8 * (cf & 3);
+    const unsigned hb = smem_u32(smem) + 4u * lane;
+    const ColGroup cg{0, F};
+    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_items;
+         it = claim_item(const_cast<int *>(a.n_items) + 1)) {
+        const int run = it;
+        const int j = find_parent(a.run_base, a.n_par, run);
+        const int k = a.first + j;
+        const NodeDev nd = a.nodes[k];
+        const int tb = a.tile_base[j];
+        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const long long seg_end = nd.start + nd.count;
+        if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
+            for (int t = t0; t < t1; ++t) {
+                const long long base = nd.start + (long long)(t - tb) * PT;
+                for (int i = threadIdx.x; i < PT; i += H_THREADS) {
+                    const long long pos = base + i;
+                    if (pos < seg_end) a.row_leaf[rin ? rin[pos] : (uint32_t)pos] = k;
+                }
+            }
+            continue;
+        }
+        for (int i = threadIdx.x; i < CH * COLB_STRIDE; i += H_THREADS) smem[i] = 0;
+        __syncthreads();
+        const bool build_left = nd.build_left != 0;
+        unsigned long long bits_acc = 0;
+        for (int t = t0; t < t1; ++t) {
+            const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
+            // (A) partition flags for the warp's 128 rows (as part_hist_kernel)
+            uint32_t row[4], bw[4];
+            int nleft = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const long long pos = base + s2 * 32 + lane;
+                row[s2] = pos < seg_end ? (rin ? rin[pos] : (uint32_t)pos) : 0u;
+            }
+            bool left[4];
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) left[s2] = base + s2 * 32 + lane < seg_end && goes_left(qm, nd, row[s2]);
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const bool valid = base + s2 * 32 + lane < seg_end;
+                const uint32_t lw2 = __ballot_sync(0xffffffffu, valid && left[s2]);
+                bw[s2] = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
+                if (lane == 0) a.flags[(long long)t * (PT / 32) + wid * 4 + s2] = lw2;
+                nleft += __popc(lw2);
+            }
+            int nbuild = 0;
+            const uint32_t ltm = (1u << lane) - 1u;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                if ((bw[s2] >> lane) & 1u) wrows[nbuild + __popc(bw[s2] & ltm)] = row[s2];
+                nbuild += __popc(bw[s2]);
+            }
+            if (lane == 0) {
+                if (nleft) atomicAdd(a.tile_left + t, nleft);
+                if (a.rows_ctr) {
+                    const long long nv = max(0ll, min((long long)WROWS, seg_end - base));
+                    bits_acc += (unsigned long long)nv * a.bits_parent_row + (unsigned long long)nbuild * a.bits_built_row;
+                }
+            }
+            __syncwarp();
+            // (B) the listed rows: PH_UNR load groups in flight, then shuffle + conflict-free ATOMS
+            for (int rb = 0; rb < nbuild; rb += PH_UNR * rpp) {
+                uint32_t wd[PH_UNR];
+                int2 qq[PH_UNR];
+#pragma unroll
+                for (int u = 0; u < PH_UNR; ++u) {
+                    const int rr = rb + u * rpp + lr;
+                    const bool ok = load_on && rr < nbuild;
+                    const uint32_t r = ok ? wrows[rr] : 0u;
+                    wd[u] = ok ? __ldg(qm.P + (size_t)r * U + lw) : 0u;
+                    qq[u] = ok ? __ldg(a.qpair + r) : make_int2(0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < PH_UNR; ++u) {
+                    for (int s0 = 0; s0 < rpp; s0 += R) {  // R rows per step (warp-uniform)
+                        const int rs = s0 + (acc_on ? cc : 0);
+                        const int src = rs * U;
+                        const uint32_t w = __shfl_sync(0xffffffffu, wd[u], src + src_w);
+                        const int qx = __shfl_sync(0xffffffffu, qq[u].x, src);
+                        const int qy = __shfl_sync(0xffffffffu, qq[u].y, src);
+                        if (acc_on && rs < rpp && rb + u * rpp + rs < nbuild) {
+                            const unsigned addr = hb + (((w >> sh) & 255u) << 7);
+                            if (WIDE) {
+                                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(qx & 0x7fff) : "memory");
+                                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr + 4 * COLB_STRIDE), "r"(qy & 0x7fff) : "memory");
+                                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr + 8 * COLB_STRIDE), "r"(qx >> 15) : "memory");
+                                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr + 12 * COLB_STRIDE), "r"(qy >> 15) : "memory");
+                            } else {
+                                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(qx) : "memory");
+                                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr + 4 * COLB_STRIDE), "r"(qy) : "memory");
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (bits_acc) atomicAdd(a.rows_ctr, bits_acc);
+        __syncthreads();
+        col_flush<WIDE>(smem, COLB_STRIDE, cg, a.cut_ptr, a.hist + (long long)j * a.TB * 2);
+        __syncthreads();
+    }
+}
+
 // ============================================================== segment histograms
 // With several shared-memory feature groups (wide data: Epsilon 63, Bosch ~40, YearMSD 3) the
 // fused kernel would repeat the partition of every parent row once per group.  Instead the level
@@ -1511,7 +1644,9 @@ struct WalkEpi {
     const double *weight;
 };
 
-template <int W, bool EPI>
+// BYTE (8-bit symbols, rows of whole words): the symbol of feature f is byte f of the staged row,
+// one LDS.U8 per level (the node record holds the byte index); SENT: the sentinel fits in 8 bits.
+template <int W, bool EPI, bool BYTE = false, bool SENT = true>
 __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, const int8_t *__restrict__ kind,
                                                                      const int32_t *__restrict__ feature,
                                                                      const int32_t *__restrict__ bin,
@@ -1526,8 +1661,12 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
     for (int k = threadIdx.x; k < n_internal; k += WALK_THREADS) {
         int x = 0;
         if (kind[k] == GBM_NODE_SPLIT) {
-            const int bp = feature[k] * qm.bits, wi = bp >> 5, off = bp & 31;
-            x = (int)(1u << 31) | ((int)dl[k] << 30) | ((off + qm.bits > 32) << 29) | (off << 16) | wi;
+            if (BYTE) {
+                x = (int)(1u << 31) | ((int)dl[k] << 30) | feature[k];
+            } else {
+                const int bp = feature[k] * qm.bits, wi = bp >> 5, off = bp & 31;
+                x = (int)(1u << 31) | ((int)dl[k] << 30) | ((off + qm.bits > 32) << 29) | (off << 16) | wi;
+            }
         }
         s_node[k] = make_int2(x, bin[k]);
     }
@@ -1563,15 +1702,26 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
             const uint32_t *row = sr + lane * PW;
             const uint32_t mask = (1u << qm.bits) - 1u;
             int k = 0;
-            for (int d = 0; d < depth; ++d) {
-                const int2 nk = s_node[k];
-                if (nk.x >= 0) break;  // leaf
-                const int wi = nk.x & 0xffff, off = (nk.x >> 16) & 31;
-                uint32_t v = row[wi] >> off;
-                if (nk.x & (1 << 29)) v |= row[wi + 1] << (32 - off);  // off > 0 here
-                const int sym = (int)(v & mask);
-                const bool left = sym == qm.B ? ((nk.x >> 30) & 1) : (sym <= nk.y);
-                k = left ? 2 * k + 1 : 2 * k + 2;
+            if (BYTE) {
+                const uint8_t *rb = reinterpret_cast<const uint8_t *>(row);
+                for (int d = 0; d < depth; ++d) {
+                    const int2 nk = s_node[k];
+                    if (nk.x >= 0) break;  // leaf
+                    const int sym = rb[nk.x & 0xffff];
+                    const bool left = (SENT && sym == qm.B) ? ((nk.x >> 30) & 1) : (sym <= nk.y);
+                    k = 2 * k + 2 - (int)left;
+                }
+            } else {
+                for (int d = 0; d < depth; ++d) {
+                    const int2 nk = s_node[k];
+                    if (nk.x >= 0) break;  // leaf
+                    const int wi = nk.x & 0xffff, off = (nk.x >> 16) & 31;
+                    uint32_t v = row[wi] >> off;
+                    if (nk.x & (1 << 29)) v |= row[wi + 1] << (32 - off);  // off > 0 here
+                    const int sym = (int)(v & mask);
+                    const bool left = sym == qm.B ? ((nk.x >> 30) & 1) : (sym <= nk.y);
+                    k = left ? 2 * k + 1 : 2 * k + 2;
+                }
             }
             const long long r = c * 32 + lane;
             row_leaf[r] = k;
@@ -3038,21 +3188,32 @@ static void launch_col_fused(const HistPlan &hp, const ColFusedArgs &ca, cudaStr
     }
 }
 
+template <int W, bool BYTE, bool SENT>
+static void launch_walk_t(int grid, size_t sm, cudaStream_t s, const QM &qm, const TreeDev &t, int n_int, int D,
+                          long long n, int32_t *rl, const WalkEpi *epi) {
+    if (epi) {
+        auto k = leaf_walk_stg_kernel<W, true, BYTE, SENT>;
+        if (sm > 16 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k<<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl, *epi);
+    } else {
+        auto k = leaf_walk_stg_kernel<W, false, BYTE, SENT>;
+        if (sm > 16 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k<<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left, n_int, D, n, rl, WalkEpi{});
+    }
+}
+
 template <int W>
 static void launch_walk_reg(int grid, size_t sm, cudaStream_t s, const QM &qm, const TreeDev &t, int n_int, int D,
                             long long n, int32_t *rl, const WalkEpi *epi) {
-    if (epi) {
-        if (sm > 16 * 1024)
-            cudaFuncSetAttribute(leaf_walk_stg_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        leaf_walk_stg_kernel<W, true><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
-                                                                     n_int, D, n, rl, *epi);
-    } else {
-        if (sm > 16 * 1024)
-            cudaFuncSetAttribute(leaf_walk_stg_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        leaf_walk_stg_kernel<W, false><<<grid, WALK_THREADS, sm, s>>>(qm, t.kind, t.feature, t.bin, t.default_left,
-                                                                      n_int, D, n, rl, WalkEpi{});
+    // byte symbols (8-bit, rows of whole words, F <= 4 W): one LDS.U8 per level
+    if constexpr (W <= 8) {
+        if (qm.bits == 8) {
+            if (qm.B < 256) launch_walk_t<W, true, true>(grid, sm, s, qm, t, n_int, D, n, rl, epi);
+            else launch_walk_t<W, true, false>(grid, sm, s, qm, t, n_int, D, n, rl, epi);
+            return;
+        }
     }
-
+    launch_walk_t<W, false, true>(grid, sm, s, qm, t, n_int, D, n, rl, epi);
 }
 
 static TreeDev tree_dev(const gbm_tree *t) {
@@ -3864,6 +4025,25 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     const bool seg_mode = !hp.col && G > 1 &&
                           (ctx->seg_hist == 2 || (ctx->seg_hist == 0 && !hp.byte_path));
     const int Gf = seg_mode ? 1 : G;  // groups of the fused launch
+    // shuffle-fed bank-column level kernel (part_hist_sb_kernel): byte symbols, one group of
+    // every feature (F <= 32), rows of whole words, row-index entries without gradient pairs
+    const bool sb_ok = !hp.col && hp.byte_path && G == 1 && F <= 32 && qm.stride == 32ll * ((F + 3) / 4) &&
+                       !hp.carry && !seg_mode;
+    const bool sb_levels = sb_ok && ctx->level_hist == 2;
+    int sb_grid = 1;
+    if (sb_levels) {
+        const size_t smb = (size_t)(hp.wide ? 4 : 2) * COLB_STRIDE * 4;
+        int occ = 0;
+        if (hp.wide) {
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_sb_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_hist_sb_kernel<true>, H_THREADS, smb));
+        } else {
+            GBM_CUDA(cudaFuncSetAttribute(part_hist_sb_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_hist_sb_kernel<false>, H_THREADS, smb));
+        }
+        GBM_REQUIRE(occ >= 1, GBM_E_ARG, "bank-column level kernel cannot be resident");
+        sb_grid = occ * ctx->sm_count;
+    }
     const long long tiles_all = (n + PT - 1) / PT;
     const long long target = 4ll * hp.blocks_fused;
     const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
@@ -4069,6 +4249,11 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
                 ca.bits_parent_row = fa.bits_parent_row;
                 ca.bits_built_row = fa.bits_built_row;
                 launch_col_fused(hp, ca, s);
+                GBM_CUDA(cudaGetLastError());
+            } else if (sb_levels) {  // shuffle-fed bank-column levels
+                const size_t smb = (size_t)(hp.wide ? 4 : 2) * COLB_STRIDE * 4;
+                if (hp.wide) part_hist_sb_kernel<true><<<sb_grid, H_THREADS, smb, s>>>(fa);
+                else part_hist_sb_kernel<false><<<sb_grid, H_THREADS, smb, s>>>(fa);
                 GBM_CUDA(cudaGetLastError());
             } else {
                 GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));

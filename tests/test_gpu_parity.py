@@ -364,6 +364,29 @@ def test_record_levels_parity(ctx, G, cfg, n, missing, align, P, B, depth, path)
     ctx.set_option(ctx.LEVEL_PATH, 0)
 
 
+@pytest.mark.parametrize("level_hist", [1, 2])
+@pytest.mark.parametrize("cfg,n,missing,align,P,B,depth", REC_CASES + [("higgs", 150_000, 0.0, 32, 15, None, 8)])
+def test_level_hist_layouts_parity(ctx, G, cfg, n, missing, align, P, B, depth, level_hist):
+    """GBM_OPT_LEVEL_HIST 2 (bank-column level histograms fed by warp shuffles) and 1 (compact),
+    both against the oracle bit for bit, with multi-tile work items (RUN_TILES 3)."""
+    ctx.set_option(ctx.LEVEL_HIST, level_hist)
+    ctx.set_option(ctx.RUN_TILES, 3)
+    c = W.CONFIGS[cfg]
+    B = B or c.max_bins
+    D = depth or c.max_depth
+    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
+    ob = O.Booster(X, y, max_bins=B, objective=c.objective, max_depth=D, grad_bits=P, row_align_bits=align,
+                   eta=0.3)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=B, objective=c.objective, max_depth=D, grad_bits=P,
+                   row_align_bits=align, base_margin=ob.base_margin, eta=0.3)
+    for _ in range(3):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.LEVEL_HIST, 0)
+    ctx.set_option(ctx.RUN_TILES, 0)
+
+
 @pytest.mark.parametrize("run_tiles", [2, 5, 8, 31])
 @pytest.mark.parametrize("cfg,n,missing,P", [("higgs", 300_000, 0.0, 15), ("airline", 250_000, 0.0, 15),
                                              ("higgs", 200_000, 0.0, 30), ("bosch", 40_000, 0.0, 15)])
