@@ -143,10 +143,17 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   bank-column (lane = feature, word = bin * 32 + lane: conflict-free atomics, the row's words
  *   moved to the feature lanes by warp shuffles; byte symbols, <= 32 features, whole-word rows);
  *   0 (default) = 1 (measured faster: the shuffles cost more issue slots than the bank conflicts
- *   they remove).  Same histograms either way. */
+ *   they remove).  Same histograms either way.
+ * GBM_OPT_EVAL_SLICED: with a communicator of p > 1 ranks, depth-wise trees:
+ *   1 = AllReduceHistograms becomes a reduce-scatter: rank r receives only the summed bins of its
+ *   contiguous feature slice (features balanced by bins), evaluates those features, and the ranks
+ *   all-gather their per-(node, feature) best candidates before the replicated node reduction --
+ *   half the collective bytes per rank and 1/p of the evaluation; 0 (default) = allreduce.  Same
+ *   trees either way (exact sums, canonical argmax). */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
        GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
-       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12, GBM_OPT_LEVEL_HIST = 13 };
+       GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12, GBM_OPT_LEVEL_HIST = 13,
+       GBM_OPT_EVAL_SLICED = 14 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

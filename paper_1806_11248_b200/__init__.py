@@ -332,6 +332,7 @@ class Context:
     ROW_DECIDE = 11
     LEVEL_PATH = 12
     LEVEL_HIST = 13
+    EVAL_SLICED = 14
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

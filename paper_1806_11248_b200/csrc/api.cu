@@ -300,6 +300,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->walk_mode = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_EVAL_SLICED) {
+        if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_EVAL_SLICED: 0 off, 1 on");
+        ctx->eval_sliced = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_LEVEL_HIST) {
         if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_LEVEL_HIST: 0 auto, 1 compact, 2 bank-column");
         ctx->level_hist = (int)value;

@@ -145,6 +145,44 @@ int coll_allgather(gbm_ctx *ctx, const void *send, void *recv, size_t bytes, cud
     });
 }
 
+// Sum of every rank's send[p][count] (int64) with chunk r delivered to rank r's recv[count]
+// (ncclReduceScatter; the reduce-scatter + feature-sliced evaluation variant of C2).
+int coll_reduce_scatter_i64(gbm_ctx *ctx, const long long *send, long long *recv, size_t count, cudaStream_t s) {
+    if (!coll_on(ctx)) {
+        if (count) GBM_CUDA(cudaMemcpyAsync(recv, send, count * 8, cudaMemcpyDeviceToDevice, s));
+        return GBM_OK;
+    }
+    if (ctx->comm) {
+        GBM_NCCL(ncclReduceScatter(send, recv, count, ncclInt64, ncclSum, ctx->comm, s));
+        return GBM_OK;
+    }
+    // virtual: rank 0 sums the posted [p][count] buffers into scratch; rank r copies chunk r
+    gbm_vcomm *v = ctx->vcomm;
+    if (capturing(s)) return fail(GBM_E_STATE, "virtual communicator: collectives cannot be graph-captured");
+    GBM_CUDA(cudaStreamSynchronize(s));
+    v->posted[ctx->rank] = send;
+    vc_barrier(v);
+    const size_t total = count * v->nranks;
+    if (ctx->rank == 0) {
+        v->err = vc_scratch(v, std::max<size_t>(total * 8, 16));
+        if (v->err == GBM_OK && total) {
+            VcPtrs p = {};
+            for (int r = 0; r < v->nranks; ++r) p.p[r] = v->posted[r];
+            vc_reduce_kernel<<<256, 256>>>(p, v->nranks, total, (int)COLL_SUM_I64, v->scratch);
+            if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) v->err = GBM_E_CUDA;
+        }
+    }
+    vc_barrier(v);
+    const int err = v->err;
+    if (err == GBM_OK && count) {
+        GBM_CUDA(cudaMemcpyAsync(recv, static_cast<const long long *>(v->scratch) + count * ctx->rank, count * 8,
+                                 cudaMemcpyDeviceToDevice, s));
+        GBM_CUDA(cudaStreamSynchronize(s));
+    }
+    vc_barrier(v);
+    return err == GBM_OK ? GBM_OK : fail(err, "virtual reduce-scatter failed on rank 0");
+}
+
 // The decision every rank must share before a collective call sequence: the first
 // nonzero local error code of any rank, or GBM_E_MISMATCH when the ranks' signatures (sizes
 // that must be equal everywhere, e.g. F, TB, bits) differ, is returned on EVERY rank, so no rank

@@ -2415,6 +2415,16 @@ struct EvalArgs {
     const StepDev *step;            // loss-guided: the current expansion
     StepDev *step_next;             // loss-guided: written by the pop of the next step
     long long *hist_pool;           // loss-guided: [max_leaves][TB][2] by LgNode::hslot
+    // reduce-scatter + feature-sliced evaluation (GBM_OPT_EVAL_SLICED): this rank evaluates the
+    // features f0 .. f0 + F - 1 into fb (its histograms hold only their bins, slot stride TB =
+    // the slice capacity, base pointers shifted by the slice's first bin); the finisher reduces
+    // the all-gathered fb_all [nslices][n_nodes][fsmax] of every rank
+    int f0;
+    int sliced;                     // 1: feature evaluation only (the finisher runs separately)
+    const long long *root_tot;      // root totals (null: hist_root[2 TB])
+    const FeatBest *fb_all;
+    const int *slice_f0, *slice_nf;
+    int nslices, fsmax;
 };
 
 // Node j's histogram source and totals; false if the node does not exist.
@@ -2446,8 +2456,8 @@ __device__ __forceinline__ bool node_source(const EvalArgs &a, int j, NodeHist &
     }
     if (a.level == 0) {
         src.direct = a.hist_root;
-        Tg = a.hist_root[2 * a.TB];
-        Th = a.hist_root[2 * a.TB + 1];
+        Tg = a.root_tot ? a.root_tot[0] : a.hist_root[2 * a.TB];
+        Th = a.root_tot ? a.root_tot[1] : a.hist_root[2 * a.TB + 1];
     } else {
         const int pk = (k - 1) / 2;
         const int pslot = pk - ((1 << (a.level - 1)) - 1);
@@ -2478,9 +2488,10 @@ __device__ __forceinline__ void eval_warp(const EvalArgs &a, long long gw) {
     const int sg = a.scale[0], sh = a.scale[1];
     const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
     const double e = ddiv(dmul(G, G), dadd(H, a.p.lambda));
-    const int b0 = __ldg(a.cut_ptr + f), nbf = __ldg(a.cut_ptr + f + 1) - b0;
+    const int fg = a.f0 + f;
+    const int b0 = __ldg(a.cut_ptr + fg), nbf = __ldg(a.cut_ptr + fg + 1) - b0;
     const FeatBest b = eval_feature(src, b0, nbf, Tg, Th, sg, sh, e, a.p);
-    if ((threadIdx.x & 31) == 0) a.fb[gw] = b;
+    if ((threadIdx.x & 31) == 0) a.fb[a.sliced ? (long long)j * a.fsmax + f : gw] = b;
 }
 
 // one block per (node, feature) = blk: the feature's best candidate into fb[blk]
@@ -2493,9 +2504,10 @@ __device__ __forceinline__ NodeKnown eval_block(const EvalArgs &a, long long blk
     const int sg = a.scale[0], sh = a.scale[1];
     const double G = fixed_to_double(Tg, sg), H = fixed_to_double(Th, sh);
     const double e = ddiv(dmul(G, G), dadd(H, a.p.lambda));
-    const int b0 = __ldg(a.cut_ptr + f), nbf = __ldg(a.cut_ptr + f + 1) - b0;
+    const int fg = a.f0 + f;
+    const int b0 = __ldg(a.cut_ptr + fg), nbf = __ldg(a.cut_ptr + fg + 1) - b0;
     const FeatBest b = eval_feature_blk(src, b0, nbf, Tg, Th, sg, sh, e, a.p);
-    if (threadIdx.x == 0) a.fb[blk] = b;
+    if (threadIdx.x == 0) a.fb[a.sliced ? (long long)j * a.fsmax + f : blk] = b;
     return NodeKnown{1, Tg, Th};
 }
 
@@ -2532,8 +2544,19 @@ __device__ FeatBest reduce_node(const EvalArgs &a, int j, int &feat) {
     double bg = 0.0;
     long long bi = LLONG_MAX, blg = 0, blh = 0;
     int bf = -1;  // feature of the best candidate (no binary search over cut_ptr afterwards)
-    for (int f = threadIdx.x; f < a.F; f += E_THREADS) {
-        const FeatBest *cp = a.fb + (long long)j * a.F + f;
+    const int nf_all = a.fb_all ? a.nslices * a.fsmax : a.F;
+    for (int i = threadIdx.x; i < nf_all; i += E_THREADS) {
+        const FeatBest *cp;
+        int f;
+        if (a.fb_all) {  // sliced: rank r's entries for node j, its features slice_f0[r] + fl
+            const int r = i / a.fsmax, fl = i - r * a.fsmax;
+            if (fl >= __ldg(a.slice_nf + r)) continue;
+            cp = a.fb_all + ((long long)r * a.n_nodes + j) * a.fsmax + fl;
+            f = __ldg(a.slice_f0 + r) + fl;
+        } else {
+            cp = a.fb + (long long)j * a.F + i;
+            f = i;
+        }
         FeatBest c;
         c.gain = __ldcg(&cp->gain);
         c.idx = __ldcg(&cp->idx);
@@ -2610,6 +2633,7 @@ __global__ void __launch_bounds__(E_THREADS, GBM_EVAL_MINB) eval_tree_kernel(Eva
     const long long total = (long long)a.n_nodes * a.F;
     const long long gw = ((long long)blockIdx.x * E_THREADS + threadIdx.x) >> 5;
     if (gw < total) eval_warp(a, gw);
+    if (a.sliced) return;  // the finisher runs after the all-gather of fb
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2635,6 +2659,7 @@ __global__ void __launch_bounds__(E_THREADS) eval_tree_blk_kernel(EvalArgs a, Tr
     __shared__ int s_nfin;
     const long long blk = blockIdx.x;
     const NodeKnown kn = eval_block(a, blk);
+    if (a.sliced) return;  // the finisher runs after the all-gather of fb
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2645,6 +2670,35 @@ __global__ void __launch_bounds__(E_THREADS) eval_tree_blk_kernel(EvalArgs a, Tr
     __syncthreads();
     if (s_nfin == 0) return;
     eval_finish(a, t, s_fin, 1, &kn);
+}
+
+// sliced evaluation: one block per node reduces the all-gathered candidates of every rank; the
+// block completing the level plans the next one (eval_finish)
+__global__ void __launch_bounds__(E_THREADS) eval_final_sliced_kernel(EvalArgs a, TreeDev t) {
+    const int fin = blockIdx.x;
+    eval_finish(a, t, &fin, 1, nullptr);
+}
+
+// send[r][slot][CB][2] = this rank's partial histograms cut into the ranks' feature slices
+// (bins bin_lo[r] .. bin_lo[r+1]), zero-padded to the slice capacity CB: the reduce-scatter
+// input of the sliced evaluation
+__global__ void slice_permute_kernel(const long long *__restrict__ hist, int n_slots, long long TB,
+                                     const int *__restrict__ bin_lo, int p, long long CB,
+                                     long long *__restrict__ send) {
+    const long long total = (long long)p * n_slots * CB;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long b = i % CB, rs = i / CB;
+        const int slot = (int)(rs % n_slots), r = (int)(rs / n_slots);
+        const long long g = bin_lo[r] + b;
+        long long vg = 0, vh = 0;
+        if (g < bin_lo[r + 1]) {
+            vg = hist[(slot * TB + g) * 2];
+            vh = hist[(slot * TB + g) * 2 + 1];
+        }
+        send[2 * i] = vg;
+        send[2 * i + 1] = vh;
+    }
 }
 
 __device__ void eval_final_body(const EvalArgs &a, const TreeDev &t, int j, NodeKnown kn) {
@@ -3912,6 +3966,37 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
         need += 2 * (rec_rows_bytes + 256) + 2 * (rec_q_bytes + 256);       // two record buffers
         need += (size_t)(2 * cap + 2) * 2 * 8 + 256;                        // cursors
     }
+    // reduce-scatter + feature-sliced evaluation (§8(f)#1; GBM_OPT_EVAL_SLICED): rank r owns the
+    // contiguous features f0[r] .. f0[r] + nf[r] - 1 (bins balanced), receives only their summed
+    // histograms (ncclReduceScatter instead of ncclAllReduce: half the bytes per rank), evaluates
+    // them, and the ranks all-gather their best candidates before the replicated node reduction
+    const int P = ctx->nranks;
+    const bool sliced = ctx->eval_sliced == 1 && coll_on(ctx) && P > 1 && !rec;
+    std::vector<int> sl_f0(P + 1, 0), sl_nf(P, 0), sl_bin(P + 1, 0);
+    long long CB = 1;
+    int fsmax = 1;
+    if (sliced) {
+        for (int r = 0; r <= P; ++r) {
+            const long long target = (long long)TB * r / P;
+            int f = 0;
+            while (f < F && q->cut_ptr_h[f] < target) ++f;
+            sl_f0[r] = r == P ? F : f;
+        }
+        for (int r = 0; r < P; ++r) {
+            sl_nf[r] = sl_f0[r + 1] - sl_f0[r];
+            sl_bin[r] = q->cut_ptr_h[sl_f0[r]];
+            fsmax = std::max(fsmax, sl_nf[r]);
+        }
+        sl_bin[P] = (int)TB;
+        for (int r = 0; r < P; ++r) CB = std::max<long long>(CB, sl_bin[r + 1] - sl_bin[r]);
+        const size_t sunit = (size_t)CB * 2;
+        need += (size_t)P * slots * sunit * 8 + 512;            // send
+        need += (size_t)slots * sunit * 8 + 512;                // received built slots
+        need += 2 * (size_t)slots * sunit * 8 + 512;            // received level slots x2
+        need += (sunit + 2) * 8 + 512;                          // received root
+        need += (size_t)P * std::max(1, 1 << std::max(0, D - 1)) * 2 * fsmax * sizeof(FeatBest) + 512;
+        need += 3 * (size_t)(P + 1) * 4 + 768;                  // slice tables
+    }
     Arena &A = ctx->tree_arena;
     GBM_TRY(A.reserve(need));
     char *ridx[2] = {nullptr, nullptr};
@@ -3949,10 +4034,74 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     int *seg_base = A.take<int>((size_t)max_par + 1);
     int *seg_items = A.take<int>(2);
     uint32_t *dbits = row_decide ? A.take<uint32_t>((size_t)((n + 31) / 32)) : nullptr;
-
+    long long *sl_send = nullptr, *sl_build = nullptr, *sl_lvl[2] = {nullptr, nullptr}, *sl_root = nullptr;
+    FeatBest *fb_all = nullptr;
+    int *sl_f0_d = nullptr, *sl_nf_d = nullptr, *sl_bin_d = nullptr;
+    const long long sl_shift = sliced ? 2ll * sl_bin[ctx->rank] : 0;  // slice base -> global bin index
+    if (sliced) {
+        const size_t sunit = (size_t)CB * 2;
+        sl_send = A.take<long long>((size_t)P * slots * sunit);
+        sl_build = A.take<long long>((size_t)slots * sunit);
+        sl_lvl[0] = A.take<long long>((size_t)slots * sunit);
+        sl_lvl[1] = A.take<long long>((size_t)slots * sunit);
+        sl_root = A.take<long long>(sunit + 2);
+        fb_all = A.take<FeatBest>((size_t)P * std::max(1, 1 << std::max(0, D - 1)) * 2 * fsmax);
+        sl_f0_d = A.take<int>(P + 1);
+        sl_nf_d = A.take<int>(P + 1);
+        sl_bin_d = A.take<int>(P + 1);
+        std::vector<int> key = {(int)A.generation, (int)(reinterpret_cast<uintptr_t>(sl_f0_d) & 0x7fffffff), P};
+        key.insert(key.end(), sl_f0.begin(), sl_f0.end());
+        key.insert(key.end(), sl_bin.begin(), sl_bin.end());
+        if (key != ctx->tree_slice_key) {  // uploaded once per shape (never inside a graph capture)
+            GBM_CUDA(cudaMemcpyAsync(sl_f0_d, sl_f0.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+            GBM_CUDA(cudaMemcpyAsync(sl_nf_d, sl_nf.data(), P * sizeof(int), cudaMemcpyHostToDevice, s));
+            GBM_CUDA(cudaMemcpyAsync(sl_bin_d, sl_bin.data(), (P + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+            GBM_CUDA(cudaStreamSynchronize(s));  // the host vectors go out of scope
+            ctx->tree_slice_key = key;
+        }
+    }
     GBM_TRY(upload_groups(ctx, hp, groups, cgroups, A, s, root_staged ? &hr : nullptr, cg_root));
     const TreeDev t = tree_dev(tree);
     const double row_bytes = (double)F * q->bits / 8.0;  // algorithmic bytes of one packed row
+    // C2 of the sliced mode: this rank's partial slots -> the summed slots of its feature slice
+    auto slice_reduce = [&](const long long *hist, int n_slots, long long *recv) -> int {
+        const long long total = (long long)P * n_slots * CB;
+        slice_permute_kernel<<<(int)std::min<long long>((total + 255) / 256, 4096), 256, 0, s>>>(
+            hist, n_slots, std::max<long long>(TB, 1), sl_bin_d, P, CB, sl_send);
+        GBM_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        ProfScope ps(ctx, PC_ALLREDUCE, s, (double)n_slots * CB * 16 * P);
+        return coll_reduce_scatter_i64(ctx, sl_send, recv, (size_t)n_slots * CB * 2, s);
+    };
+    // features-only evaluation of this rank's slice, all-gather of the candidates, node reduction
+    auto sliced_eval = [&](EvalArgs e, bool wait_scan) -> int {
+        e.sliced = 1;
+        e.f0 = sl_f0[ctx->rank];
+        e.F = sl_nf[ctx->rank];
+        e.TB = CB;
+        e.fsmax = fsmax;
+        const size_t fbb = (size_t)e.n_nodes * fsmax * sizeof(FeatBest);
+        if (e.F > 0) {
+            ProfScope ps(ctx, PC_EVAL, s, (double)e.n_nodes * CB * 16);
+            GBM_TRY(launch_eval_tree(ctx, e, t, s));
+        }
+        {
+            ProfScope ps(ctx, PC_ALLREDUCE, s, (double)fbb * P);
+            GBM_TRY(coll_allgather(ctx, fb, fb_all, fbb, s));
+        }
+        if (wait_scan) GBM_CUDA(cudaStreamWaitEvent(s, ctx->ev_scan, 0));
+        e.sliced = 0;
+        e.fb_all = fb_all;
+        e.slice_f0 = sl_f0_d;
+        e.slice_nf = sl_nf_d;
+        e.nslices = P;
+        ProfScope ps(ctx, PC_EVAL_FINAL, s);
+        eval_final_sliced_kernel<<<e.n_nodes, E_THREADS, 0, s>>>(e, t);
+        GBM_CUDA(cudaGetLastError());
+        return GBM_OK;
+    };
+
+
     {
         ProfScope ps(ctx, PC_INIT, s);
         init_tree_kernel<<<(int)std::min<long long>((cap + 255) / 256, 1024), 256, 0, s>>>(t, cap, nodes, n);
@@ -4006,7 +4155,13 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     } else if (n > 0) {
         return fail(GBM_E_ARG, "gbm_build_tree: no feature has a cut (all values missing)");
     }
-    {
+    if (sliced) {  // the root's totals (all ranks), its histogram cut into the feature slices
+        {
+            ProfScope ps(ctx, PC_ALLREDUCE, s, 16.0);
+            GBM_TRY(allreduce_i64(ctx, hist_root + hist_unit, 2, s));
+        }
+        GBM_TRY(slice_reduce(hist_root, 1, sl_root));
+    } else {
         ProfScope ps(ctx, PC_ALLREDUCE, s, (double)(hist_unit + 2) * 8);
         GBM_TRY(allreduce_i64(ctx, hist_root, hist_unit + 2, s));
     }
@@ -4060,7 +4215,11 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     ea.done = done;
     ea.node_done = done + 1;
     ea.plan_mode = (1 < D) ? 1 : 0;
-    {
+    if (sliced) {
+        ea.root_tot = hist_root + hist_unit;
+        ea.hist_root = sl_root - sl_shift;
+        GBM_TRY(sliced_eval(ea, false));
+    } else {
         ProfScope ps(ctx, PC_EVAL, s, (double)TB * 16);
         GBM_TRY(launch_eval_tree(ctx, ea, t, s));
     }
@@ -4307,6 +4466,22 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
             sa.rows_ctr = prof_rows_slot(ctx, &slot);
             ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, row_bytes + 8.0 + esz);
             GBM_TRY(GBM_DISPATCH(hp, launch_seg, ctx, hp, sa, s, hp.carry));
+        }
+        if (sliced) {  // reduce-scatter into this rank's feature slice, sliced evaluation
+            GBM_TRY(slice_reduce(hist_build, n_par, sl_build));
+            ea.level = l;
+            ea.first = (1 << l) - 1;
+            ea.n_nodes = 1 << l;
+            ea.hist_build = sl_build - sl_shift;
+            ea.hist_prev = l == 1 ? nullptr : sl_lvl[(l - 1) & 1] - sl_shift;
+            ea.hist_store = (l < D - 1) ? sl_lvl[l & 1] - sl_shift : nullptr;
+            ea.plan_mode = (l + 1 < D) ? 1 : 0;
+            ea.tile_base = tile_base_b[(l + 1) & 1];
+            ea.run_base = run_base_b[(l + 1) & 1];
+            ea.n_items = n_items_b[(l + 1) & 1];
+            GBM_TRY(sliced_eval(ea, !seg_mode));
+            if (!seg_mode) GBM_TRY(wait_on(s, ctx->ev_join, ctx->side));
+            continue;
         }
         {  // AllReduceHistograms
             ProfScope ps(ctx, PC_ALLREDUCE, s, (double)n_par * hist_unit * 8);

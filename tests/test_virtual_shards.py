@@ -70,11 +70,16 @@ CASES = [  # cfg, rows, missing, grow, p
     ("higgs", 30_000, 0.0, "lossguide", 3),
     ("tiny", 2000, 0.0, "depthwise", 8),     # 250-row shards
     ("tiny", 5, 0.0, "depthwise", 8),        # ranks with no rows at all
+    ("tiny", 3000, 0.0, "depthwise", 12),    # more ranks than features: ranks owning no feature
+    ("epsilon", 3000, 0.0, "depthwise", 3),  # 2000 features in three slices
 ]
 
 
+@pytest.mark.parametrize("sliced", [0, 1])
 @pytest.mark.parametrize("cfg,n,missing,grow,p", CASES)
-def test_virtual_shards_equal_oracle_workers(G, cfg, n, missing, grow, p):
+def test_virtual_shards_equal_oracle_workers(G, cfg, n, missing, grow, p, sliced):
+    """sliced = 1: the reduce-scatter + feature-sliced evaluation variant of C2 (GBM_OPT_EVAL_SLICED):
+    each rank evaluates its feature slice, the candidates are all-gathered -- same trees."""
     c = W.CONFIGS[cfg]
     X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
     D = c.max_depth if grow == "depthwise" else 9
@@ -89,6 +94,7 @@ def test_virtual_shards_equal_oracle_workers(G, cfg, n, missing, grow, p):
         oleaf.append(ob.last["row_leaf"].copy())
 
     def body(ctx, k):
+        ctx.set_option(ctx.EVAL_SLICED, sliced)
         lo, hi = W.shard_range(n, k, p)
         gb = G.Booster(ctx, dev(X[lo:hi]), dev(y[lo:hi]), max_bins=c.max_bins, objective=c.objective,
                        max_depth=D, eta=0.3, base_margin=ob.base_margin, grow_policy=grow, max_leaves=L)
