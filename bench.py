@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0 = the host's cores)")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size oracle parity leg")
     ap.add_argument("--no-p30", action="store_true", help="skip the grad_bits = 30 figure")
+    ap.add_argument("--no-full-run", action="store_true",
+                    help="skip the full-training figure (the config's round count, e.g. 500 for Higgs)")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--row-align-bits", type=int, default=32,
                     help="packed row stride rounded up to this many bits (gbm_compress)")
@@ -300,6 +302,9 @@ def run_ours(a, world, rank, local):
     # the committed ncu capture is of the depth-wise bench command: attach it only to that line
     traffic, traffic_src, l1_pct = ncu_traffic(a.config) if a.grow_policy == "depthwise" else (None, None, None)
     roofline = {"bound": "hbm", "kernel": "hist_kernel (root + level launches)",
+                "bytes_definition": "SURVEY 8(d): root n (F b/8 + 8); level: each row of the built child "
+                                    "F b/8 + 12 (packed row, row index, qpair); the fused level kernel's "
+                                    "partition inputs (split symbol + row index per parent row) not counted",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": hist_bytes / max(1, hist_launches),
@@ -384,6 +389,13 @@ def run_ours(a, world, rank, local):
                        "amortised per round"}
         del b2, Xd, yd, g2
 
+    # ---- the whole training of the config (e.g. 500 rounds for Higgs) from a fresh booster: the
+    # per-round cost falls as training proceeds (later trees split off smaller children, so fewer
+    # rows are histogrammed), so a K-step window early in training is not the training's average
+    full = None
+    if not a.no_full_run and a.grow_policy == "depthwise":
+        full = time_full_training(G, ctx, torch, Xd_keep, yd_keep, kw, a, stream, barrier, max_over_ranks,
+                                  cfg.n_rounds)
     # ---- grad_bits = 30 (SURVEY §8(c) Q4's s = 30 - E): the same timed graph protocol
     p30 = None
     if not a.no_p30 and a.grad_bits != 30 and a.grow_policy == "depthwise":
@@ -395,7 +407,7 @@ def run_ours(a, world, rank, local):
     cpu = parity = None
     if rank == 0 and world == 1 and not (a.no_cpu_baseline and a.no_parity):
         cpu, parity = cpu_baseline_and_parity(G, ctx, torch, dev, X, y, kw, a)
-    return dict(p30=p30, parity=parity, ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages, l2=l2_note,
+    return dict(p30=p30, parity=parity, full=full, ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages, l2=l2_note,
                 one_time=one_time, clocks=clk, launches=launches, e2e=e2e, cpu=cpu,
                 predict_ms=predict_ms, allreduce_ms=allreduce_ms, grad_bits=a.grad_bits)
 
@@ -412,6 +424,32 @@ def host_facts():
     except OSError:
         pass
     return nproc, model
+
+
+def time_full_training(G, ctx, torch, Xd, yd, kw, a, stream, barrier, max_over_ranks, rounds):
+    """Seconds per round averaged over a whole training of `rounds` rounds: one eager round, then
+    rounds - 1 replays of the captured round, all inside one pair of CUDA events."""
+    b = G.Booster(ctx, Xd, yd, **kw)
+    side = torch.cuda.Stream()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    b.round(keep_tree=False)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            b.round(keep_tree=False)
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(rounds - 1):
+        g.replay()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    del g, b
+    return {"rounds": rounds, "total_s": ms / 1e3, "value": ms / 1e3 / rounds, "unit": "s/round",
+            "note": "a fresh booster trained for the config's full round count (BASELINE.json), one "
+                    "eager round + graph replays, the capture itself included; total / rounds"}
 
 
 def time_precision(G, ctx, torch, dev, Xd, yd, kw, a, stream, barrier, max_over_ranks, bits):
@@ -615,6 +653,7 @@ def main():
             "cpu_baseline": r["cpu"],
             "parity": r["parity"],
             "grad_bits_30": r["p30"],
+            "full_training": r["full"],
             "e2e": r["e2e"],
             "gpu_launches": r["launches"],
             "clocks": r["clocks"],

@@ -4378,9 +4378,11 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
             fa.ridx_in = rin;
             int slot;
             fa.rows_ctr = prof_rows_slot(ctx, &slot);
-            // algorithmic bits: split symbol + ridx per parent row; packed row + qpair per built row
-            fa.bits_parent_row = q->bits + (rin ? 32 : 0);
-            fa.bits_built_row = F * q->bits + 64;
+            // algorithmic bits of the histogram: per row of the built child its packed
+            // row + row index + qpair (F b / 8 + 12 bytes); the partition inputs the fused kernel also
+            // reads (split symbol + row index per parent row) are §8(d)'s partition bytes, not counted
+            fa.bits_parent_row = 0;
+            fa.bits_built_row = F * q->bits + 96;
             ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
             if (hp.col) {
                 ColFusedArgs ca = {};

@@ -1,6 +1,9 @@
-"""Summarise an ncu --set full capture of the histogram kernels into profiles/ (md + json)."""
+"""Summarise an ncu --set full capture of the histogram kernels into profiles/ (md + json).
+usage: ncu_hist_summary.py REPORT TAG [capture description]"""
 import csv, subprocess, io, json, sys
 rep, tag = sys.argv[1], sys.argv[2]
+capture = sys.argv[3] if len(sys.argv) > 3 else "bench.py --steps 3 --warmup 3, Higgs 11M x 28, one round = root + 5 level launches"
+PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if __import__("os").path.exists("MEASURED_PEAKS.json") else 6546.6
 raw=subprocess.run(['ncu','-i',rep,'--page','raw','--csv'],capture_output=True,text=True).stdout
 rows=list(csv.reader(io.StringIO(raw))); hdr=rows[0]; units=rows[1]
 def find(name):
@@ -24,15 +27,20 @@ def tof(x):
     try: return float(x.split(' ')[0].replace(',',''))
     except Exception: return None
 l1=[tof(d['l1']) for d in out]
-summary={"source":f"ncu --set full (profiles/{tag}_ncu_hist_summary.md): bench.py --steps 3 --warmup 3, Higgs 11M x 28, one round = root + 5 level launches",
+def tous(x):
+    v,u=x.split(' ',1); v=float(v.replace(',',''))
+    return v*{'nsecond':1e-3,'usecond':1.0,'msecond':1e3,'ns':1e-3,'us':1.0,'ms':1e3}[u.strip()]
+times=[tous(d['time']) for d in out]
+for d,t,us in zip(out,tr,times):
+    d['dpct']=f"{100*t/(us*1e-6)/1e9/PEAK:.1f} %"
+summary={"source":f"ncu --set full (profiles/{tag}_ncu_hist_summary.md): {capture}",
          "dram_bytes_per_launch": sum(tr)/len(tr),
          "l1tex_pct_of_peak_active_mean": sum(v for v in l1 if v is not None)/max(1,len([v for v in l1 if v is not None])),
-         "launches": [ {"kernel":d['kernel'], "dram_bytes": t, "l1tex_pct_active": l, "smem_atom_wavefronts": tof(d['aw']),
-                        "smem_atom_bank_conflicts": tof(d['ac'])} for d,t,l in zip(out,tr,l1)]}
+         "launches": [ {"kernel":d['kernel'], "dram_bytes": t, "time_us": us, "l1tex_pct_active": l, "smem_atom_wavefronts": tof(d['aw']),
+                        "smem_atom_bank_conflicts": tof(d['ac'])} for d,t,l,us in zip(out,tr,l1,times)]}
 json.dump(summary, open('profiles/ncu_hist_higgs.json','w'), indent=1)
 lines=[f"# {tag} ncu --set full: histogram kernels, one boosting round (Higgs-shaped 11M x 28, depth 6)","",
-"Capture: `ncu --set full --clock-control none --import-source on -k regex:\"hist_cs_range|hist_range|part_hist\" -s 6 -c 6`",
-"on `python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline` (round 2: root + levels 1..5).  The .ncu-rep",
+f"Capture: {capture}.  DRAM % of peak = (read + write) / duration / {PEAK} GB/s (MEASURED_PEAKS.json).  The .ncu-rep",
 "stays in gpurun_out/ (scratch); this table is the committed summary.","",
 "| launch | kernel | time | DRAM read | DRAM write | DRAM % of peak | L1/TEX % (active) | smem atom wavefronts | of which bank conflicts | warp instr | regs | dyn smem |",
 "|---|---|---|---|---|---|---|---|---|---|---|---|"]
