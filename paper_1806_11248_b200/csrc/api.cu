@@ -306,7 +306,8 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         return GBM_OK;
     }
     if (option == GBM_OPT_LEVEL_HIST) {
-        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_LEVEL_HIST: 0 auto, 1 compact, 2 bank-column");
+        if (value < 0 || value > 3)
+            return fail(GBM_E_ARG, "GBM_OPT_LEVEL_HIST: 0 auto, 1 compact, 2 bank-column, 3 warp-specialised compact");
         ctx->level_hist = (int)value;
         return GBM_OK;
     }

@@ -679,6 +679,166 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
     }
 }
 
+// ============================================================== warp-specialised levels
+// GBM_OPT_LEVEL_HIST = 3: the fused level kernel with the partition and the histogram in
+// different warps.  ncu on part_hist_kernel (profiles/r02): at the deep levels ~30 % of the stall
+// samples wait on the split-symbol gather of the partition phase (ridx -> symbol: two dependent
+// DRAM latencies per tile) and ~14 % on the built rows' word gathers, with each warp alternating
+// both phases.  Here WS_NP producer warps decide tile t + 1 (16 rows in flight per lane) while the
+// consumer warps accumulate tile t from the producers' lists: named barriers full[b] / empty[b]
+// hand the double-buffered lists over.  Compact layout, byte symbols, one feature group.
+constexpr int WS_NP = 4;               // producer warps
+constexpr int WS_NC = H_THREADS / 32 - WS_NP;  // consumer warps
+constexpr int WS_PROWS = PT / WS_NP;   // rows per producer warp per tile (512)
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <bool WIDE, bool SENT>
+__global__ void __launch_bounds__(H_THREADS, 2) part_hist_ws_kernel(FusedArgs a) {
+    extern __shared__ int smem[];
+    __shared__ int s_off[2049];
+    __shared__ uint32_t s_list[2][WS_NP][WS_PROWS];
+    __shared__ int s_cnt[2][WS_NP];
+    const QM &qm = a.qm;
+    const uint32_t *rin = static_cast<const uint32_t *>(a.ridx_in);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool producer = wid < WS_NP;
+    const int n_items = *a.n_items;
+    const uint32_t ltm = (1u << lane) - 1u;
+    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_items;
+         it = claim_item(const_cast<int *>(a.n_items) + 1)) {
+        const int run = it;
+        const int j = find_parent(a.run_base, a.n_par, run);
+        const int k = a.first + j;
+        const NodeDev nd = a.nodes[k];
+        const int tb = a.tile_base[j];
+        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const long long seg_end = nd.start + nd.count;
+        if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
+            for (int t = t0; t < t1; ++t) {
+                const long long base = nd.start + (long long)(t - tb) * PT;
+                for (int i = threadIdx.x; i < PT; i += H_THREADS) {
+                    const long long pos = base + i;
+                    if (pos < seg_end) a.row_leaf[rin ? rin[pos] : (uint32_t)pos] = k;
+                }
+            }
+            continue;
+        }
+        const Group grp = a.groups[0];
+        SmemHist h{smem, grp.bin_hi - grp.bin_lo, a.hstride};
+        smem_zero<WIDE>(h);
+        load_group(qm, grp, a.cut_ptr, s_off);
+        __syncthreads();
+        const bool build_left = nd.build_left != 0;
+        const int nt = t1 - t0;
+        if (producer) {
+            unsigned long long bits_acc = 0;
+            for (int i = 0; i < nt; ++i) {
+                const int t = t0 + i, b = i & 1;
+                if (i >= 2) named_sync(3 + b, H_THREADS);  // consumers are done with buffer b
+                const long long base = nd.start + (long long)(t - tb) * PT + wid * WS_PROWS;
+                uint32_t row[16];
+                bool left[16];
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) {
+                    const long long pos = base + s2 * 32 + lane;
+                    row[s2] = pos < seg_end ? (rin ? __ldg(rin + pos) : (uint32_t)pos) : 0u;
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) left[s2] = base + s2 * 32 + lane < seg_end && goes_left(qm, nd, row[s2]);
+                int nleft = 0, nbuild = 0;
+                uint32_t *lst = s_list[b][wid];
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) {
+                    const bool valid = base + s2 * 32 + lane < seg_end;
+                    const uint32_t lw2 = __ballot_sync(0xffffffffu, valid && left[s2]);
+                    const uint32_t bw = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
+                    if (lane == 0) a.flags[(long long)t * (PT / 32) + wid * 16 + s2] = lw2;
+                    nleft += __popc(lw2);
+                    if ((bw >> lane) & 1u) lst[nbuild + __popc(bw & ltm)] = row[s2];
+                    nbuild += __popc(bw);
+                }
+                if (lane == 0) {
+                    s_cnt[b][wid] = nbuild;
+                    if (nleft) atomicAdd(a.tile_left + t, nleft);
+                    if (a.rows_ctr) bits_acc += (unsigned long long)nbuild * a.bits_built_row;
+                }
+                __threadfence_block();
+                named_arrive(1 + b, H_THREADS);  // list b of tile t is ready
+            }
+            for (int i = max(0, nt - 2); i < nt; ++i) named_sync(3 + (i & 1), H_THREADS);  // balance the empties
+            if (lane == 0 && bits_acc) atomicAdd(a.rows_ctr, bits_acc);
+        } else {
+            const int cw = wid - WS_NP;
+            const int Ug = grp.u_hi - grp.u_lo;
+            const int rpp = 32 / Ug;
+            const int my_r = lane < rpp * Ug ? lane / Ug : -1;
+            const int my_u = grp.u_lo + (lane - (my_r < 0 ? 0 : my_r) * Ug);
+            const int f_lo = grp.u_lo * qm.S;
+            int off[4] = {h.nb, h.nb, h.nb, h.nb};
+            if (my_r >= 0) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int f = my_u * 4 + jj;
+                    if (f < qm.F) off[jj] = s_off[f - f_lo];
+                }
+            }
+            const long long sw = qm.stride >> 5;
+            for (int i = 0; i < nt; ++i) {
+                const int b = i & 1;
+                named_sync(1 + b, H_THREADS);  // the producers' lists of this tile
+                int pre[WS_NP + 1];
+                pre[0] = 0;
+#pragma unroll
+                for (int w = 0; w < WS_NP; ++w) pre[w + 1] = pre[w] + s_cnt[b][w];
+                const int N = pre[WS_NP];
+                const int k0 = (int)((long long)cw * N / WS_NC), k1 = (int)((long long)(cw + 1) * N / WS_NC);
+                auto entry = [&](int kk) -> uint32_t {
+                    int w = 0;
+#pragma unroll
+                    for (int q = 1; q < WS_NP; ++q) w += kk >= pre[q];
+                    return s_list[b][w][kk - pre[w]];
+                };
+                if (my_r >= 0) {
+                    int rr = k0 + my_r;
+                    for (; rr + (PH_UNR - 1) * rpp < k1; rr += PH_UNR * rpp) {
+                        uint32_t wd[PH_UNR];
+                        int2 qq[PH_UNR];
+#pragma unroll
+                        for (int u = 0; u < PH_UNR; ++u) {
+                            const uint32_t r = entry(rr + u * rpp);
+                            wd[u] = __ldg(qm.P + r * sw + my_u);
+                            qq[u] = __ldg(a.qpair + r);
+                        }
+#pragma unroll
+                        for (int u = 0; u < PH_UNR; ++u)
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj) {
+                                const int sy = (wd[u] >> (8 * jj)) & 255;
+                                if (!SENT || sy != qm.B) hist_add<WIDE>(h.base, h.hstride, off[jj] + sy, qq[u]);
+                            }
+                    }
+                    for (; rr < k1; rr += rpp) {
+                        const uint32_t r = entry(rr);
+                        const uint32_t wa = __ldg(qm.P + r * sw + my_u);
+                        const int2 qa = __ldg(a.qpair + r);
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int sa = (wa >> (8 * jj)) & 255;
+                            if (!SENT || sa != qm.B) hist_add<WIDE>(h.base, h.hstride, off[jj] + sa, qa);
+                        }
+                    }
+                }
+                named_arrive(3 + b, H_THREADS);  // buffer b may be refilled
+            }
+        }
+        __syncthreads();
+        smem_flush<WIDE>(h, a.hist + ((long long)j * a.TB + grp.bin_lo) * 2);
+        __syncthreads();
+    }
+}
+
 // ============================================================== shuffle-fed bank-column levels
 // The fused level kernel for byte symbols with every feature in one group (F <= 32, rows of U
 // whole words): the partition phase is part_hist_kernel's; the built rows are fetched exactly as
@@ -4185,6 +4345,22 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     const bool sb_ok = !hp.col && hp.byte_path && G == 1 && F <= 32 && qm.stride == 32ll * ((F + 3) / 4) &&
                        !hp.carry && !seg_mode;
     const bool sb_levels = sb_ok && ctx->level_hist == 2;
+    // warp-specialised compact level kernel (part_hist_ws_kernel): byte symbols, one group
+    const bool ws_levels = !hp.col && hp.byte_path && G == 1 && !hp.carry && !seg_mode && ctx->level_hist == 3;
+    int ws_grid = 1;
+    if (ws_levels) {
+        int occ = 0;
+        auto setk = [&](auto kern) -> int {
+            GBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hp.smem_bytes));
+            GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, H_THREADS, hp.smem_bytes));
+            return GBM_OK;
+        };
+        if (hp.wide) GBM_TRY(setk(part_hist_ws_kernel<true, false>));
+        else if (hp.sent) GBM_TRY(setk(part_hist_ws_kernel<false, true>));
+        else GBM_TRY(setk(part_hist_ws_kernel<false, false>));
+        GBM_REQUIRE(occ >= 1, GBM_E_ARG, "warp-specialised level kernel cannot be resident");
+        ws_grid = occ * ctx->sm_count;
+    }
     int sb_grid = 1;
     if (sb_levels) {
         const size_t smb = (size_t)(hp.wide ? 4 : 2) * COLB_STRIDE * 4;
@@ -4410,6 +4586,11 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
                 ca.bits_parent_row = fa.bits_parent_row;
                 ca.bits_built_row = fa.bits_built_row;
                 launch_col_fused(hp, ca, s);
+                GBM_CUDA(cudaGetLastError());
+            } else if (ws_levels) {  // warp-specialised levels
+                if (hp.wide) part_hist_ws_kernel<true, false><<<ws_grid, H_THREADS, hp.smem_bytes, s>>>(fa);
+                else if (hp.sent) part_hist_ws_kernel<false, true><<<ws_grid, H_THREADS, hp.smem_bytes, s>>>(fa);
+                else part_hist_ws_kernel<false, false><<<ws_grid, H_THREADS, hp.smem_bytes, s>>>(fa);
                 GBM_CUDA(cudaGetLastError());
             } else if (sb_levels) {  // shuffle-fed bank-column levels
                 const size_t smb = (size_t)(hp.wide ? 4 : 2) * COLB_STRIDE * 4;

@@ -364,7 +364,7 @@ def test_record_levels_parity(ctx, G, cfg, n, missing, align, P, B, depth, path)
     ctx.set_option(ctx.LEVEL_PATH, 0)
 
 
-@pytest.mark.parametrize("level_hist", [1, 2])
+@pytest.mark.parametrize("level_hist", [1, 2, 3])
 @pytest.mark.parametrize("cfg,n,missing,align,P,B,depth", REC_CASES + [("higgs", 150_000, 0.0, 32, 15, None, 8)])
 def test_level_hist_layouts_parity(ctx, G, cfg, n, missing, align, P, B, depth, level_hist):
     """GBM_OPT_LEVEL_HIST 2 (bank-column level histograms fed by warp shuffles) and 1 (compact),
