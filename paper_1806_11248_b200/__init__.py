@@ -333,6 +333,7 @@ class Context:
     LEVEL_PATH = 12
     LEVEL_HIST = 13
     EVAL_SLICED = 14
+    CUTS_GATHER = 15
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

@@ -25,6 +25,7 @@ struct gbm_vcomm {
     int arrived = 0;
     unsigned long long gen = 0;
     std::vector<const void *> posted;
+    std::vector<const size_t *> posted_off;  // all-to-all: each rank's per-destination offsets
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     int err = GBM_OK;  // rank 0's result of the current collective, read by every rank
@@ -145,6 +146,42 @@ int coll_allgather(gbm_ctx *ctx, const void *send, void *recv, size_t bytes, cud
     });
 }
 
+// All-to-all of float pieces: this rank sends scnt[d] floats at send + soff[d] to rank d and
+// receives rcnt[q] floats from rank q at recv + roff[q] (host arrays of p entries; C3 of the
+// per-feature cut ownership).  NCCL: grouped ncclSend / ncclRecv.
+int coll_alltoallv_f32(gbm_ctx *ctx, const float *send, const size_t *soff, const size_t *scnt, float *recv,
+                       const size_t *roff, const size_t *rcnt, cudaStream_t s) {
+    const int p = ctx->nranks, me = ctx->rank;
+    if (!coll_on(ctx) || p == 1) {
+        if (scnt[0]) GBM_CUDA(cudaMemcpyAsync(recv + roff[0], send + soff[0], scnt[0] * 4, cudaMemcpyDeviceToDevice, s));
+        return GBM_OK;
+    }
+    if (ctx->comm) {
+        GBM_NCCL(ncclGroupStart());
+        for (int q = 0; q < p; ++q) {
+            if (scnt[q]) GBM_NCCL(ncclSend(send + soff[q], scnt[q], ncclFloat32, q, ctx->comm, s));
+            if (rcnt[q]) GBM_NCCL(ncclRecv(recv + roff[q], rcnt[q], ncclFloat32, q, ctx->comm, s));
+        }
+        GBM_NCCL(ncclGroupEnd());
+        return GBM_OK;
+    }
+    // virtual: every rank posts its send buffer and offsets, then copies its pieces from the peers'
+    gbm_vcomm *v = ctx->vcomm;
+    if (capturing(s)) return fail(GBM_E_STATE, "virtual communicator: collectives cannot be graph-captured");
+    GBM_CUDA(cudaStreamSynchronize(s));
+    v->posted[me] = send;
+    v->posted_off[me] = soff;
+    vc_barrier(v);
+    int err = GBM_OK;
+    for (int q = 0; q < p && err == GBM_OK; ++q)
+        if (rcnt[q] && cudaMemcpyAsync(recv + roff[q], static_cast<const float *>(v->posted[q]) + v->posted_off[q][me],
+                                       rcnt[q] * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            err = GBM_E_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) err = GBM_E_CUDA;
+    vc_barrier(v);  // the peers' buffers may be released after this
+    return err == GBM_OK ? GBM_OK : fail(err, "virtual all-to-all failed");
+}
+
 // Sum of every rank's send[p][count] (int64) with chunk r delivered to rank r's recv[count]
 // (ncclReduceScatter; the reduce-scatter + feature-sliced evaluation variant of C2).
 int coll_reduce_scatter_i64(gbm_ctx *ctx, const long long *send, long long *recv, size_t count, cudaStream_t s) {
@@ -230,6 +267,7 @@ int gbm_vcomm_create(int nranks, gbm_vcomm **out) {
     gbm_vcomm *v = new gbm_vcomm();
     v->nranks = nranks;
     v->posted.assign(nranks, nullptr);
+    v->posted_off.assign(nranks, nullptr);
     cudaGetDevice(&v->device);
     *out = v;
     return GBM_OK;

@@ -120,7 +120,8 @@ struct gbm_ctx {
     int row_decide = 0;            // GBM_OPT_ROW_DECIDE (2 on; measured slower, off by default)
     int level_path = 0;
     int level_hist = 0;
-    int eval_sliced = 0;           // GBM_OPT_EVAL_SLICED (1: reduce-scatter + feature-sliced evaluation)            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed bank-column)            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
+    int eval_sliced = 0;
+    int cuts_gather = 0;           // GBM_OPT_CUTS_GATHER (1: C3 as an all-gather of X, not per-feature ownership)           // GBM_OPT_EVAL_SLICED (1: reduce-scatter + feature-sliced evaluation)            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed bank-column)            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     std::vector<int> tree_slice_key;   // feature-slice tables currently uploaded (sliced evaluation)
@@ -159,6 +160,8 @@ enum CollOp { COLL_SUM_I64 = 0, COLL_MAX_U64 = 1, COLL_MAX_I64 = 2 };
 bool coll_on(const gbm_ctx *ctx);  // an NCCL or virtual communicator is attached
 int coll_allreduce(gbm_ctx *ctx, void *buf, size_t count, CollOp op, cudaStream_t s);
 int coll_allgather(gbm_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank, cudaStream_t s);
+int coll_alltoallv_f32(gbm_ctx *ctx, const float *send, const size_t *soff, const size_t *scnt, float *recv,
+                       const size_t *roff, const size_t *rcnt, cudaStream_t s);
 int coll_reduce_scatter_i64(gbm_ctx *ctx, const long long *send, long long *recv, size_t count_per_rank,
                             cudaStream_t s);
 int coll_agree(gbm_ctx *ctx, int local_code, const long long *sig, int nsig, cudaStream_t s, const char *where);

@@ -461,57 +461,13 @@ int gbm_quantise_compress(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_
     return GBM_OK;
 }
 
-int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t max_bins,
-             float *cut_values_d, int32_t *cut_ptr_d, int32_t *n_cuts_h, int32_t *max_symbol_h,
-             void *stream) {
-    GBM_TRY(ctx_enter(ctx));
-    GBM_REQUIRE(F > 0 && max_bins >= 2 && max_bins <= 65535 && cut_values_d && cut_ptr_d &&
-                    n_cuts_h && max_symbol_h && n_rows >= 0 && (X_d || n_rows == 0),
-                GBM_E_ARG, "gbm_cuts: bad arguments");
-    cudaStream_t s = (cudaStream_t)stream;
-    // ---- global rows: all-gather the shards (C3), padded to the largest shard with NaN
-    long long n_total = n_rows, n_max = n_rows;
-    const float *Xg = X_d;
-    float *gathered = nullptr;
-    if (coll_on(ctx)) {
-        long long *tmp;
-        GBM_CUDA(cudaMallocAsync((void **)&tmp, 2 * sizeof(long long), s));
-        long long h2[2] = {n_rows, n_rows};
-        GBM_CUDA(cudaMemcpyAsync(tmp, h2, sizeof(h2), cudaMemcpyHostToDevice, s));
-        int rc = coll_allreduce(ctx, tmp, 1, COLL_SUM_I64, s);
-        if (rc == GBM_OK) rc = coll_allreduce(ctx, tmp + 1, 1, COLL_MAX_I64, s);
-        if (rc == GBM_OK && cudaMemcpyAsync(h2, tmp, sizeof(h2), cudaMemcpyDeviceToHost, s) != cudaSuccess)
-            rc = fail(GBM_E_CUDA, "gbm_cuts: copy of the global row counts");
-        if (rc == GBM_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = fail(GBM_E_CUDA, "gbm_cuts: sync");
-        cudaFreeAsync(tmp, s);
-        if (rc != GBM_OK) return rc;
-        n_total = h2[0];
-        n_max = h2[1];
-        size_t slab = (size_t)n_max * F;
-        float *mine = nullptr;
-        if (cudaMallocAsync((void **)&gathered, std::max<size_t>(slab, 1) * ctx->nranks * sizeof(float), s) != cudaSuccess ||
-            cudaMallocAsync((void **)&mine, std::max<size_t>(slab, 1) * sizeof(float), s) != cudaSuccess) {
-            cudaGetLastError();
-            if (gathered) cudaFreeAsync(gathered, s);
-            return fail(GBM_E_NOMEM, "gbm_cuts: cannot allocate the gathered rows");
-        }
-        cudaMemsetAsync(mine, 0xff, slab * sizeof(float), s);  // 0xffffffff is a NaN
-        if (n_rows) cudaMemcpyAsync(mine, X_d, (size_t)n_rows * F * sizeof(float), cudaMemcpyDeviceToDevice, s);
-        rc = coll_allgather(ctx, mine, gathered, slab * sizeof(float), s);  // C3
-        cudaFreeAsync(mine, s);
-        if (rc != GBM_OK) {
-            cudaFreeAsync(gathered, s);
-            return rc;
-        }
-        Xg = gathered;
-        n_max = n_max * ctx->nranks;  // rows of the gathered buffer (padding rows are all-NaN)
-    }
-    if (n_total <= 0) {
-        if (gathered) cudaFreeAsync(gathered, s);
-        return fail(GBM_E_EMPTY, "gbm_cuts: zero rows");
-    }
-    const long long n_all = n_max;  // rows present in Xg
-    ProfScope ps(ctx, PC_CUTS, s, (double)n_total * F * 4);
+// The exact cuts (R5) of the F columns of Xg ([n_all][F] row-major, NaN = missing, padding rows
+// all-NaN) into cut_values_d / cut_ptr_d; on the host: each feature's bin count nb[f] and present
+// value count pres[f].  GBM_E_NONFINITE on +-inf.  Synchronises s.
+static int cuts_core(gbm_ctx *ctx, const float *Xg, long long n_all, int F, int max_bins, float *cut_values_d,
+                     int32_t *cut_ptr_d, std::vector<int32_t> &nb, std::vector<unsigned long long> &pres,
+                     cudaStream_t s) {
+    ProfScope ps(ctx, PC_CUTS, s, (double)n_all * F * 4);
     const int tiles = (int)((n_all + SORT_TILE - 1) / SORT_TILE);
     const long long n_pad = (long long)tiles * SORT_TILE;
     Arena &A = ctx->arena;
@@ -550,17 +506,240 @@ int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t 
     write_cuts_kernel<<<sg, SORT_THREADS, 0, s>>>(kA, n_pad, tiles, run_off, nbins, tmp, max_bins,
                                                   cut_ptr_d, cut_values_d);
     GBM_CUDA(cudaGetLastError());
-    std::vector<int32_t> nb(F);
-    std::vector<unsigned long long> pres(F);
+    nb.assign(F, 0);
+    pres.assign(F, 0);
     uint32_t err = 0;
     GBM_CUDA(cudaMemcpyAsync(nb.data(), nbins_plain, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
     GBM_CUDA(cudaMemcpyAsync(pres.data(), present, (size_t)F * 8, cudaMemcpyDeviceToHost, s));
     GBM_CUDA(cudaMemcpyAsync(&err, ctx->dev_err, 4, cudaMemcpyDeviceToHost, s));
-    if (gathered) GBM_CUDA(cudaFreeAsync(gathered, s));
     GBM_CUDA(cudaStreamSynchronize(s));
     if (err & DERR_NONFINITE) {
         cudaMemsetAsync(ctx->dev_err, 0, 4, s);
         return fail(GBM_E_NONFINITE, "gbm_cuts: +-inf feature value (S:32)");
+    }
+    return GBM_OK;
+}
+
+// C3 by per-feature ownership: feature f belongs to rank f mod p; every rank sends
+// each owner its shard's columns of the owner's features (all-to-all), the owner computes their
+// exact cuts over the global rows, and the ranks all-gather the cuts.  Per-rank memory and traffic
+// O(n F / p) instead of the O(n F) of an all-gather of X.
+__global__ void owned_columns_kernel(const float *__restrict__ X, long long n, int F, int p,
+                                     float *__restrict__ out /* [p][n][F_d] */) {
+    // destination d holds features d, d + p, ...; its block starts at n * (features of ranks < d)
+    const long long total = n * (long long)F;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / F;
+        const int f = (int)(e - i * F);
+        const int d = f % p, c = f / p;
+        const int Fd = (F - d + p - 1) / p;
+        long long before = 0;  // features owned by ranks < d
+        for (int q = 0; q < d; ++q) before += (F - q + p - 1) / p;
+        out[n * before + i * Fd + c] = X[e];
+    }
+}
+
+// gathered per-rank results -> the global cut arrays in feature order
+__global__ void assemble_cuts_kernel(const float *__restrict__ vals /* [p][Fo][B] */, const int32_t *__restrict__ cnt /* [p][Fo] */,
+                                     int F, int p, int Fo, int B, const int32_t *__restrict__ cut_ptr,
+                                     float *__restrict__ cut_values) {
+    for (int f = blockIdx.x; f < F; f += gridDim.x) {
+        const int r = f % p, c = f / p;
+        const int nbf = cnt[r * Fo + c];
+        const float *src = vals + ((long long)r * Fo + c) * B;
+        for (int k = threadIdx.x; k < nbf; k += blockDim.x) cut_values[cut_ptr[f] + k] = src[k];
+    }
+}
+
+static int cuts_by_ownership(gbm_ctx *ctx, const float *X_d, long long n_rows, int F, int max_bins, float *cut_values_d,
+                             int32_t *cut_ptr_d, std::vector<int32_t> &nb, std::vector<unsigned long long> &pres,
+                             long long &n_total, cudaStream_t s) {
+    const int p = ctx->nranks, r = ctx->rank;
+    auto owned = [&](int q) { return q < F ? (F - q + p - 1) / p : 0; };
+    const int Fr = owned(r), Fo = std::max(1, owned(0));  // rank 0 owns the most features
+    // every rank's row count
+    std::vector<long long> ns(p);
+    long long *d_n = nullptr;
+    GBM_CUDA(cudaMalloc(&d_n, (size_t)(p + 1) * 8));
+    struct Free {
+        std::vector<void *> v;
+        ~Free() { for (void *x : v) cudaFree(x); }
+    } fr;
+    fr.v.push_back(d_n);
+    GBM_CUDA(cudaMemcpyAsync(d_n + p, &n_rows, 8, cudaMemcpyHostToDevice, s));
+    GBM_TRY(coll_allgather(ctx, d_n + p, d_n, 8, s));
+    GBM_CUDA(cudaMemcpyAsync(ns.data(), d_n, (size_t)p * 8, cudaMemcpyDeviceToHost, s));
+    GBM_CUDA(cudaStreamSynchronize(s));
+    n_total = 0;
+    for (long long v : ns) n_total += v;
+    if (n_total <= 0) return fail(GBM_E_EMPTY, "gbm_cuts: zero rows");
+    // all-to-all of the owned columns: to rank d, [n_rows][F_d]; from rank q, [ns[q]][F_r]
+    std::vector<size_t> soff(p), scnt(p), roff(p), rcnt(p);
+    size_t o = 0;
+    for (int d = 0; d < p; ++d) {
+        soff[d] = o;
+        scnt[d] = (size_t)n_rows * owned(d);
+        o += scnt[d];
+    }
+    o = 0;
+    for (int q = 0; q < p; ++q) {
+        roff[q] = o;
+        rcnt[q] = (size_t)ns[q] * Fr;
+        o += rcnt[q];
+    }
+    float *sendb = nullptr, *recvb = nullptr;
+    GBM_CUDA(cudaMalloc(&sendb, std::max<size_t>((size_t)n_rows * F, 1) * 4));
+    fr.v.push_back(sendb);
+    GBM_CUDA(cudaMalloc(&recvb, std::max<size_t>((size_t)n_total * Fr, 1) * 4));
+    fr.v.push_back(recvb);
+    if (n_rows > 0) {
+        owned_columns_kernel<<<grid_for(n_rows * (long long)F, 256, ctx->sm_count), 256, 0, s>>>(X_d, n_rows, F, p, sendb);
+        GBM_CUDA(cudaGetLastError());
+    }
+    GBM_TRY(coll_alltoallv_f32(ctx, sendb, soff.data(), scnt.data(), recvb, roff.data(), rcnt.data(), s));
+    // this rank's features over the global rows
+    const size_t vbytes = (size_t)Fo * max_bins * 4;
+    float *vals = nullptr, *gvals = nullptr;
+    int32_t *cnt = nullptr, *gcnt = nullptr, *lptr = nullptr, *gptr = nullptr;
+    unsigned long long *pr = nullptr, *gpr = nullptr;
+    GBM_CUDA(cudaMalloc(&vals, vbytes));
+    fr.v.push_back(vals);
+    GBM_CUDA(cudaMalloc(&gvals, vbytes * p));
+    fr.v.push_back(gvals);
+    GBM_CUDA(cudaMalloc(&cnt, (size_t)Fo * 4));
+    fr.v.push_back(cnt);
+    GBM_CUDA(cudaMalloc(&gcnt, (size_t)Fo * 4 * p));
+    fr.v.push_back(gcnt);
+    GBM_CUDA(cudaMalloc(&pr, (size_t)Fo * 8));
+    fr.v.push_back(pr);
+    GBM_CUDA(cudaMalloc(&gpr, (size_t)Fo * 8 * p));
+    fr.v.push_back(gpr);
+    GBM_CUDA(cudaMalloc(&lptr, (size_t)(Fo + 1) * 4));
+    fr.v.push_back(lptr);
+    GBM_CUDA(cudaMalloc(&gptr, (size_t)(F + 1) * 4));
+    fr.v.push_back(gptr);
+    GBM_CUDA(cudaMemsetAsync(vals, 0, vbytes, s));
+    GBM_CUDA(cudaMemsetAsync(cnt, 0, (size_t)Fo * 4, s));
+    GBM_CUDA(cudaMemsetAsync(pr, 0, (size_t)Fo * 8, s));
+    std::vector<int32_t> lnb;
+    std::vector<unsigned long long> lpres;
+    int rc = GBM_OK;
+    if (Fr > 0) {
+        float *lcv = nullptr;
+        GBM_CUDA(cudaMalloc(&lcv, (size_t)Fr * max_bins * 4));
+        fr.v.push_back(lcv);
+        rc = cuts_core(ctx, recvb, n_total, Fr, max_bins, lcv, lptr, lnb, lpres, s);
+        if (rc == GBM_OK) {  // to the fixed-stride exchange layout [Fo][max_bins]
+            std::vector<int32_t> lp(Fr + 1);
+            GBM_CUDA(cudaMemcpy(lp.data(), lptr, (size_t)(Fr + 1) * 4, cudaMemcpyDeviceToHost));
+            for (int c = 0; c < Fr; ++c)
+                if (lnb[c])
+                    GBM_CUDA(cudaMemcpyAsync(vals + (size_t)c * max_bins, lcv + lp[c], (size_t)lnb[c] * 4,
+                                             cudaMemcpyDeviceToDevice, s));
+            GBM_CUDA(cudaMemcpyAsync(cnt, lnb.data(), (size_t)Fr * 4, cudaMemcpyHostToDevice, s));
+            GBM_CUDA(cudaMemcpyAsync(pr, lpres.data(), (size_t)Fr * 8, cudaMemcpyHostToDevice, s));
+        }
+    }
+    // every rank joins the exchange even if its own cuts failed (its code rides along in cnt)
+    int32_t my_err = rc == GBM_OK ? 0 : rc;
+    int32_t *errb = nullptr;
+    GBM_CUDA(cudaMalloc(&errb, (size_t)(p + 1) * 4));
+    fr.v.push_back(errb);
+    GBM_CUDA(cudaMemcpyAsync(errb + p, &my_err, 4, cudaMemcpyHostToDevice, s));
+    GBM_TRY(coll_allgather(ctx, errb + p, errb, 4, s));
+    GBM_TRY(coll_allgather(ctx, vals, gvals, vbytes, s));
+    GBM_TRY(coll_allgather(ctx, cnt, gcnt, (size_t)Fo * 4, s));
+    GBM_TRY(coll_allgather(ctx, pr, gpr, (size_t)Fo * 8, s));
+    std::vector<int32_t> errs(p), hc((size_t)Fo * p);
+    std::vector<unsigned long long> hp((size_t)Fo * p);
+    GBM_CUDA(cudaMemcpyAsync(errs.data(), errb, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+    GBM_CUDA(cudaMemcpyAsync(hc.data(), gcnt, (size_t)Fo * 4 * p, cudaMemcpyDeviceToHost, s));
+    GBM_CUDA(cudaMemcpyAsync(hp.data(), gpr, (size_t)Fo * 8 * p, cudaMemcpyDeviceToHost, s));
+    GBM_CUDA(cudaStreamSynchronize(s));
+    for (int q = 0; q < p; ++q)
+        if (errs[q] != 0)
+            return rc != GBM_OK ? rc : fail(errs[q], "gbm_cuts: another rank failed (code " + std::to_string(errs[q]) + ")");
+    nb.assign(F, 0);
+    pres.assign(F, 0);
+    std::vector<int32_t> cp(F + 1, 0);
+    for (int f = 0; f < F; ++f) {
+        const int q = f % p, c = f / p;
+        nb[f] = hc[(size_t)q * Fo + c];
+        pres[f] = hp[(size_t)q * Fo + c];
+        cp[f + 1] = cp[f] + nb[f];
+    }
+    GBM_CUDA(cudaMemcpyAsync(cut_ptr_d, cp.data(), (size_t)(F + 1) * 4, cudaMemcpyHostToDevice, s));
+    GBM_CUDA(cudaMemcpyAsync(gptr, cp.data(), (size_t)(F + 1) * 4, cudaMemcpyHostToDevice, s));
+    assemble_cuts_kernel<<<std::min(F, 1024), 256, 0, s>>>(gvals, gcnt, F, p, Fo, max_bins, gptr, cut_values_d);
+    GBM_CUDA(cudaGetLastError());
+    GBM_CUDA(cudaStreamSynchronize(s));  // the host tables and scratch are released on return
+    return GBM_OK;
+}
+
+int gbm_cuts(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_t F, int32_t max_bins,
+             float *cut_values_d, int32_t *cut_ptr_d, int32_t *n_cuts_h, int32_t *max_symbol_h,
+             void *stream) {
+    GBM_TRY(ctx_enter(ctx));
+    cudaStream_t s = (cudaStream_t)stream;
+    // local checks, then one collective decision: the same error, or GBM_E_MISMATCH when the ranks
+    // disagree on the features, max_bins or the C3 mode
+    const int local = (F > 0 && max_bins >= 2 && max_bins <= 65535 && cut_values_d && cut_ptr_d && n_cuts_h &&
+                       max_symbol_h && n_rows >= 0 && (X_d || n_rows == 0))
+                          ? GBM_OK
+                          : fail(GBM_E_ARG, "gbm_cuts: bad arguments");
+    const long long sig[3] = {F, max_bins, ctx->cuts_gather};
+    GBM_TRY(coll_agree(ctx, local, sig, 3, s, "gbm_cuts"));
+    std::vector<int32_t> nb;
+    std::vector<unsigned long long> pres;
+    long long n_total = n_rows;
+    if (coll_on(ctx) && ctx->nranks > 1 && ctx->cuts_gather == 0) {
+        GBM_TRY(cuts_by_ownership(ctx, X_d, n_rows, F, max_bins, cut_values_d, cut_ptr_d, nb, pres, n_total, s));
+    } else {
+        // single rank, or GBM_OPT_CUTS_GATHER: all-gather the shards (C3), padded with NaN rows
+        long long n_max = n_rows;
+        const float *Xg = X_d;
+        float *gathered = nullptr;
+        if (coll_on(ctx)) {
+            long long *tmp;
+            GBM_CUDA(cudaMallocAsync((void **)&tmp, 2 * sizeof(long long), s));
+            long long h2[2] = {n_rows, n_rows};
+            GBM_CUDA(cudaMemcpyAsync(tmp, h2, sizeof(h2), cudaMemcpyHostToDevice, s));
+            int rc = coll_allreduce(ctx, tmp, 1, COLL_SUM_I64, s);
+            if (rc == GBM_OK) rc = coll_allreduce(ctx, tmp + 1, 1, COLL_MAX_I64, s);
+            if (rc == GBM_OK && cudaMemcpyAsync(h2, tmp, sizeof(h2), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                rc = fail(GBM_E_CUDA, "gbm_cuts: copy of the global row counts");
+            if (rc == GBM_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = fail(GBM_E_CUDA, "gbm_cuts: sync");
+            cudaFreeAsync(tmp, s);
+            if (rc != GBM_OK) return rc;
+            n_total = h2[0];
+            n_max = h2[1];
+            size_t slab = (size_t)n_max * F;
+            float *mine = nullptr;
+            if (cudaMallocAsync((void **)&gathered, std::max<size_t>(slab, 1) * ctx->nranks * sizeof(float), s) != cudaSuccess ||
+                cudaMallocAsync((void **)&mine, std::max<size_t>(slab, 1) * sizeof(float), s) != cudaSuccess) {
+                cudaGetLastError();
+                if (gathered) cudaFreeAsync(gathered, s);
+                return fail(GBM_E_NOMEM, "gbm_cuts: cannot allocate the gathered rows");
+            }
+            cudaMemsetAsync(mine, 0xff, slab * sizeof(float), s);  // 0xffffffff is a NaN
+            if (n_rows) cudaMemcpyAsync(mine, X_d, (size_t)n_rows * F * sizeof(float), cudaMemcpyDeviceToDevice, s);
+            rc = coll_allgather(ctx, mine, gathered, slab * sizeof(float), s);  // C3
+            cudaFreeAsync(mine, s);
+            if (rc != GBM_OK) {
+                cudaFreeAsync(gathered, s);
+                return rc;
+            }
+            Xg = gathered;
+            n_max = n_max * ctx->nranks;  // rows of the gathered buffer (padding rows are all-NaN)
+        }
+        if (n_total <= 0) {
+            if (gathered) cudaFreeAsync(gathered, s);
+            return fail(GBM_E_EMPTY, "gbm_cuts: zero rows");
+        }
+        const int rc = cuts_core(ctx, Xg, n_max, F, max_bins, cut_values_d, cut_ptr_d, nb, pres, s);
+        if (gathered) cudaFreeAsync(gathered, s);
+        GBM_TRY(rc);
     }
     long long tb = 0, present_total = 0;
     int max_nb = 0;

@@ -179,3 +179,32 @@ def test_virtual_local_argument_error_is_collective(G):
     out, err = run_ranks(G, p, body, timeout=120)
     assert err == [None, None]
     assert out == [-1, -1], out
+
+
+@pytest.mark.parametrize("gather", [0, 1])
+@pytest.mark.parametrize("cfg,n,missing,p", [("higgs", 20_011, 0.03, 3), ("airline", 30_000, 0.0, 5),
+                                             ("tiny", 2000, 0.05, 12), ("yearmsd", 9_000, 0.0, 2),
+                                             ("tiny", 3, 0.0, 4)])
+def test_virtual_cuts_both_c3_modes(G, cfg, n, missing, p, gather):
+    """C3 by per-feature ownership (all-to-all of the owned columns, cuts all-gathered; default) and
+    by an all-gather of X (GBM_OPT_CUTS_GATHER=1): every rank's cuts and max symbol equal the
+    oracle's global cuts (R5 over the concatenated shards)."""
+    c = W.CONFIGS[cfg]
+    X, _ = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
+    v, ptr = O.cuts(X, c.max_bins)
+    _, mx = O.symbols(X, v, ptr, c.max_bins)
+
+    def body(ctx, k):
+        ctx.set_option(ctx.CUTS_GATHER, gather)
+        lo, hi = W.shard_range(n, k, p)
+        cv, cp, m = ctx.cuts(dev(X[lo:hi]), c.max_bins)
+        return cv.cpu().numpy().copy(), cp.cpu().numpy().copy(), m
+
+    out, err = run_ranks(G, p, body)
+    for e in err:
+        if e is not None:
+            raise e
+    for k in range(p):
+        np.testing.assert_array_equal(out[k][1], ptr)
+        np.testing.assert_array_equal(out[k][0].view(np.uint32), v.view(np.uint32))
+        assert out[k][2] == mx
