@@ -2184,14 +2184,22 @@ __device__ __forceinline__ bool better(double ga, long long ia, double gb, long 
 struct NodeHist {
     const long long *direct, *parent, *build;
     long long *store;
+    // (g, h) of one bin as one 16-byte load (histogram slots are 16-byte aligned): half the L1
+    // requests of two 8-byte loads (the wide-data evaluation is L1-bound)
     __device__ __forceinline__ void get(int bin, long long &g, long long &h) const {
         if (direct) {
-            g = __ldg(direct + 2 * bin);
-            h = __ldg(direct + 2 * bin + 1);
+            const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(direct) + bin);
+            g = v.x;
+            h = v.y;
         } else {
-            g = __ldg(parent + 2 * bin) - __ldg(build + 2 * bin);
-            h = __ldg(parent + 2 * bin + 1) - __ldg(build + 2 * bin + 1);
+            const longlong2 pa = __ldg(reinterpret_cast<const longlong2 *>(parent) + bin);
+            const longlong2 bu = __ldg(reinterpret_cast<const longlong2 *>(build) + bin);
+            g = pa.x - bu.x;
+            h = pa.y - bu.y;
         }
+    }
+    __device__ __forceinline__ void put(int bin, long long g, long long h) const {
+        reinterpret_cast<longlong2 *>(store)[bin] = make_longlong2(g, h);
     }
 };
 
@@ -2307,10 +2315,7 @@ __device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long
             vg[i] = vh[i] = 0;
             if (b < nbf) {
                 src.get(b0 + b, vg[i], vh[i]);
-                if (src.store) {
-                    src.store[2 * (b0 + b)] = vg[i];
-                    src.store[2 * (b0 + b) + 1] = vh[i];
-                }
+                if (src.store) src.put(b0 + b, vg[i], vh[i]);
             }
         }
     };
@@ -2504,10 +2509,7 @@ __device__ FeatBest eval_feature_blk(const NodeHist &src, int b0, int nbf, long 
         long long vg = 0, vh = 0;
         if (b < nbf) {
             src.get(b0 + b, vg, vh);
-            if (src.store) {
-                src.store[2 * (b0 + b)] = vg;
-                src.store[2 * (b0 + b) + 1] = vh;
-            }
+            if (src.store) src.put(b0 + b, vg, vh);
         }
         long long tg, th;
         block_scan2(vg, vh, tg, th);
