@@ -544,23 +544,23 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
         const bool no_hist = a.no_hist != 0;
         for (int t = t0; t < t1; ++t) {
             const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
-            // (A) partition flags for the warp's 128 rows (4 per lane)
+            const int rem = (int)max(-1ll, min((long long)WROWS, seg_end - base));  // this warp's rows in the tile
+            // (A) partition flags for the warp's 128 rows (4 per lane); 32-bit offsets from base
             E row[4];
             uint32_t bw[4];
             int nleft = 0;
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
-                const long long pos = base + s2 * 32 + lane;
-                if (pos < seg_end) row[s2] = rin ? rin[pos] : make_entry<CARRY>((uint32_t)pos, a.qpair);
+                const int q = s2 * 32 + lane;
+                if (q < rem) row[s2] = rin ? rin[base + q] : make_entry<CARRY>((uint32_t)(base + q), a.qpair);
                 else row[s2] = E{};
             }
             bool left[4];
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2)
-                left[s2] = base + s2 * 32 + lane < seg_end && goes_left(qm, nd, row_of(row[s2]));
+            for (int s2 = 0; s2 < 4; ++s2) left[s2] = s2 * 32 + lane < rem && goes_left(qm, nd, row_of(row[s2]));
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
-                const bool valid = base + s2 * 32 + lane < seg_end;
+                const bool valid = s2 * 32 + lane < rem;
                 const uint32_t lw = __ballot_sync(0xffffffffu, valid && left[s2]);
                 bw[s2] = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
                 if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 4 + s2] = lw;
@@ -2129,17 +2129,22 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
         const int k = step ? step->k : first + j;
         const NodeDev nd = nodes[k];
         if (nd.state != GBM_NODE_SPLIT) continue;  // uniform per block
-        const long long n_left = nodes[step ? step->c : 2 * k + 1].count;
+        // segment-local 32-bit positions (a rank's segment holds < 2^31 rows); one pointer per tile
+        const int n_left = (int)nodes[step ? step->c : 2 * k + 1].count;
         const int lt = t - tile_base[j];
-        if (rows_ctr && threadIdx.x == 0)
-            atomicAdd(rows_ctr, (unsigned long long)min((long long)PT, nd.count - (long long)lt * PT));
+        const int tile_rows = (int)min((long long)PT, nd.count - (long long)lt * PT);
+        if (rows_ctr && threadIdx.x == 0) atomicAdd(rows_ctr, (unsigned long long)tile_rows);
         // every load of the tile is issued before the block scan (one exposed DRAM latency)
-        const long long off = tile_off[t];
+        const int off = tile_off[t];
+        const long long tile0 = nd.start + (long long)lt * PT;  // first position of this tile
+        const E *src = ridx_in ? ridx_in + tile0 : nullptr;
+        E *dst = ridx_out + nd.start;
+        const int wbase = wid * (WPW * 32);
         E rows[WPW];
 #pragma unroll
         for (int s = 0; s < WPW; ++s) {
-            const long long pin = (long long)lt * PT + wid * (WPW * 32) + s * 32 + lane;
-            if (pin < nd.count) rows[s] = ridx_in ? ridx_in[nd.start + pin] : make_entry<CARRY>((uint32_t)(nd.start + pin), qpair);
+            const int q = wbase + s * 32 + lane;  // position within the tile
+            if (q < tile_rows) rows[s] = src ? src[q] : make_entry<CARRY>((uint32_t)(tile0 + q), qpair);
             else rows[s] = E{};
         }
         // one flag word per lane (lanes >= WPW idle), warp-scan of the popcounts
@@ -2160,14 +2165,14 @@ __global__ void __launch_bounds__(P_THREADS) part_scatter_kernel(
         }
         __syncthreads();
         const uint32_t ltm = (1u << lane) - 1u;
+        const int pin0 = lt * PT + wbase + lane;  // segment position of row s = 0 of this lane
 #pragma unroll
         for (int s = 0; s < WPW; ++s) {
             const uint32_t w = __shfl_sync(0xffffffffu, myw, s);
-            const long long pin = (long long)lt * PT + wid * (WPW * 32) + s * 32 + lane;  // position within the node
-            if (pin >= nd.count) continue;
-            const long long lb = off + wpre[wid * WPW + s] + __popc(w & ltm);  // lefts before
+            if (wbase + s * 32 + lane >= tile_rows) continue;
+            const int lb = off + wpre[wid * WPW + s] + __popc(w & ltm);  // lefts before
             const bool left = (w >> lane) & 1u;
-            ridx_out[left ? nd.start + lb : nd.start + n_left + (pin - lb)] = rows[s];
+            dst[left ? lb : n_left + (pin0 + s * 32 - lb)] = rows[s];
         }
         __syncthreads();
     }
