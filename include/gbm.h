@@ -153,11 +153,16 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  * GBM_OPT_CUTS_GATHER: gbm_cuts with several ranks (C3).  0 (default) = per-feature ownership:
  *   feature f belongs to rank f mod p, the ranks exchange their shards' columns (all-to-all), each
  *   owner cuts its features over the global rows and the cuts are all-gathered -- O(n F / p) per
- *   rank; 1 = all-gather every shard's X to every rank (O(n F) per rank).  Same cuts either way. */
+ *   rank; 1 = all-gather every shard's X to every rank (O(n F) per rank).  Same cuts either way.
+ * GBM_OPT_ROOT_TENSOR: the root histogram of byte-symbol matrices with the feature-major copy
+ *   (gbm_transpose_symbols) and n a multiple of 16: 2 = every warp fetches a [features x 32 rows]
+ *   tile of that copy with one TMA tensor copy and lane f holds its feature's 32 symbols in
+ *   registers (root_ct.cu); 1 = the staged packed rows; 0 (default) = 2 when there are several
+ *   feature groups (> 32 features) or <= 16 features, else 1 (measured).  Same histogram. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
        GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
        GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12, GBM_OPT_LEVEL_HIST = 13,
-       GBM_OPT_EVAL_SLICED = 14, GBM_OPT_CUTS_GATHER = 15 };
+       GBM_OPT_EVAL_SLICED = 14, GBM_OPT_CUTS_GATHER = 15, GBM_OPT_ROOT_TENSOR = 16 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

@@ -334,6 +334,7 @@ class Context:
     LEVEL_HIST = 13
     EVAL_SLICED = 14
     CUTS_GATHER = 15
+    ROOT_TENSOR = 16
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

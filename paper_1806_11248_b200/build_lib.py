@@ -9,7 +9,7 @@ import sysconfig
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgbm.so")
-SOURCES = ["api.cu", "comm.cu", "quantise.cu", "gradients.cu", "tree.cu", "records.cu"]
+SOURCES = ["api.cu", "comm.cu", "quantise.cu", "gradients.cu", "tree.cu", "records.cu", "root_ct.cu"]
 HEADERS = ["gbm_internal.cuh", "tree_common.cuh", os.path.join("..", "..", "include", "gbm.h")]
 
 

@@ -300,6 +300,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->walk_mode = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_ROOT_TENSOR) {
+        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_ROOT_TENSOR: 0 auto, 1 off, 2 always (where it applies)");
+        ctx->root_ct = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_CUTS_GATHER) {
         if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_CUTS_GATHER: 0 per-feature ownership, 1 all-gather");
         ctx->cuts_gather = (int)value;

@@ -121,7 +121,8 @@ struct gbm_ctx {
     int level_path = 0;
     int level_hist = 0;
     int eval_sliced = 0;
-    int cuts_gather = 0;           // GBM_OPT_CUTS_GATHER (1: C3 as an all-gather of X, not per-feature ownership)           // GBM_OPT_EVAL_SLICED (1: reduce-scatter + feature-sliced evaluation)            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed bank-column)            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
+    int cuts_gather = 0;
+    int root_ct = 0;               // GBM_OPT_ROOT_TENSOR (0 auto = tensor-fed root where it applies, 1 off)           // GBM_OPT_CUTS_GATHER (1: C3 as an all-gather of X, not per-feature ownership)           // GBM_OPT_EVAL_SLICED (1: reduce-scatter + feature-sliced evaluation)            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed bank-column)            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     std::vector<int> tree_slice_key;   // feature-slice tables currently uploaded (sliced evaluation)

@@ -3619,6 +3619,22 @@ static int launch_root_staged(gbm_ctx *ctx, const HistPlan &hr, const QM &qm, co
     return GBM_OK;
 }
 
+// the tensor-fed root (root_ct.cu) where it applies: 1 launched, 0 not applicable, < 0 error
+static int try_root_tensor(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm, const int32_t *qpair_d, int grad_bits,
+                           long long *hist, long long *totals, long long n, cudaStream_t s) {
+    RootCtLaunch L = {};
+    L.colsym = qm.col;
+    L.qpair = reinterpret_cast<const int2 *>(qpair_d);
+    L.n = n;
+    L.F = q->n_features;
+    L.bits = q->bits;
+    L.wide = grad_bits > 15;
+    L.cut_ptr = q->cut_ptr_d;
+    L.hist = reinterpret_cast<unsigned long long *>(hist);
+    L.totals = reinterpret_cast<unsigned long long *>(totals);
+    return root_ct_launch(ctx, L, s);  // profiled as PC_HIST_ROOT when it launches
+}
+
 // Loss-guided growth (R25-R27): InitRoot as depth-wise, then max_leaves - 1 device-driven
 // expansion steps, each = select (pop) -> fused repartition + smaller-child histogram of the one
 // parent -> scan -> scatter -> allreduce -> sibling by subtraction + EvaluateSplit of both
@@ -3687,7 +3703,13 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     }
     // ---- InitRoot
     GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
-    if (n > 0 && TB > 0 && root_staged) {
+    const int root_ct = (n > 0 && TB > 0) ? try_root_tensor(ctx, q, qm, qpair_d, prm->grad_bits, hist_root,
+                                                            hist_root + hist_unit, n, s)
+                                          : 0;
+    if (root_ct < 0) return root_ct;
+    if (root_ct == 1) {
+        // the tensor-fed root (root_ct.cu)
+    } else if (n > 0 && TB > 0 && root_staged) {
         GBM_TRY(launch_root_staged(ctx, hr, qm, q, qpair_d, cg_root, hist_root, hist_root + hist_unit, n, row_bytes, s));
     } else if (n > 0 && TB > 0) {
         RangeArgs ra = {};
@@ -3864,6 +3886,13 @@ int gbm_build_histogram(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qpair
     GBM_CUDA(cudaMemsetAsync(hist_d, 0, (size_t)std::max(TB, 1) * 2 * 8, s));
     if (n_sel == 0 || TB == 0) return GBM_OK;
     HistPlan hr;
+    if (!rows_d) {  // the tensor-fed root first (as gbm_build_tree's InitRoot)
+        GBM_TRY(ctx->arena.reserve(512));
+        long long *tot0 = ctx->arena.take<long long>(2);
+        GBM_CUDA(cudaMemsetAsync(tot0, 0, 16, s));
+        const int ct = try_root_tensor(ctx, q, qm, qpair_d, grad_bits, reinterpret_cast<long long *>(hist_d), tot0, n_sel, s);
+        if (ct != 0) return ct < 0 ? ct : GBM_OK;
+    }
     if (!rows_d && plan_root_staged(ctx, q, qm, hp, grad_bits, n_sel, hr)) {
         // the staged bank-column root of gbm_build_tree (hist_cs_range / hist_csg_range), so it can
         // be compared bin for bin with the oracle
@@ -4280,7 +4309,13 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
 
     // ---- InitRoot: root histogram + totals, allreduce, evaluate
     GBM_CUDA(cudaMemsetAsync(hist_root, 0, (hist_unit + 2) * 8, s));
-    if (n > 0 && TB > 0 && root_staged) {
+    const int root_ct = (n > 0 && TB > 0) ? try_root_tensor(ctx, q, qm, qpair_d, prm->grad_bits, hist_root,
+                                                            hist_root + hist_unit, n, s)
+                                          : 0;
+    if (root_ct < 0) return root_ct;
+    if (root_ct == 1) {
+        // the tensor-fed root (root_ct.cu)
+    } else if (n > 0 && TB > 0 && root_staged) {
         GBM_TRY(launch_root_staged(ctx, hr, qm, q, qpair_d, cg_root, hist_root, hist_root + hist_unit, n, row_bytes, s));
     } else if (n > 0 && TB > 0 && hp.col) {
         ColRangeArgs ca = {};

@@ -155,4 +155,16 @@ int rec_level_launch(gbm_ctx *ctx, const RecLaunch &L, cudaStream_t s);
 int rec_seg_launch(gbm_ctx *ctx, NodeDev *nodes, int first, int n_par, unsigned long long *cursor, cudaStream_t s);
 int rec_root_launch(gbm_ctx *ctx, unsigned long long *cursor, long long n, cudaStream_t s);
 
+// ---- root_ct.cu: the root histogram fed by TMA tensor tiles of the feature-major symbols
+struct RootCtLaunch {
+    const uint8_t *colsym;            // [F][n] (null: not available)
+    const int2 *qpair;
+    long long n;
+    int F, bits;
+    bool wide;
+    const int32_t *cut_ptr;
+    unsigned long long *hist, *totals, *rows_ctr;
+};
+int root_ct_launch(gbm_ctx *ctx, const RootCtLaunch &L, cudaStream_t s);  // 1 launched, 0 n/a, < 0 error
+
 }  // namespace gbm

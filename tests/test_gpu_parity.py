@@ -857,3 +857,35 @@ def test_predict_many_trees_parity(ctx, G, cfg, n, rounds, grow, missing):
     Xt, _ = W.generate(cfg, n, n + 2_345, n_rows=max(n + 2_345, c.n_rows), missing=0.1)
     np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy().view(np.uint64),
                                   ob.predict(Xt).view(np.uint64))
+
+
+@pytest.mark.parametrize("P", [15, 30])
+@pytest.mark.parametrize("cfg,n,B", [("higgs", 40_016, None), ("airline", 30_000, None), ("yearmsd", 20_000, None),
+                                     ("epsilon", 2_048, None), ("tiny", 2_000, 256), ("higgs", 9_008, 200)])
+def test_root_tensor_parity(ctx, G, cfg, n, B, P):
+    """The tensor-fed root (root_ct.cu: TMA tiles of the feature-major symbols, GBM_OPT_ROOT_TENSOR
+    forced on): the root histogram bin for bin and whole rounds bit for bit vs the oracle, with a
+    16-row tail batch (n = 16 mod 32), several feature groups, 1 / 2 / 4 rows per step (28, 13, 8
+    features), wide accumulators (P = 30) and the 8-bit sentinel (B = 200)."""
+    ctx.set_option(ctx.ROOT_TENSOR, 2)
+    c = W.CONFIGS[cfg]
+    B = B or c.max_bins
+    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=0.02 if B == 200 else 0.0)
+    qm, v, p, s, bits, words = _qm_from_oracle(G, X, B, 32)
+    assert bits == 8
+    ctx.transpose_symbols(qm)
+    _, _, q, _ = O.gradients(c.objective, np.zeros(n), y, P)
+    ref = O.node_histogram(words, X.shape[1], bits, 32, p, B, q, np.arange(n))
+    ctx.profile(True, only=("hist_root", "hist_level"))
+    got = ctx.build_histogram(qm, dev(q), P)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    assert prof["hist_root"]["launches"] == 1
+    ob = O.Booster(X, y, max_bins=B, objective=c.objective, max_depth=4, grad_bits=P, eta=0.3)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=B, objective=c.objective, max_depth=4, grad_bits=P,
+                   base_margin=ob.base_margin, eta=0.3)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.ROOT_TENSOR, 0)
