@@ -102,6 +102,20 @@ def ncu_traffic(config):
         return None, None, None
 
 
+def clocks_max_mhz():
+    """Max SM clock (MEASURED_PEAKS.json sm_max_mhz, else nvidia-smi, else 1965)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        pass
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits", "-i", "0"],
+                             capture_output=True, text=True, timeout=10).stdout
+        return float(out.split()[0])
+    except Exception:
+        return 1965.0
+
+
 class Clocks:
     """nvidia-smi sampler running across the timed region (B200_PROFILING.md clocks line)."""
 
@@ -213,6 +227,7 @@ def run_ours(a, world, rank, local):
     booster = G.Booster(ctx, Xd, yd, cuts=cuts, **kw)
     e2.record(stream)
     torch.cuda.synchronize()
+    booster_bits = booster.qm.bits
     one_time = {"cuts_ms": max_over_ranks(e0.elapsed_time(e1)),
                 "quantise_compress_ms": max_over_ranks(e1.elapsed_time(e2)),
                 "bits": booster.qm.bits, "n_bins_total": booster.qm.n_bins_total,
@@ -318,6 +333,25 @@ def run_ours(a, world, rank, local):
                 "binding_unit": {"unit": "L1/TEX data pipe (shared-memory ATOMS)",
                                  "pct_of_peak": round(l1_pct, 1) if l1_pct else None,
                                  "source": traffic_src}}
+    # ---- the unit that binds the histogram kernels: shared-memory atomics.  (g, h) updates per
+    # round = rows streamed or built x features (missing symbols included: an upper bound for the
+    # sparse sets), against the measured conflict-free rate of 8.65 updates/clk/SM
+    # (profiles/microbench_smem_atomics.txt, lane-private copies) x SMs x the max SM clock
+    cfg_b = W.CONFIGS[a.config]
+    bits_b = booster_bits
+    root_rows = prof["hist_root"]["bytes"] / ms_div / (cfg_b.n_features * bits_b / 8.0 + 8.0)
+    level_rows = prof["hist_level"]["bytes"] / ms_div / (cfg_b.n_features * bits_b / 8.0 + 12.0)
+    updates = (root_rows + level_rows) * cfg_b.n_features
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk = clocks_max_mhz() * 1e6
+    atom_peak = 8.65 * sm_count * clk
+    atom_ach = updates / (hist_ms * 1e-3) if hist_ms > 0 else 0.0
+    roofline_atomics = {"bound": "smem_atomics", "kernel": "hist_kernel (root + level launches)",
+                        "achieved": atom_ach / 1e9, "peak": atom_peak / 1e9, "unit": "G (g,h) updates/s",
+                        "frac": round(atom_ach / atom_peak, 4) if atom_peak else None,
+                        "updates_per_round": updates,
+                        "peak_source": "8.65 conflict-free (g,h) updates/clk/SM measured "
+                                       "(profiles/microbench_smem_atomics.txt) x SMs x max SM clock"}
     # ---- per-stage breakdown: a separate eager window with every launch timed
     ctx.profile(True)
     n_st = min(20, a.steps)
@@ -407,7 +441,7 @@ def run_ours(a, world, rank, local):
     cpu = parity = None
     if rank == 0 and world == 1 and not (a.no_cpu_baseline and a.no_parity):
         cpu, parity = cpu_baseline_and_parity(G, ctx, torch, dev, X, y, kw, a)
-    return dict(p30=p30, parity=parity, full=full, ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages, l2=l2_note,
+    return dict(p30=p30, parity=parity, full=full, roofline_atomics=roofline_atomics, ms_step=ms_step, n=n, world=world, roofline=roofline, stages=stages, l2=l2_note,
                 one_time=one_time, clocks=clk, launches=launches, e2e=e2e, cpu=cpu,
                 predict_ms=predict_ms, allreduce_ms=allreduce_ms, grad_bits=a.grad_bits)
 
@@ -650,6 +684,7 @@ def main():
                        "parallelism": f"dp{world} (rows sharded, NCCL histogram allreduce)",
                        "l2": r["l2"]},
             "roofline": r["roofline"],
+            "roofline_atomics": r["roofline_atomics"],
             "cpu_baseline": r["cpu"],
             "parity": r["parity"],
             "grad_bits_30": r["p30"],

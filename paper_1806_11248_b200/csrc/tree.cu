@@ -4541,9 +4541,9 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
             L.TB = std::max<long long>(TB, 1);
             int slot;
             L.rows_ctr = prof_rows_slot(ctx, &slot);
-            // algorithmic bits: per parent row the split symbol + a row-index read
-            // and write (b + 64), per row of the built child the packed row + qpair + row index
-            L.bits_parent_row = q->bits + 64;
+            // algorithmic bits of the histogram: per row of the built child its packed
+            // row + qpair + row index; the partition bytes are §8(d)'s partition term, not counted
+            L.bits_parent_row = 0;
             L.bits_built_row = F * q->bits + 96;
             {
                 ProfScope ps(ctx, PC_HIST_LEVEL, s, 0.0, slot, 1.0 / 8.0);
