@@ -18,7 +18,6 @@
 
 namespace gbm {
 
-constexpr int CT_NW = H_THREADS / 32;
 
 struct __align__(128) CtBuf {  // one staging buffer of a warp (tensor-copy destination)
     uint8_t sym[32][32];       // [feature of the group][row of the batch]
@@ -62,20 +61,20 @@ __device__ __forceinline__ void col_red2(unsigned addr, int qx, int qy) {
 }
 
 // R rows per accumulate step: lane = copy * Fg + feature, copy c takes rows c, c + R, ...
-template <bool WIDE, int R>
-__global__ void __launch_bounds__(H_THREADS, WIDE ? 1 : 2) hist_ct_root_kernel(const __grid_constant__ CUtensorMap map,
-                                                                              CtArgs a) {
+template <bool WIDE, int R, int NW, int NS>
+__global__ void __launch_bounds__(NW * 32, WIDE ? 1 : 2) hist_ct_root_kernel(const __grid_constant__ CUtensorMap map,
+                                                                            CtArgs a) {
     extern __shared__ __align__(128) int smem[];
     constexpr int CH = WIDE ? 4 : 2;
-    CtBuf *stage = reinterpret_cast<CtBuf *>(smem + CH * COLB_STRIDE);  // [CT_NW][2]
-    __shared__ uint64_t s_bar[2 * CT_NW];
-    __shared__ long long s_red[2 * CT_NW];
+    CtBuf *stage = reinterpret_cast<CtBuf *>(smem + CH * COLB_STRIDE);  // [NW][NS]
+    __shared__ uint64_t s_bar[NS * NW];
+    __shared__ long long s_red[2 * NW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint64_t *bar = s_bar + 2 * wid;
-    CtBuf *buf = stage + 2 * wid;
+    uint64_t *bar = s_bar + NS * wid;
+    CtBuf *buf = stage + NS * wid;
     if (lane == 0) {
-        mbar_init(bar, 1);
-        mbar_init(bar + 1, 1);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) mbar_init(bar + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -94,16 +93,16 @@ __global__ void __launch_bounds__(H_THREADS, WIDE ? 1 : 2) hist_ct_root_kernel(c
         const int c = lane / Fg, f = lane - c * Fg;
         const bool on = c < R;
         const bool tot = a.totals && g == 0;
-        for (int i = threadIdx.x; i < CH * COLB_STRIDE; i += H_THREADS) smem[i] = 0;
+        for (int i = threadIdx.x; i < CH * COLB_STRIDE; i += NW * 32) smem[i] = 0;
         if (a.rows_ctr && g == 0 && threadIdx.x == 0) atomicAdd(a.rows_ctr, (unsigned long long)(end - start));
         __syncthreads();
-        // this warp's 32-row batches b0 = start + 32 (wid + CT_NW m) < end; the last one of the
+        // this warp's 32-row batches b0 = start + 32 (wid + NW m) < end; the last one of the
         // matrix may hold 16 rows (n is a multiple of 16): the tensor copy zero-fills the rows past
         // n, the pair copy takes 16 rows and the rest of the pairs are zeroed (adds of 0)
         const long long b_first = start + 32ll * wid;
-        const int nb = b_first < end ? (int)((end - b_first - 1) / (32ll * CT_NW)) + 1 : 0;
+        const int nb = b_first < end ? (int)((end - b_first - 1) / (32ll * NW)) + 1 : 0;
         auto issue = [&](int m, unsigned cb) {
-            const long long b0 = b_first + 32ll * CT_NW * m;
+            const long long b0 = b_first + 32ll * NW * m;
             const int rows = (int)min(32ll, end - b0);
             if (rows < 32) {
                 if (lane >= rows) buf[cb].q[lane] = make_int2(0, 0);
@@ -116,10 +115,14 @@ __global__ void __launch_bounds__(H_THREADS, WIDE ? 1 : 2) hist_ct_root_kernel(c
                 bulk_g2s(buf[cb].q, a.qpair + b0, 8u * rows, bar + cb);
             }
         };
-        if (nb > 0) issue(0, seq & 1);
+        // NS-deep pipeline: batch m lands in buffer (seq0 + m) % NS, NS - 1 batches in flight
+        const unsigned seq0 = seq;
+#pragma unroll
+        for (int m = 0; m < NS - 1; ++m)
+            if (m < nb) issue(m, (seq0 + m) % NS);
         for (int m = 0; m < nb; ++m) {
-            const unsigned cb = seq & 1;
-            if (m + 1 < nb) issue(m + 1, cb ^ 1);
+            const unsigned cb = seq % NS;
+            if (m + NS - 1 < nb) issue(m + NS - 1, (seq + NS - 1) % NS);
             mbar_wait(bar + cb, (phbits >> cb) & 1u);
             phbits ^= 1u << cb;
             const CtBuf &st = buf[cb];
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(H_THREADS, WIDE ? 1 : 2) hist_ct_root_kernel(c
         __syncthreads();
         if (tot && threadIdx.x == 0) {
             long long x = 0, y = 0;
-            for (int i = 0; i < CT_NW; ++i) {
+            for (int i = 0; i < NW; ++i) {
                 x += s_red[2 * i];
                 y += s_red[2 * i + 1];
             }
@@ -198,17 +201,28 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <bool W, int R>
+template <bool W, int R, int NW, int NS>
 static int ct_launch_t(gbm_ctx *ctx, const CUtensorMap &map, const CtArgs &a, long long n_items, cudaStream_t s) {
-    const size_t sm = (size_t)(W ? 4 : 2) * COLB_STRIDE * 4 + 2 * CT_NW * sizeof(CtBuf);
-    GBM_CUDA(cudaFuncSetAttribute(hist_ct_root_kernel<W, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const size_t sm = (size_t)(W ? 4 : 2) * COLB_STRIDE * 4 + (size_t)NS * NW * sizeof(CtBuf);
+    auto kern = hist_ct_root_kernel<W, R, NW, NS>;
+    GBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int occ = 0;
-    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hist_ct_root_kernel<W, R>, H_THREADS, sm));
+    GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, sm));
     if (occ < 1) return fail(GBM_E_ARG, "tensor-fed root kernel cannot be resident");
     const int grid = (int)std::max<long long>(1, std::min<long long>(n_items, (long long)occ * ctx->sm_count));
-    hist_ct_root_kernel<W, R><<<grid, H_THREADS, sm, s>>>(map, a);
+    kern<<<grid, NW * 32, sm, s>>>(map, a);
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
+}
+
+template <bool W, int R>
+static int ct_launch_cfg(gbm_ctx *ctx, const CUtensorMap &map, const CtArgs &a, long long n_items, int cfg,
+                         cudaStream_t s) {
+    switch (cfg) {  // (warps per block, pipeline depth)
+        case 3: return ct_launch_t<W, R, 12, 3>(ctx, map, a, n_items, s);
+        case 4: return ct_launch_t<W, R, 8, 4>(ctx, map, a, n_items, s);
+        default: return ct_launch_t<W, R, 16, 2>(ctx, map, a, n_items, s);
+    }
 }
 
 // 1: launched; 0: does not apply (the caller uses the staged / compact root); < 0: error
@@ -247,16 +261,19 @@ int root_ct_launch(gbm_ctx *ctx, const RootCtLaunch &L, cudaStream_t s) {
     a.totals = L.totals;
     // about two items per resident block (flush amortisation vs balance), whole 32-row batches
     const long long blocks = (long long)(L.wide ? 1 : 2) * ctx->sm_count;
-    a.chunk = std::max<long long>(32 * CT_NW, ((L.n * ng + 2 * blocks - 1) / (2 * blocks) + 31) / 32 * 32);
+    a.chunk = std::max<long long>(32 * 16, ((L.n * ng + 2 * blocks - 1) / (2 * blocks) + 31) / 32 * 32);
     const long long n_items = (L.n + a.chunk - 1) / a.chunk * ng;
     int slot = -1;
     a.rows_ctr = prof_rows_slot(ctx, &slot);  // algorithmic bytes: n (F b / 8 + 8), SURVEY §8(d)
     ProfScope ps(ctx, PC_HIST_ROOT, s, 0.0, slot, (double)L.F + 8.0);
     int rc;
-    if (L.wide) rc = R == 1 ? ct_launch_t<true, 1>(ctx, map, a, n_items, s)
-                            : R == 2 ? ct_launch_t<true, 2>(ctx, map, a, n_items, s) : ct_launch_t<true, 4>(ctx, map, a, n_items, s);
-    else rc = R == 1 ? ct_launch_t<false, 1>(ctx, map, a, n_items, s)
-                     : R == 2 ? ct_launch_t<false, 2>(ctx, map, a, n_items, s) : ct_launch_t<false, 4>(ctx, map, a, n_items, s);
+    const int cfg = ctx->root_ct;  // 2 (default shape), 3, 4: the measured pipeline shapes
+    if (L.wide) rc = R == 1 ? ct_launch_cfg<true, 1>(ctx, map, a, n_items, cfg, s)
+                            : R == 2 ? ct_launch_cfg<true, 2>(ctx, map, a, n_items, cfg, s)
+                                     : ct_launch_cfg<true, 4>(ctx, map, a, n_items, cfg, s);
+    else rc = R == 1 ? ct_launch_cfg<false, 1>(ctx, map, a, n_items, cfg, s)
+                     : R == 2 ? ct_launch_cfg<false, 2>(ctx, map, a, n_items, cfg, s)
+                              : ct_launch_cfg<false, 4>(ctx, map, a, n_items, cfg, s);
     return rc == GBM_OK ? 1 : rc;
 }
 
