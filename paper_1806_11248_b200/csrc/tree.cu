@@ -1838,13 +1838,26 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
     const long long n_chunks = (n + 31) / 32;
     const long long cstep = (long long)gridDim.x * (WALK_THREADS / 32);
     uint32_t v[W];
+    double m_next = 0.0;  // (EPI) the lane's row of the next chunk: margin and label in flight
+    float y_next = 0.0f;
     auto load = [&](long long c) {  // chunk c's words into registers (coalesced)
         const uint32_t *src = qm.P + c * 32 * W;
-        const long long rows_c = c < n_chunks ? min(32ll, n - c * 32) : 0;
+        if (c + 1 < n_chunks) {  // a full chunk: no per-word bounds
 #pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const int j = lane + 32 * k;
-            v[k] = j / W < rows_c ? __ldg(src + j) : 0u;
+            for (int k = 0; k < W; ++k) v[k] = __ldg(src + lane + 32 * k);
+        } else {
+            const int rows_c = c < n_chunks ? (int)(n - c * 32) : 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int j = lane + 32 * k;
+                v[k] = j / W < rows_c ? __ldg(src + j) : 0u;
+            }
+        }
+        if (EPI) {
+            const long long r = c * 32 + lane;
+            const bool ok = r < n;
+            m_next = ok ? ep.margin[r] : 0.0;
+            y_next = ok ? __ldg(ep.label + r) : 0.0f;
         }
     };
     long long c = blockIdx.x * (long long)(WALK_THREADS / 32) + wid;
@@ -1857,6 +1870,8 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
             sr[(j / W) * PW + j % W] = v[k];
         }
         __syncwarp();
+        const double m_cur = m_next;
+        const float y_cur = y_next;
         load(c + cstep);  // the next chunk's loads fly during this chunk's walk
         if (lane < rows_here) {  // walk on the staged row: one shared-memory read per level
             const uint32_t *row = sr + lane * PW;
@@ -1886,9 +1901,9 @@ __global__ void __launch_bounds__(WALK_THREADS) leaf_walk_stg_kernel(QM qm, cons
             const long long r = c * 32 + lane;
             row_leaf[r] = k;
             if (EPI) {
-                const double m = dadd(ep.margin[r], __ldg(ep.weight + k));
+                const double m = dadd(m_cur, __ldg(ep.weight + k));
                 ep.margin[r] = m;
-                const float yl = __ldg(ep.label + r);
+                const float yl = y_cur;
                 double v = m;
                 if (ep.objective == GBM_LOGISTIC) {
                     v = sigmoid(m);
