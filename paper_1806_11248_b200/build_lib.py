@@ -45,6 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     flags = [nvcc(), "-std=c++17", "-O3", "-lineinfo", "--fmad=false",
              "-gencode", "arch=compute_100a,code=sm_100a",
              "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-I", inc]
+    flags += os.environ.get("GBM_NVCC_EXTRA", "").split()  # tuning experiments only (-DGBM_PH_UNR=...)
     hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
     procs, objs = [], []
     for src in SOURCES:

@@ -380,20 +380,42 @@ __device__ __forceinline__ bool goes_left(const QM &qm, const NodeDev &nd, uint3
 // run_base[j] (first RUN-tile run); n_items = runs x feature groups.  Work item i of the fused
 // kernel is run i / G, group i % G, resolved on the fly (find_parent over run_base).
 // Works for any block size that is a multiple of 32 (<= 1024).
+// run_tiles < 0: sized per level for -run_tiles resident blocks -- about one item per block, or
+// the fewest whole waves when MAX_CHUNK caps the item (each item zeroes and flushes a whole shared
+// histogram; measured: Higgs levels 0.975 -> 0.870 ms/round, YearMSD 0.300 -> 0.247, Airline
+// 11.94 -> 11.56 against ~4 items per block).  The tiles per item go to n_items[2].
 __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_par, int n_groups, int run_tiles,
                            int *__restrict__ tile_base, int *__restrict__ run_base, int *__restrict__ n_items,
-                           bool split_only = false) {
+                           bool split_only = false, long long rows_ub = 0) {
     __shared__ long long sm32[32];
     __shared__ long long carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    auto eligible = [&](const NodeDev &nd) {
+        return nd.count > 0 && (split_only ? nd.state == GBM_NODE_SPLIT : nd.state != GBM_NODE_ABSENT);
+    };
+    if (run_tiles < 0) {  // the level's tiles: at most ceil(rows / PT) + n_par (no extra pass)
+        const long long T = (rows_ub + PT - 1) / PT + n_par, np = n_par, B = -(long long)run_tiles;
+        // the fewest whole waves of items (w x B, at most) whose items fit MAX_CHUNK rows
+        long long rt = MAX_CHUNK / PT;
+        for (long long w = 1; w <= 64; ++w) {
+            const long long slots = w * B - np * n_groups;  // ceil per parent: <= np extra runs
+            if (slots <= 0) continue;
+            const long long r = (T * n_groups + slots - 1) / slots;
+            if (r <= MAX_CHUNK / PT) {
+                rt = max(1ll, r);
+                break;
+            }
+        }
+        run_tiles = (int)rt;
+    }
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int c = 0; c < n_par; c += blockDim.x) {
         const int j = c + threadIdx.x;
         long long nt = 0, nr = 0;
         if (j < n_par) {
             const NodeDev nd = nodes[first + j];
-            if (nd.count > 0 && (split_only ? nd.state == GBM_NODE_SPLIT : nd.state != GBM_NODE_ABSENT)) {
+            if (eligible(nd)) {
                 nt = (nd.count + PT - 1) / PT;
                 nr = (nt + run_tiles - 1) / run_tiles;
             }
@@ -429,6 +451,7 @@ __device__ void plan_block(const NodeDev *__restrict__ nodes, int first, int n_p
         run_base[n_par] = (int)(carry & 0xffffffff);
         n_items[0] = (int)(carry & 0xffffffff) * n_groups;
         n_items[1] = 0;  // dynamic work counter of the fused kernel
+        n_items[2] = run_tiles;
     }
 }
 
@@ -474,9 +497,9 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
     using E = typename EntryOf<CARRY>::T;
     extern __shared__ int smem[];
     __shared__ int s_off[2049];
-    __shared__ E s_rows[H_THREADS / 32][WROWS];
+    __shared__ E s_rows[H_THREADS / 32][WROWS * (BYTE && !CARRY ? GBM_PH_TPS : 1)];
     const E *rin = static_cast<const E *>(a.ridx_in);
-    int first = a.first, run_tiles = a.run_tiles;
+    int first = a.first, run_tiles = a.n_items[2];
     if (a.step) {  // loss-guided step (n_par = 1): no items at all when nothing is expanded
         first = a.step->k;
         run_tiles = a.step->run_tiles;
@@ -542,45 +565,62 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
         const uint32_t mask = (1u << qm.bits) - 1u;
         unsigned long long bits_acc = 0;
         const bool no_hist = a.no_hist != 0;
-        for (int t = t0; t < t1; ++t) {
-            const long long base = nd.start + (long long)(t - tb) * PT + wid * WROWS;
-            const int rem = (int)max(-1ll, min((long long)WROWS, seg_end - base));  // this warp's rows in the tile
-            // (A) partition flags for the warp's 128 rows (4 per lane); 32-bit offsets from base
-            E row[4];
-            uint32_t bw[4];
-            int nleft = 0;
+        // TPS tiles per step (byte path: 2): the warp decides its 128 rows of each of the step's
+        // tiles (8 entry loads, then 8 split-symbol gathers in flight per lane) and accumulates the
+        // built rows of all of them as ONE list, so phase (B) runs on fuller batches.
+        constexpr int TPS = BYTE && !CARRY ? GBM_PH_TPS : 1;  // (static shared memory budget: plan_hist)
+        for (int t = t0; t < t1; t += TPS) {
+            E row[TPS][4];
+            uint32_t raw[TPS][4];
+            int rem[TPS];
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                const int q = s2 * 32 + lane;
-                if (q < rem) row[s2] = rin ? rin[base + q] : make_entry<CARRY>((uint32_t)(base + q), a.qpair);
-                else row[s2] = E{};
+            for (int tt = 0; tt < TPS; ++tt) {
+                const long long base = nd.start + (long long)(t + tt - tb) * PT + wid * WROWS;
+                rem[tt] = t + tt < t1 ? (int)max(-1ll, min((long long)WROWS, seg_end - base)) : -1;
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) {
+                    const int q = s2 * 32 + lane;
+                    if (q < rem[tt]) row[tt][s2] = rin ? rin[base + q] : make_entry<CARRY>((uint32_t)(base + q), a.qpair);
+                    else row[tt][s2] = E{};
+                }
             }
-            bool left[4];
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) left[s2] = s2 * 32 + lane < rem && goes_left(qm, nd, row_of(row[s2]));
+            for (int tt = 0; tt < TPS; ++tt)
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                const bool valid = s2 * 32 + lane < rem;
-                const uint32_t lw = __ballot_sync(0xffffffffu, valid && left[s2]);
-                bw[s2] = __ballot_sync(0xffffffffu, valid && (left[s2] == build_left));
-                if (g == 0 && lane == 0) a.flags[(long long)t * (PT / 32) + wid * 4 + s2] = lw;
-                nleft += __popc(lw);
-            }
+                for (int s2 = 0; s2 < 4; ++s2) {
+                    const uint32_t ro = row_of(row[tt][s2]);
+                    raw[tt][s2] = s2 * 32 + lane >= rem[tt] ? 0u
+                                  : qm.dbits ? __ldg(qm.dbits + (ro >> 5))
+                                             : split_symbol(qm, ro, nd.f);
+                }
+            // (A) partition flags for the warp's 128 rows of each tile (4 per lane)
             int nbuild = 0;
             const uint32_t ltm = (1u << lane) - 1u;
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                if ((bw[s2] >> lane) & 1u) wrows[nbuild + __popc(bw[s2] & ltm)] = row[s2];
-                nbuild += __popc(bw[s2]);
-            }
-            if (g == 0 && lane == 0) {
-                if (nleft) atomicAdd(a.tile_left + t, nleft);
-                if (a.rows_ctr) {
-                    const long long nv = max(0ll, min((long long)WROWS, seg_end - base));
-                    bits_acc += (unsigned long long)nv * a.bits_parent_row +
-                                (a.no_hist ? 0ull : (unsigned long long)nbuild * a.bits_built_row);
+            for (int tt = 0; tt < TPS; ++tt) {
+                if (rem[tt] < 0 && tt > 0) break;  // warp-uniform
+                int nleft = 0;
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) {
+                    const bool valid = s2 * 32 + lane < rem[tt];
+                    const uint32_t ro = row_of(row[tt][s2]);
+                    const uint32_t rv = raw[tt][s2];
+                    const bool left = valid && (qm.dbits ? ((rv >> (ro & 31)) & 1u) != 0
+                                                         : ((int)rv == qm.B ? (nd.dl != 0) : ((int)rv <= nd.b)));
+                    const uint32_t lw = __ballot_sync(0xffffffffu, left);
+                    const uint32_t bw = __ballot_sync(0xffffffffu, valid && (left == build_left));
+                    if (g == 0 && lane == 0) a.flags[(long long)(t + tt) * (PT / 32) + wid * 4 + s2] = lw;
+                    nleft += __popc(lw);
+                    if ((bw >> lane) & 1u) wrows[nbuild + __popc(bw & ltm)] = row[tt][s2];
+                    nbuild += __popc(bw);
+                }
+                if (g == 0 && lane == 0) {
+                    if (nleft) atomicAdd(a.tile_left + t + tt, nleft);
+                    if (a.rows_ctr) bits_acc += (unsigned long long)max(0, rem[tt]) * a.bits_parent_row;
                 }
             }
+            if (g == 0 && lane == 0 && a.rows_ctr && !a.no_hist)
+                bits_acc += (unsigned long long)nbuild * a.bits_built_row;
             __syncwarp();
             if (no_hist) continue;  // partition only
             // (B) histogram of the listed rows
@@ -713,7 +753,7 @@ __global__ void __launch_bounds__(H_THREADS, 2) part_hist_ws_kernel(FusedArgs a)
         const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const int rt = a.n_items[2], t0 = tb + (run - a.run_base[j]) * rt, t1 = min(a.tile_base[j + 1], t0 + rt);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             for (int t = t0; t < t1; ++t) {
@@ -876,7 +916,7 @@ __global__ void __launch_bounds__(H_THREADS, WIDE ? 1 : 2) part_hist_sb_kernel(F
         const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const int rt = a.n_items[2], t0 = tb + (run - a.run_base[j]) * rt, t1 = min(a.tile_base[j + 1], t0 + rt);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             for (int t = t0; t < t1; ++t) {
@@ -1530,7 +1570,7 @@ __global__ void __launch_bounds__(H_THREADS) part_hist_col_kernel(ColFusedArgs a
         const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const int rt = a.n_items[2], t0 = tb + (run - a.run_base[j]) * rt, t1 = min(a.tile_base[j + 1], t0 + rt);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             if (g != 0) continue;
@@ -1665,7 +1705,7 @@ __global__ void __launch_bounds__(H_THREADS, 2) part_hist_cs_kernel(ColFusedArgs
         const int k = a.first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
-        const int t0 = tb + (run - a.run_base[j]) * a.run_tiles, t1 = min(a.tile_base[j + 1], t0 + a.run_tiles);
+        const int rt = a.n_items[2], t0 = tb + (run - a.run_base[j]) * rt, t1 = min(a.tile_base[j + 1], t0 + rt);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {
             if (g != 0) continue;
@@ -2579,6 +2619,7 @@ struct EvalArgs {
     int plan_groups, plan_run;
     int plan_split_only;            // record level path: items only for split parents
     int plan_run_min;               // loss-guided: smallest work item (tiles)
+    long long plan_rows;            // this rank's rows (plan_run < 0: tiles per item sized per level)
     int *tile_base, *run_base, *n_items;
     long long TB;
     const int32_t *cut_ptr;
@@ -2802,7 +2843,7 @@ __device__ void eval_finish(const EvalArgs &a, const TreeDev &t, const int *fin,
     __threadfence();
     if (a.plan_mode == 1)  // the children of this level are the next level's parents
         plan_block(a.nodes, a.first, a.n_nodes, a.plan_groups, a.plan_run, a.tile_base, a.run_base, a.n_items,
-                   a.plan_split_only != 0);
+                   a.plan_split_only != 0, a.plan_rows);
     else if (a.plan_mode == 2)
         lg_select_block(a, t, a.sel_step);
     if (threadIdx.x == 0) *a.done = 0;
@@ -3061,6 +3102,7 @@ __device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s) {
             a.tile_base[0] = a.tile_base[1] = 0;
             a.run_base[0] = a.run_base[1] = 0;
             a.n_items[0] = a.n_items[1] = 0;
+            a.n_items[2] = 1;
         } else {
             const int k = bk;
             NodeDev &nd = nodes[k];
@@ -3105,6 +3147,7 @@ __device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s) {
             a.run_base[1] = (int)runs;
             a.n_items[0] = (int)runs * a.plan_groups;
             a.n_items[1] = 0;
+            a.n_items[2] = (int)rt;
             s_tiles = tiles;
         }
     }
@@ -3695,7 +3738,7 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     // while step st's scatter still reads step st's plan on the side stream
     int *tile_base_b[2] = {A.take<int>(4), A.take<int>(4)};
     int *run_base_b[2] = {A.take<int>(4), A.take<int>(4)};
-    int *n_items_b[2] = {A.take<int>(2), A.take<int>(2)};
+    int *n_items_b[2] = {A.take<int>(4), A.take<int>(4)};
     NodeDev *nodes = A.take<NodeDev>(cap + 2);
     LgNode *lg = A.take<LgNode>(cap + 2);
     StepDev *step_b[2] = {A.take<StepDev>(1), A.take<StepDev>(1)};
@@ -4023,7 +4066,7 @@ int gbm_repartition(gbm_ctx *ctx, const gbm_qmatrix *q, const uint32_t *rows_d, 
     uint32_t *flags = A.take<uint32_t>((size_t)tiles * (PT / 32));
     int *tile_left = A.take<int>(tiles);
     int *tile_off = A.take<int>(tiles);
-    int *n_items = A.take<int>(2);  // [0] items, [1] work counter
+    int *n_items = A.take<int>(4);  // [0] items, [1] work counter, [2] tiles per item
     int *run_base = A.take<int>(4);
     unsigned long long *hist = A.take<unsigned long long>((size_t)std::max(1, q->cut_ptr_h[q->n_features]) * 2);
     Group *groups = A.take<Group>(hp.groups.size());
@@ -4233,7 +4276,7 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     int *tile_base_b[2] = {A.take<int>(2 * max_par + 2), A.take<int>(2 * max_par + 2)};
     NodeDev *nodes = A.take<NodeDev>(2 * cap + 2);
     int *run_base_b[2] = {A.take<int>(2 * max_par + 2), A.take<int>(2 * max_par + 2)};
-    int *n_items_b[2] = {A.take<int>(2), A.take<int>(2)};  // [0] items, [1] work counter
+    int *n_items_b[2] = {A.take<int>(4), A.take<int>(4)};  // [0] items, [1] work counter, [2] tiles per item
     Group *groups = A.take<Group>(hp.col ? 1 : G);
     ColGroup *cgroups = A.take<ColGroup>(hp.col ? G : 1);
     ColGroup *cg_root = A.take<ColGroup>(root_staged ? hr.cgroups.size() : 1);
@@ -4437,7 +4480,10 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
         1, std::min<long long>(RUN_MAX, (tiles_all * Gf + target - 1) / target));
     ea.plan_groups = rec ? 1 : Gf;
-    ea.plan_run = rec ? 1 : run_tiles;  // records: items of one 2048-row tile, split parents only
+    // auto: tiles per item chosen per level by the plan for the level kernel's resident blocks
+    const int lvl_blocks = sb_levels ? sb_grid : ws_levels ? ws_grid : hp.blocks_fused;
+    ea.plan_run = rec ? 1 : ctx->run_tiles > 0 ? run_tiles : -lvl_blocks;  // records: one-tile items, split parents only
+    ea.plan_rows = n;
     ea.plan_split_only = rec ? 1 : 0;
     ea.tile_base = tile_base_b[1];  // the root's evaluation plans level 1
     ea.run_base = run_base_b[1];

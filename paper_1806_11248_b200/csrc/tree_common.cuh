@@ -23,6 +23,9 @@ constexpr int H_THREADS = 512;   // histogram / fused kernels
 #ifndef GBM_PH_UNR
 #define GBM_PH_UNR 4
 #endif
+#ifndef GBM_PH_TPS  // tiles per step of the fused level kernel's byte path (1 or 2)
+#define GBM_PH_TPS 2
+#endif
 #ifndef GBM_PH_MINB
 #define GBM_PH_MINB 3
 #endif
