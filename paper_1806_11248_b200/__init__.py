@@ -335,6 +335,7 @@ class Context:
     EVAL_SLICED = 14
     CUTS_GATHER = 15
     ROOT_TENSOR = 16
+    LEVEL_REPLICAS = 17
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

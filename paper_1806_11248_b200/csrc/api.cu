@@ -306,6 +306,11 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->root_ct = (int)value;
         return GBM_OK;
     }
+    if (option == GBM_OPT_LEVEL_REPLICAS) {
+        if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_LEVEL_REPLICAS: 1 on (default), 0 off");
+        ctx->level_rep = (int)value;
+        return GBM_OK;
+    }
     if (option == GBM_OPT_CUTS_GATHER) {
         if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_CUTS_GATHER: 0 per-feature ownership, 1 all-gather");
         ctx->cuts_gather = (int)value;

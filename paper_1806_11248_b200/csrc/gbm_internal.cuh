@@ -118,11 +118,12 @@ struct gbm_ctx {
     int seg_hist = 0;              // GBM_OPT_SEGMENT_HIST (0 auto, 1 off, 2 on)
     int stage_tma = 1;             // staged root: TMA bulk row copies (GBM_OPT_TMA_ROWS)
     int row_decide = 0;            // GBM_OPT_ROW_DECIDE (2 on; measured slower, off by default)
-    int level_path = 0;
-    int level_hist = 0;
-    int eval_sliced = 0;
-    int cuts_gather = 0;
-    int root_ct = 0;               // GBM_OPT_ROOT_TENSOR (0 auto = tensor-fed root where it applies, 1 off)           // GBM_OPT_CUTS_GATHER (1: C3 as an all-gather of X, not per-feature ownership)           // GBM_OPT_EVAL_SLICED (1: reduce-scatter + feature-sliced evaluation)            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed bank-column)            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
+    int level_path = 0;            // GBM_OPT_LEVEL_PATH (0 auto, 1 row-index lists, 2 records)
+    int level_hist = 0;            // GBM_OPT_LEVEL_HIST (0 auto, 1 compact, 2 shuffle-fed, 3 warp-specialised)
+    int eval_sliced = 0;           // GBM_OPT_EVAL_SLICED (1: reduce-scatter + feature-sliced evaluation)
+    int cuts_gather = 0;           // GBM_OPT_CUTS_GATHER (1: C3 as an all-gather of X)
+    int root_ct = 0;               // GBM_OPT_ROOT_TENSOR (0 auto, 1 off, 2-4 tensor-fed root shapes)
+    int level_rep = 1;             // GBM_OPT_LEVEL_REPLICAS (1: replicated low-cardinality bins)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     std::vector<int> tree_slice_key;   // feature-slice tables currently uploaded (sliced evaluation)

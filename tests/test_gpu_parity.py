@@ -387,6 +387,29 @@ def test_level_hist_layouts_parity(ctx, G, cfg, n, missing, align, P, B, depth, 
     ctx.set_option(ctx.RUN_TILES, 0)
 
 
+@pytest.mark.parametrize("rep", [1, 0])
+@pytest.mark.parametrize("cfg,n,missing,P,B", [("airline", 250_000, 0.0, 15, None), ("airline", 120_000, 0.1, 30, None),
+                                               ("higgs", 200_000, 0.0, 15, None), ("yearmsd", 60_000, 0.0, 15, 16),
+                                               ("higgs", 100_000, 0.05, 15, 3), ("epsilon", 20_000, 0.0, 15, 8)])
+def test_level_replicas_parity(ctx, G, cfg, n, missing, P, B, rep):
+    """GBM_OPT_LEVEL_REPLICAS: copies of the bins of low-cardinality features in the fused level
+    kernel (row slot r adds into copy r mod R, folded before the flush) -- Airline's few-level
+    columns, Higgs's b-tags, every feature at 16 / 8 / 3 bins (copies capped by REP_CAP), missing
+    values (sentinel skipped) and P = 30 (four channels); bit for bit against the oracle."""
+    ctx.set_option(ctx.LEVEL_REPLICAS, rep)
+    c = W.CONFIGS[cfg]
+    B = B or c.max_bins
+    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
+    ob = O.Booster(X, y, max_bins=B, objective=c.objective, max_depth=c.max_depth, grad_bits=P)
+    gb = G.Booster(ctx, dev(X), dev(y), max_bins=B, objective=c.objective, max_depth=c.max_depth,
+                   grad_bits=P, base_margin=ob.base_margin)
+    for _ in range(2):
+        _compare_tree(gb.round().to_numpy(), ob.round())
+        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
+        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
+    ctx.set_option(ctx.LEVEL_REPLICAS, 1)
+
+
 @pytest.mark.parametrize("run_tiles", [2, 5, 8, 31])
 @pytest.mark.parametrize("cfg,n,missing,P", [("higgs", 300_000, 0.0, 15), ("airline", 250_000, 0.0, 15),
                                              ("higgs", 200_000, 0.0, 30), ("bosch", 40_000, 0.0, 15)])
