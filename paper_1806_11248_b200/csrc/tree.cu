@@ -2416,13 +2416,15 @@ __device__ __forceinline__ void eval_candidate_dl(long long Pg, long long Ph, lo
 // Register-blocked: lane owns KB consecutive bins of each 32*KB-bin chunk, so all histogram
 // loads of a chunk are in flight together; the prefix is a per-lane serial scan plus one warp
 // scan of the lane totals.
-// warp variant: bins per lane per chunk, and resident blocks it is compiled for -- occupancy
-// matters more than ILP here (Epsilon 4.53 ms/round at KB 2 / 4 blocks vs 5.05 at KB 8 / 1)
+// warp variant: bins per lane per chunk, and resident blocks it is compiled for.  Measured
+// (Epsilon evaluation, ms/round): KB 2 at 4 blocks (64 registers) spills ~1.7 KB per thread, 0.84;
+// KB 2 at 2 blocks (no spills) 0.69; KB 4 / 2 blocks 0.77; KB 8 / 2 blocks 0.90; KB 8 / 1 1.18
+// (Bosch 0.56 -> 0.48 at KB 2 / 2 blocks)
 #ifndef GBM_EVAL_KB
 #define GBM_EVAL_KB 2
 #endif
 #ifndef GBM_EVAL_MINB
-#define GBM_EVAL_MINB 4
+#define GBM_EVAL_MINB 2
 #endif
 constexpr int KB = GBM_EVAL_KB;
 __device__ FeatBest eval_feature(const NodeHist &src, int b0, int nbf, long long Tg, long long Th, int sg, int sh,
