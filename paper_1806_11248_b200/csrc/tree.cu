@@ -3203,7 +3203,7 @@ __device__ void lg_select_block(const EvalArgs &a, const TreeDev &t, int s) {
             const long long tiles = nd.count > 0 ? (nd.count + PT - 1) / PT : 0;
             // about plan_run (4 x resident blocks) items for this parent (the depth-wise rule)
             const long long rt = max((long long)a.plan_run_min,
-                                     min((long long)RUN_MAX, (tiles * a.plan_groups + a.plan_run - 1) / a.plan_run));
+                                     min((long long)(MAX_CHUNK / PT), (tiles * a.plan_groups + a.plan_run - 1) / a.plan_run));
             const long long runs = (tiles + rt - 1) / rt;
             step->run_tiles = (int)rt;
             a.tile_base[0] = 0;
@@ -3891,7 +3891,10 @@ static int build_tree_lossguide(gbm_ctx *ctx, const gbm_qmatrix *q, const QM &qm
     ea.n_nodes = 1;
     ea.hist_store = grow ? hist_pool : nullptr;  // the root's histogram -> pool slot 0
     const long long tiles_all = (n + PT - 1) / PT;
-    const long long target = 4ll * hp.blocks_fused;
+#ifndef GBM_LG_ITEMS  // work items per resident block for a large parent (measured, Higgs 64
+#define GBM_LG_ITEMS 1  // leaves: 5.93 ms/round at 4, 5.81 at 2, 5.54 at 1 -- fewer flushes)
+#endif
+    const long long target = (long long)GBM_LG_ITEMS * hp.blocks_fused;
     const int run_tiles = ctx->run_tiles > 0 ? ctx->run_tiles : (int)std::max<long long>(
         1, std::min<long long>(RUN_MAX, (tiles_all * G + target - 1) / target));
     ea.done = done;
