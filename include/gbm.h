@@ -162,17 +162,12 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  * GBM_OPT_LEVEL_REPLICAS: 1 (default) = the fused level histogram of byte symbols keeps R <= 8
  *   copies of the bins of each feature with few bins (R x bins <= 128), row slot r adding into
  *   copy r mod R, folded before the flush: lanes hitting one bin of a low-cardinality feature no
- *   longer serialise on one shared-memory word; 0 = one copy.  Same histogram.
- * GBM_OPT_GROUP_DECISIONS: matrices of several shared-memory feature groups (byte symbols):
- *   2 = a partition-only launch decides each level's rows once (one 2048-row tile per item,
- *   flags + left counts) and every group's histogram item reads those flags; 1 = every group
- *   re-gathers the split symbols; 0 (default) = 2 from 16 groups on (measured).  Same partition
- *   and histograms. */
+ *   longer serialise on one shared-memory word; 0 = one copy.  Same histogram. */
 enum { GBM_OPT_HIST_LAYOUT = 1, GBM_OPT_CARRY_GRADIENTS = 2, GBM_OPT_RUN_TILES = 3, GBM_OPT_GROUP_UNITS = 4,
        GBM_OPT_EVAL_WARP = 5, GBM_OPT_LEAF_WALK = 6, GBM_OPT_EVAL_SCREEN = 7, GBM_OPT_SEGMENT_HIST = 8,
        GBM_OPT_TMA_ROWS = 10, GBM_OPT_ROW_DECIDE = 11, GBM_OPT_LEVEL_PATH = 12, GBM_OPT_LEVEL_HIST = 13,
        GBM_OPT_EVAL_SLICED = 14, GBM_OPT_CUTS_GATHER = 15, GBM_OPT_ROOT_TENSOR = 16,
-       GBM_OPT_LEVEL_REPLICAS = 17, GBM_OPT_GROUP_DECISIONS = 18 };
+       GBM_OPT_LEVEL_REPLICAS = 17 };
 GBM_API int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value);
 
 /* ---------------------------------------------------------------- communicator

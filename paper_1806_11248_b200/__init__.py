@@ -336,7 +336,6 @@ class Context:
     CUTS_GATHER = 15
     ROOT_TENSOR = 16
     LEVEL_REPLICAS = 17
-    GROUP_DECISIONS = 18
 
     def set_option(self, option: int, value: int):
         _call("gbm_set_option", self.h, int(option), int(value))

@@ -311,11 +311,6 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         ctx->level_rep = (int)value;
         return GBM_OK;
     }
-    if (option == GBM_OPT_GROUP_DECISIONS) {
-        if (value < 0 || value > 2) return fail(GBM_E_ARG, "GBM_OPT_GROUP_DECISIONS: 0 auto, 1 off, 2 on");
-        ctx->group_decisions = (int)value;
-        return GBM_OK;
-    }
     if (option == GBM_OPT_CUTS_GATHER) {
         if (value < 0 || value > 1) return fail(GBM_E_ARG, "GBM_OPT_CUTS_GATHER: 0 per-feature ownership, 1 all-gather");
         ctx->cuts_gather = (int)value;

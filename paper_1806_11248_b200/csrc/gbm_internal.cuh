@@ -124,7 +124,6 @@ struct gbm_ctx {
     int cuts_gather = 0;           // GBM_OPT_CUTS_GATHER (1: C3 as an all-gather of X)
     int root_ct = 0;               // GBM_OPT_ROOT_TENSOR (0 auto, 1 off, 2-4 tensor-fed root shapes)
     int level_rep = 1;             // GBM_OPT_LEVEL_REPLICAS (1: replicated low-cardinality bins)
-    int group_decisions = 0;       // GBM_OPT_GROUP_DECISIONS (0 auto, 1 off, 2 on: one partition pass for all groups)
     int walk_mode = 0;             // GBM_OPT_LEAF_WALK (0 auto = staged rows, 1 feature-major copy)
     std::vector<int> tree_groups_key;  // group table currently uploaded in tree_arena
     std::vector<int> tree_slice_key;   // feature-slice tables currently uploaded (sliced evaluation)

@@ -502,12 +502,7 @@ struct FusedArgs {
     int bits_built_row;            // packed row + qpair, per row of the built child
     int no_hist;                   // partition only (flags + left counts): hist_seg_kernel follows
     int rep_cap;                   // > 0: replicated low-cardinality bins (byte path, REP_CAP words)
-    // several feature groups: a partition-only launch (no_hist, group 0 only) writes the flags
-    // first; then every group reads its rows' decisions from them instead of re-gathering the
-    // split symbols (flags and tile_left are not written again)
-    int flags_in;
 };
-
 
 // Warp-independent: each warp owns 64 rows of every tile of the item (no block barrier
 // inside an item).  Per 64-row batch: (A) split symbol of each row -> left flags (ballot), the
@@ -531,27 +526,14 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int n_items = *a.n_items;
     E *wrows = s_rows[wid];
-    // the partition-only pass of several feature groups (GBM_OPT_GROUP_DECISIONS) takes one
-    // 2048-row tile per work item: the level's items are sized for the G groups' histograms
-    const bool by_tile = a.no_hist && a.n_groups > 1;
-    const int n_work = by_tile ? a.tile_base[a.n_par] : n_items;
-    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_work;
+    for (int it = claim_item(const_cast<int *>(a.n_items) + 1); it < n_items;
          it = claim_item(const_cast<int *>(a.n_items) + 1)) {
-        int g = 0, j, t0, t1;
-        if (by_tile) {
-            j = find_parent(a.tile_base, a.n_par, it);
-            t0 = it;
-            t1 = it + 1;
-        } else {
-            const int run = it / a.n_groups;
-            g = it - run * a.n_groups;
-            j = find_parent(a.run_base, a.n_par, run);
-            t0 = a.tile_base[j] + (run - a.run_base[j]) * run_tiles;
-            t1 = min(a.tile_base[j + 1], t0 + run_tiles);
-        }
+        const int run = it / a.n_groups, g = it - run * a.n_groups;
+        const int j = find_parent(a.run_base, a.n_par, run);
         const int k = first + j;
         const NodeDev nd = a.nodes[k];
         const int tb = a.tile_base[j];
+        const int t0 = tb + (run - a.run_base[j]) * run_tiles, t1 = min(a.tile_base[j + 1], t0 + run_tiles);
         const long long seg_end = nd.start + nd.count;
         if (nd.state == GBM_NODE_LEAF) {  // rows stay in this leaf
             if (g != 0) continue;
@@ -578,7 +560,6 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
             smem_zero<WIDE>(h);
             load_group(qm, grp, a.cut_ptr, s_off);
         }
-        const bool use_flags = a.flags_in != 0;  // decisions from the partition-only pass
         if (rep_on && wid == 0) {  // the replica plan: s_rep[fl] = (word of copy 1) << 4 | log2 R
             int carry = 0;
             for (int c0 = 0; c0 < nf; c0 += 32) {
@@ -655,8 +636,7 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
 #pragma unroll
                 for (int s2 = 0; s2 < 4; ++s2) {
                     const uint32_t ro = row_of(row[tt][s2]);
-                    raw[tt][s2] = use_flags ? (rem[tt] > s2 * 32 ? __ldcg(a.flags + (long long)(t + tt) * (PT / 32) + wid * 4 + s2) : 0u)
-                                  : s2 * 32 + lane >= rem[tt] ? 0u
+                    raw[tt][s2] = s2 * 32 + lane >= rem[tt] ? 0u
                                   : qm.dbits ? __ldg(qm.dbits + (ro >> 5))
                                              : split_symbol(qm, ro, nd.f);
                 }
@@ -672,17 +652,16 @@ __global__ void __launch_bounds__(H_THREADS, BYTE ? PH_MINB_BYTE : PH_MINB) part
                     const bool valid = s2 * 32 + lane < rem[tt];
                     const uint32_t ro = row_of(row[tt][s2]);
                     const uint32_t rv = raw[tt][s2];
-                    const bool left = valid && (use_flags ? ((rv >> lane) & 1u) != 0
-                                                : qm.dbits ? ((rv >> (ro & 31)) & 1u) != 0
-                                                           : ((int)rv == qm.B ? (nd.dl != 0) : ((int)rv <= nd.b)));
+                    const bool left = valid && (qm.dbits ? ((rv >> (ro & 31)) & 1u) != 0
+                                                         : ((int)rv == qm.B ? (nd.dl != 0) : ((int)rv <= nd.b)));
                     const uint32_t lw = __ballot_sync(0xffffffffu, left);
                     const uint32_t bw = __ballot_sync(0xffffffffu, valid && (left == build_left));
-                    if (g == 0 && lane == 0 && !use_flags) a.flags[(long long)(t + tt) * (PT / 32) + wid * 4 + s2] = lw;
+                    if (g == 0 && lane == 0) a.flags[(long long)(t + tt) * (PT / 32) + wid * 4 + s2] = lw;
                     nleft += __popc(lw);
                     if ((bw >> lane) & 1u) wrows[nbuild + __popc(bw & ltm)] = row[tt][s2];
                     nbuild += __popc(bw);
                 }
-                if (g == 0 && lane == 0 && !use_flags) {
+                if (g == 0 && lane == 0) {
                     if (nleft) atomicAdd(a.tile_left + t + tt, nleft);
                     if (a.rows_ctr) bits_acc += (unsigned long long)max(0, rem[tt]) * a.bits_parent_row;
                 }
@@ -4634,12 +4613,6 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
     fa.TB = std::max<long long>(TB, 1);
     fa.hstride = hp.hstride;
     fa.rep_cap = hp.rep_cap;
-    // several feature groups (byte path): a partition-only pass decides each level's rows once and
-    // every group's histogram item reads the flags (GBM_OPT_GROUP_DECISIONS).  Measured (levels,
-    // ms/round): Epsilon (63 groups) 2.549 -> 2.518, YearMSD (3 groups) 0.252 -> 0.298 (the extra
-    // launch outweighs two groups' split-symbol gathers), so auto = at least 16 groups
-    const bool shared_dec = (ctx->group_decisions == 2 || (ctx->group_decisions == 0 && Gf >= 16)) && !hp.col &&
-                            hp.byte_path && Gf > 1 && !rec && !ws_levels && !sb_levels && !seg_mode;
     const int pgrid = ctx->sm_count * 8;
     for (int l = 1; l <= D; ++l) {
         const int first = (1 << (l - 1)) - 1, n_par = 1 << (l - 1);
@@ -4819,19 +4792,7 @@ static int build_tree_impl(gbm_ctx *ctx, const gbm_qmatrix *q, const int32_t *qp
                 else part_hist_sb_kernel<false><<<sb_grid, H_THREADS, smb, s>>>(fa);
                 GBM_CUDA(cudaGetLastError());
             } else {
-                if (shared_dec) {  // decide once (group-0 items only), then every group from the flags
-                    FusedArgs fd = fa;
-                    fd.no_hist = 1;
-                    fd.bits_built_row = 0;
-                    GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fd, s, hp.carry));
-                    GBM_CUDA(cudaMemsetAsync(n_items + 1, 0, sizeof(int), s));  // the work counter
-                    FusedArgs fh = fa;
-                    fh.flags_in = 1;
-                    fh.bits_parent_row = 0;  // the parent rows were counted by the partition pass
-                    GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fh, s, hp.carry));
-                } else {
-                    GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));
-                }
+                GBM_TRY(GBM_DISPATCH(hp, launch_fused, ctx, hp, fa, s, hp.carry));
             }
         }
         // side stream: scan + scatter of this level, concurrent with the allreduce and (after the

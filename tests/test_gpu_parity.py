@@ -410,34 +410,6 @@ def test_level_replicas_parity(ctx, G, cfg, n, missing, P, B, rep):
     ctx.set_option(ctx.LEVEL_REPLICAS, 1)
 
 
-@pytest.mark.parametrize("dec", [2, 1])
-@pytest.mark.parametrize("cfg,n,missing,P,units,run_tiles", [("yearmsd", 120_000, 0.0, 15, 0, 0),
-                                                             ("epsilon", 30_000, 0.0, 15, 0, 0),
-                                                             ("higgs", 200_000, 0.05, 30, 2, 3),
-                                                             ("airline", 150_000, 0.0, 15, 1, 31),
-                                                             ("higgs", 90_000, 0.0, 15, 1, 1)])
-def test_group_decisions_parity(ctx, G, cfg, n, missing, P, units, run_tiles, dec):
-    """GBM_OPT_GROUP_DECISIONS: with several feature groups, a partition-only launch decides the
-    level's rows (one tile per item) and every group's histogram item reads the flags --
-    YearMSD (3 groups), Epsilon (63), Higgs / Airline split into 4-28 groups by GROUP_UNITS,
-    missing values, P = 30, 1- to 31-tile items; bit for bit against the oracle."""
-    ctx.set_option(ctx.GROUP_DECISIONS, dec)
-    ctx.set_option(ctx.GROUP_UNITS, units)
-    ctx.set_option(ctx.RUN_TILES, run_tiles)
-    c = W.CONFIGS[cfg]
-    X, y = W.generate(cfg, 0, n, n_rows=max(n, c.n_rows), missing=missing)
-    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth, grad_bits=P)
-    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=c.max_depth,
-                   grad_bits=P, base_margin=ob.base_margin)
-    for _ in range(2):
-        _compare_tree(gb.round().to_numpy(), ob.round())
-        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
-        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
-    ctx.set_option(ctx.GROUP_DECISIONS, 0)
-    ctx.set_option(ctx.GROUP_UNITS, 0)
-    ctx.set_option(ctx.RUN_TILES, 0)
-
-
 @pytest.mark.parametrize("run_tiles", [2, 5, 8, 31])
 @pytest.mark.parametrize("cfg,n,missing,P", [("higgs", 300_000, 0.0, 15), ("airline", 250_000, 0.0, 15),
                                              ("higgs", 200_000, 0.0, 30), ("bosch", 40_000, 0.0, 15)])
@@ -685,26 +657,6 @@ def test_lossguide_rounds_parity(ctx, G, cfg, n, missing, align, P, rounds, D, L
     np.testing.assert_array_equal(gb.predict(dev(X)).cpu().numpy(), ob.predict())
     np.testing.assert_array_equal(gb.predict(dev(Xt)).cpu().numpy(), ob.predict(Xt))
     ctx.set_option(ctx.CARRY_GRADIENTS, 0)
-
-
-@pytest.mark.parametrize("run_tiles", [31, 3])
-def test_lossguide_large_items_parity(ctx, G, run_tiles):
-    """Loss-guided steps with work items of up to 31 tiles (63488 rows per shared-memory flush,
-    the exactness bound) and of 3: bit for bit against the oracle."""
-    ctx.set_option(ctx.RUN_TILES, run_tiles)
-    c = W.CONFIGS["higgs"]
-    X, y = W.generate("higgs", 0, 400_000)
-    kw = dict(eta=0.3, reg_lambda=1.0, gamma=0.0)
-    ob = O.Booster(X, y, max_bins=c.max_bins, objective=c.objective, max_depth=12, grad_bits=15,
-                   mcw=1.0, grow_policy="lossguide", max_leaves=24, **kw)
-    gb = G.Booster(ctx, dev(X), dev(y), max_bins=c.max_bins, objective=c.objective, max_depth=12,
-                   grad_bits=15, base_margin=ob.base_margin, min_child_weight=1.0, grow_policy="lossguide",
-                   max_leaves=24, **kw)
-    for _ in range(2):
-        _compare_tree(gb.round().to_numpy(), ob.round())
-        np.testing.assert_array_equal(gb.row_leaf.cpu().numpy(), ob.last["row_leaf"])
-        np.testing.assert_array_equal(gb.margin.cpu().numpy(), ob.margin)
-    ctx.set_option(ctx.RUN_TILES, 0)
 
 
 def test_depthwise_trees_carry_links(ctx, G):
