@@ -93,6 +93,29 @@ __global__ void pack_kernel(const uint16_t *__restrict__ bins, const float *__re
     }
 }
 
+// Byte symbols with rows of whole words (the common layout): word w = (row, unit u) by one 32-bit
+// division, its 4 symbols from X[row][4u .. 4u+3] -- the generic walk above spends two 64-bit
+// divisions per element (Higgs 11M x 28: 1.35 ms).
+__global__ void pack_byte_kernel(const float *__restrict__ X, int F, uint32_t W, const float *__restrict__ cv,
+                                 const int32_t *__restrict__ cp, int B, uint32_t *__restrict__ out,
+                                 uint32_t n_words, uint32_t *dev_err) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_words; w += gridDim.x * blockDim.x) {
+        const uint32_t row = w / W, u = w - row * W;
+        const float *xr = X + (size_t)row * F;
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int f = (int)(4 * u) + j;
+            if (f < F) {
+                const uint32_t s = (uint32_t)quantise_one(__ldg(xr + f), f, cv, cp, B, dev_err);
+                if (s >> 8) atomicOr(dev_err, DERR_OVERFLOW);
+                word |= (s & 255u) << (8 * j);
+            }
+        }
+        out[w] = word;
+    }
+}
+
 // ------------------------------------------------------------------ cuts: radix sort machinery
 constexpr int SORT_THREADS = 256;                 // 8 warps
 constexpr int SORT_ITEMS = 16;                    // per thread
@@ -102,35 +125,47 @@ constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // 4096 keys per tile
 __global__ void keys_kernel(const float *__restrict__ X, long long n, int F, long long n_pad,
                             uint32_t *__restrict__ keys, unsigned long long *__restrict__ present,
                             uint32_t *dev_err) {
-    // grid: x over row blocks of 32, y over feature blocks of 32; transpose through smem
+    // grid: x strides over row blocks of 32, y over feature blocks of 32; transpose through smem.
+    // The present-value counts stay in registers (4 features per thread) and reach `present`
+    // once per (block, feature): one atomic per 32-row block serialised on F addresses.
     __shared__ uint32_t t[32][33];
-    long long r0 = (long long)blockIdx.x * 32;
-    int f0 = blockIdx.y * 32;
-    int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    unsigned cnt = 0;
-    for (int k = ty; k < 32; k += 8) {
-        long long r = r0 + k;
-        int f = f0 + tx;
-        uint32_t key = KEY_MISSING;
-        if (r < n && f < F) {
-            float v = __ldg(X + r * F + f);
-            if (isinf(v)) atomicOr(dev_err, DERR_NONFINITE);
-            if (!isnan(v)) key = float_key(v);
+    const int f0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    unsigned cnt[4] = {0u, 0u, 0u, 0u};
+    unsigned err = 0;
+    for (long long r0 = (long long)blockIdx.x * 32; r0 < n_pad; r0 += (long long)gridDim.x * 32) {
+        for (int k = ty; k < 32; k += 8) {
+            const long long r = r0 + k;
+            const int f = f0 + tx;
+            uint32_t key = KEY_MISSING;
+            if (r < n && f < F) {
+                const float v = __ldg(X + r * F + f);
+                if (isinf(v)) err = 1;
+                if (!isnan(v)) key = float_key(v);
+            }
+            t[k][tx] = key;
         }
-        t[k][tx] = key;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k = ty + 8 * i;
+            const int f = f0 + k;
+            const long long r = r0 + tx;
+            if (f < F && r < n_pad) {
+                const uint32_t key = t[tx][k];
+                keys[(long long)f * n_pad + r] = key;
+                cnt[i] += key != KEY_MISSING;
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-        int f = f0 + k;
-        long long r = r0 + tx;
-        if (f < F && r < n_pad) {
-            uint32_t key = t[tx][k];
-            keys[(long long)f * n_pad + r] = key;
-            cnt = __popc(__ballot_sync(0xffffffffu, key != KEY_MISSING));
-            if (tx == 0 && cnt) atomicAdd(present + f, (unsigned long long)cnt);
-        } else {
-            __ballot_sync(0xffffffffu, false);
-        }
+    if (err) atomicOr(dev_err, DERR_NONFINITE);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        unsigned c = cnt[i];
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        const int f = f0 + ty + 8 * i;
+        if (tx == 0 && f < F && c) atomicAdd(present + f, (unsigned long long)c);
     }
 }
 
@@ -454,9 +489,19 @@ int gbm_quantise_compress(gbm_ctx *ctx, const float *X_d, int64_t n_rows, int32_
     }
     long long stride = row_stride_bits(F, bits, row_align_bits);
     ProfScope ps(ctx, PC_QUANT, (cudaStream_t)stream, (double)n_rows * F * 4 + (double)packed_words * 4);
-    pack_kernel<true><<<grid_for(packed_words, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
-        nullptr, X_d, n_rows, F, bits, stride, cv, cp, max_bins, packed_d, packed_words,
-        ctx->dev_err);
+    const long long row_words = stride / 32, data_words = (long long)n_rows * row_words;
+    if (bits == 8 && stride % 32 == 0 && data_words < (1ll << 32)) {
+        // the words past the last row (if any) stay zero
+        if (packed_words > data_words)
+            GBM_CUDA(cudaMemsetAsync(packed_d + data_words, 0, (size_t)(packed_words - data_words) * 4,
+                                     (cudaStream_t)stream));
+        pack_byte_kernel<<<grid_for(data_words, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
+            X_d, F, (uint32_t)row_words, cv, cp, max_bins, packed_d, (uint32_t)data_words, ctx->dev_err);
+    } else {
+        pack_kernel<true><<<grid_for(packed_words, 256, ctx->sm_count), 256, 0, (cudaStream_t)stream>>>(
+            nullptr, X_d, n_rows, F, bits, stride, cv, cp, max_bins, packed_d, packed_words,
+            ctx->dev_err);
+    }
     GBM_CUDA(cudaGetLastError());
     return GBM_OK;
 }
@@ -485,7 +530,7 @@ static int cuts_core(gbm_ctx *ctx, const float *Xg, long long n_all, int F, int 
     int32_t *nbins_plain = A.take<int32_t>(F);
     GBM_CUDA(cudaMemsetAsync(present, 0, (size_t)F * 8, s));
     GBM_CUDA(cudaMemsetAsync(ctx->dev_err, 0, 4, s));
-    dim3 tg((unsigned)((n_pad + 31) / 32), (unsigned)((F + 31) / 32));
+    dim3 tg((unsigned)std::min<long long>((n_pad + 31) / 32, 16ll * ctx->sm_count), (unsigned)((F + 31) / 32));
     keys_kernel<<<tg, 256, 0, s>>>(Xg, n_all, F, n_pad, kA, present, ctx->dev_err);
     GBM_CUDA(cudaGetLastError());
     dim3 sg((unsigned)tiles, (unsigned)F);

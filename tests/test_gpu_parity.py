@@ -103,12 +103,16 @@ def test_compress_parity(ctx, bits, align):
     np.testing.assert_array_equal(u32(words), O.pack(sym, bits, align))
 
 
-@pytest.mark.parametrize("cfg,align", [("tiny", 0), ("higgs", 32), ("airline", 128),
-                                       ("yearmsd", 32)])
-def test_quantise_compress_parity(ctx, G, cfg, align):
-    X, _ = W.generate(cfg, 0, 2000 if cfg == "tiny" else 40_000,
-                      missing=0.03 if cfg == "tiny" else 0.0)
-    B = W.CONFIGS[cfg].max_bins
+@pytest.mark.parametrize("cfg,align,B,missing", [("tiny", 0, None, 0.03), ("higgs", 32, None, 0.0),
+                                                 ("airline", 128, None, 0.0), ("yearmsd", 32, None, 0.0),
+                                                 ("higgs", 256, 200, 0.05), ("airline", 32, 255, 0.02),
+                                                 ("epsilon", 32, None, 0.0)])
+def test_quantise_compress_parity(ctx, G, cfg, align, B, missing):
+    """The fused bin map + pack: the generic walk and the byte kernel (8-bit symbols, rows of whole
+    words: padding slots and words, the missing sentinel inside 8 bits)."""
+    X, _ = W.generate(cfg, 0, 2000 if cfg == "tiny" else 3000 if cfg == "epsilon" else 40_000,
+                      n_rows=None if cfg != "epsilon" else 3000, missing=missing)
+    B = B or W.CONFIGS[cfg].max_bins
     v, p = O.cuts(X, B)
     s, mx = O.symbols(X, v, p, B)
     bits = O.symbol_bits(mx)
