@@ -155,10 +155,12 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   owner cuts its features over the global rows and the cuts are all-gathered -- O(n F / p) per
  *   rank; 1 = all-gather every shard's X to every rank (O(n F) per rank).  Same cuts either way.
  * GBM_OPT_ROOT_TENSOR: the root histogram of byte-symbol matrices with the feature-major copy
- *   (gbm_transpose_symbols) and n a multiple of 16: 2 = every warp fetches a [features x 32 rows]
- *   tile of that copy with one TMA tensor copy and lane f holds its feature's 32 symbols in
- *   registers (root_ct.cu); 1 = the staged packed rows; 0 (default) = 2 when there are several
- *   feature groups (> 32 features) or <= 16 features, else 1 (measured).  Same histogram.
+ *   (gbm_transpose_symbols) and n a multiple of 16: every warp fetches a [features x TR rows]
+ *   tile of that copy with one TMA tensor copy and lane f holds its feature's symbols in
+ *   registers (root_ct.cu); 1 = the staged packed rows; 2-7 = the tensor-fed root with (warps x
+ *   stages x TR) 16x2x32, 12x3x32, 8x4x32, 8x2x64, 16x2x64, 16x2x128; 0 (default) = 2 with several
+ *   feature groups (> 32 features) or <= 16 features, 6 for one group of 17..32 features
+ *   (narrow accumulators), else 1 (measured).  Same histogram.
  * GBM_OPT_LEVEL_REPLICAS: 1 (default) = the fused level histogram of byte symbols keeps R <= 8
  *   copies of the bins of each feature with few bins (R x bins <= 128), row slot r adding into
  *   copy r mod R, folded before the flush: lanes hitting one bin of a low-cardinality feature no

@@ -301,8 +301,9 @@ int gbm_set_option(gbm_ctx *ctx, int32_t option, int64_t value) {
         return GBM_OK;
     }
     if (option == GBM_OPT_ROOT_TENSOR) {
-        if (value < 0 || value > 4)
-            return fail(GBM_E_ARG, "GBM_OPT_ROOT_TENSOR: 0 auto, 1 off, 2-4 always (pipeline shapes 16x2, 12x3, 8x4)");
+        if (value < 0 || value > 7)
+            return fail(GBM_E_ARG, "GBM_OPT_ROOT_TENSOR: 0 auto, 1 off, 2-7 always (warps x stages x tile rows: "
+                                   "16x2x32, 12x3x32, 8x4x32, 8x2x64, 16x2x64, 16x2x128)");
         ctx->root_ct = (int)value;
         return GBM_OK;
     }

@@ -19,9 +19,10 @@
 namespace gbm {
 
 
+template <int TR>
 struct __align__(128) CtBuf {  // one staging buffer of a warp (tensor-copy destination)
-    uint8_t sym[32][32];       // [feature of the group][row of the batch]
-    int2 q[32];
+    uint8_t sym[32][TR];       // [feature of the group][row of the batch]
+    int2 q[TR];
 };
 
 struct CtArgs {
@@ -61,11 +62,13 @@ __device__ __forceinline__ void col_red2(unsigned addr, int qx, int qy) {
 }
 
 // R rows per accumulate step: lane = copy * Fg + feature, copy c takes rows c, c + R, ...
-template <bool WIDE, int R, int NW, int NS>
+// TR rows per tensor tile (32, 64 or 128): each feature's piece of a tile is TR contiguous bytes.
+template <bool WIDE, int R, int NW, int NS, int TR>
 __global__ void __launch_bounds__(NW * 32, WIDE ? 1 : 2) hist_ct_root_kernel(const __grid_constant__ CUtensorMap map,
                                                                             CtArgs a) {
     extern __shared__ __align__(128) int smem[];
     constexpr int CH = WIDE ? 4 : 2;
+    using CtBuf = gbm::CtBuf<TR>;
     CtBuf *stage = reinterpret_cast<CtBuf *>(smem + CH * COLB_STRIDE);  // [NW][NS]
     __shared__ uint64_t s_bar[NS * NW];
     __shared__ long long s_red[2 * NW];
@@ -99,18 +102,19 @@ __global__ void __launch_bounds__(NW * 32, WIDE ? 1 : 2) hist_ct_root_kernel(con
         // this warp's 32-row batches b0 = start + 32 (wid + NW m) < end; the last one of the
         // matrix may hold 16 rows (n is a multiple of 16): the tensor copy zero-fills the rows past
         // n, the pair copy takes 16 rows and the rest of the pairs are zeroed (adds of 0)
-        const long long b_first = start + 32ll * wid;
-        const int nb = b_first < end ? (int)((end - b_first - 1) / (32ll * NW)) + 1 : 0;
+        const long long b_first = start + (long long)TR * wid;
+        const int nb = b_first < end ? (int)((end - b_first - 1) / ((long long)TR * NW)) + 1 : 0;
         auto issue = [&](int m, unsigned cb) {
-            const long long b0 = b_first + 32ll * NW * m;
-            const int rows = (int)min(32ll, end - b0);
-            if (rows < 32) {
-                if (lane >= rows) buf[cb].q[lane] = make_int2(0, 0);
+            const long long b0 = b_first + (long long)TR * NW * m;
+            const int rows = (int)min((long long)TR, end - b0);
+            if (rows < TR) {
+                for (int i = lane; i < TR; i += 32)
+                    if (i >= rows) buf[cb].q[i] = make_int2(0, 0);
                 __syncwarp();
             }
             if (lane == 0) {
                 fence_proxy_async();
-                mbar_arrive_expect_tx(bar + cb, 32u * a.fbox + 8u * rows);
+                mbar_arrive_expect_tx(bar + cb, (unsigned)TR * a.fbox + 8u * rows);
                 tensor_g2s(buf[cb].sym, &map, (int)b0, f_lo, bar + cb);
                 bulk_g2s(buf[cb].q, a.qpair + b0, 8u * rows, bar + cb);
             }
@@ -126,11 +130,13 @@ __global__ void __launch_bounds__(NW * 32, WIDE ? 1 : 2) hist_ct_root_kernel(con
             mbar_wait(bar + cb, (phbits >> cb) & 1u);
             phbits ^= 1u << cb;
             const CtBuf &st = buf[cb];
+#pragma unroll 1
+            for (int sb = 0; sb < TR; sb += 32)  // 32-row sub-batches of the tile
             if (on) {
-                const uint4 v0 = *reinterpret_cast<const uint4 *>(&st.sym[f][0]);
-                const uint4 v1 = *reinterpret_cast<const uint4 *>(&st.sym[f][16]);
+                const uint4 v0 = *reinterpret_cast<const uint4 *>(&st.sym[f][sb]);
+                const uint4 v1 = *reinterpret_cast<const uint4 *>(&st.sym[f][sb + 16]);
                 const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                const int4 *q2 = reinterpret_cast<const int4 *>(st.q);
+                const int4 *q2 = reinterpret_cast<const int4 *>(st.q + sb);
 #pragma unroll
                 for (int mm = 0; mm < 32 / R; mm += 2) {  // rows R mm + c and R (mm + 1) + c
 #pragma unroll
@@ -144,7 +150,7 @@ __global__ void __launch_bounds__(NW * 32, WIDE ? 1 : 2) hist_ct_root_kernel(con
                             qx = (m2 & 1) ? qq.z : qq.x;
                             qy = (m2 & 1) ? qq.w : qq.y;
                         } else {
-                            const int2 qq = st.q[R * m2 + c];
+                            const int2 qq = st.q[sb + R * m2 + c];
                             qx = qq.x;
                             qy = qq.y;
                         }
@@ -153,9 +159,12 @@ __global__ void __launch_bounds__(NW * 32, WIDE ? 1 : 2) hist_ct_root_kernel(con
                 }
             }
             if (tot) {
-                const int2 qq = st.q[lane];
-                tg += qq.x;
-                th += qq.y;
+#pragma unroll
+                for (int i = lane; i < TR; i += 32) {
+                    const int2 qq = st.q[i];
+                    tg += qq.x;
+                    th += qq.y;
+                }
             }
             __syncwarp();
             ++seq;
@@ -201,10 +210,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <bool W, int R, int NW, int NS>
+template <bool W, int R, int NW, int NS, int TR>
 static int ct_launch_t(gbm_ctx *ctx, const CUtensorMap &map, const CtArgs &a, long long n_items, cudaStream_t s) {
-    const size_t sm = (size_t)(W ? 4 : 2) * COLB_STRIDE * 4 + (size_t)NS * NW * sizeof(CtBuf);
-    auto kern = hist_ct_root_kernel<W, R, NW, NS>;
+    const size_t sm = (size_t)(W ? 4 : 2) * COLB_STRIDE * 4 + (size_t)NS * NW * sizeof(CtBuf<TR>);
+    auto kern = hist_ct_root_kernel<W, R, NW, NS, TR>;
     GBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int occ = 0;
     GBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, sm));
@@ -218,10 +227,13 @@ static int ct_launch_t(gbm_ctx *ctx, const CUtensorMap &map, const CtArgs &a, lo
 template <bool W, int R>
 static int ct_launch_cfg(gbm_ctx *ctx, const CUtensorMap &map, const CtArgs &a, long long n_items, int cfg,
                          cudaStream_t s) {
-    switch (cfg) {  // (warps per block, pipeline depth)
-        case 3: return ct_launch_t<W, R, 12, 3>(ctx, map, a, n_items, s);
-        case 4: return ct_launch_t<W, R, 8, 4>(ctx, map, a, n_items, s);
-        default: return ct_launch_t<W, R, 16, 2>(ctx, map, a, n_items, s);
+    switch (cfg) {  // (warps per block, pipeline depth, rows per tile)
+        case 3: return ct_launch_t<W, R, 12, 3, 32>(ctx, map, a, n_items, s);
+        case 4: return ct_launch_t<W, R, 8, 4, 32>(ctx, map, a, n_items, s);
+        case 5: return ct_launch_t<W, R, 8, 2, 64>(ctx, map, a, n_items, s);
+        case 6: return ct_launch_t<W, R, 16, 2, 64>(ctx, map, a, n_items, s);
+        case 7: return ct_launch_t<W, R, 16, 2, 128>(ctx, map, a, n_items, s);
+        default: return ct_launch_t<W, R, 16, 2, 32>(ctx, map, a, n_items, s);
     }
 }
 
@@ -235,16 +247,25 @@ int root_ct_launch(gbm_ctx *ctx, const RootCtLaunch &L, cudaStream_t s) {
     const int R = 32 / fmax;
     if ((R != 1 && R != 2 && R != 4) || 32 / fmin != R) return 0;  // every group the same copy count
     // measured (profiles/r02/root_tensor_ab.txt): faster with several feature groups (Epsilon root
-    // 0.58 vs 0.76 ms) or several rows per step (Airline, 13 features: 1.29 vs 1.66 ms), slower
-    // for one group of 17..32 features (Higgs: 0.31 vs 0.28 ms: the 28 scattered 32-byte pieces of
-    // each tile arrive too late for a two-deep pipeline -- ncu long-scoreboard 5.6 vs 1.5)
-    if (ctx->root_ct == 0 && ng == 1 && R == 1) return 0;
+    // 0.58 vs 0.76 ms) or several rows per step (Airline, 13 features: 1.29 vs 1.66 ms) at 32-row
+    // tiles; for one group of 17..32 features the 28 scattered 32-byte pieces of a 32-row tile
+    // arrive too late (Higgs: 0.31 vs 0.28 ms staged, ncu long-scoreboard 5.6 vs 1.5), 64-row
+    // tiles with 16 warps x 2 stages (one block per SM) win (0.262 vs 0.285 ms)
+    int cfg = ctx->root_ct;  // 2 (default shape), 3-7: the measured pipeline shapes / tile rows
+    if (cfg == 0) cfg = (ng == 1 && R == 1) ? (L.wide ? 1 : 6) : 2;
+    if (cfg == 1) return 0;
     PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
     if (!enc) return 0;
     CUtensorMap map;
     const cuuint64_t dims[2] = {(cuuint64_t)L.n, (cuuint64_t)L.F};
     const cuuint64_t strides[1] = {(cuuint64_t)L.n};
-    const cuuint32_t box[2] = {32u, (cuuint32_t)fmax};
+    const int TR = cfg == 7 ? 128 : (cfg == 5 || cfg == 6) ? 64 : 32;
+    {  // the shape's shared memory (histogram channels + staging buffers) must fit one block
+        const int NWS[8] = {0, 0, 32, 36, 32, 16, 32, 32};  // warps x stages per shape
+        const size_t sm = (size_t)(L.wide ? 4 : 2) * COLB_STRIDE * 4 + (size_t)NWS[cfg] * (32 * TR + 8 * TR);
+        if (sm + 1024 > ctx->smem_optin) return 0;  // (wide accumulators at 128-row tiles)
+    }
+    const cuuint32_t box[2] = {(cuuint32_t)TR, (cuuint32_t)fmax};
     const cuuint32_t estr[2] = {1u, 1u};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(L.colsym), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -261,13 +282,13 @@ int root_ct_launch(gbm_ctx *ctx, const RootCtLaunch &L, cudaStream_t s) {
     a.totals = L.totals;
     // about two items per resident block (flush amortisation vs balance), whole 32-row batches
     const long long blocks = (long long)(L.wide ? 1 : 2) * ctx->sm_count;
-    a.chunk = std::max<long long>(32 * 16, ((L.n * ng + 2 * blocks - 1) / (2 * blocks) + 31) / 32 * 32);
+    a.chunk = std::max<long long>((long long)TR * 16,
+                                  ((L.n * ng + 2 * blocks - 1) / (2 * blocks) + TR - 1) / TR * TR);
     const long long n_items = (L.n + a.chunk - 1) / a.chunk * ng;
     int slot = -1;
     a.rows_ctr = prof_rows_slot(ctx, &slot);  // algorithmic bytes: n (F b / 8 + 8), SURVEY §8(d)
     ProfScope ps(ctx, PC_HIST_ROOT, s, 0.0, slot, (double)L.F + 8.0);
     int rc;
-    const int cfg = ctx->root_ct;  // 2 (default shape), 3, 4: the measured pipeline shapes
     if (L.wide) rc = R == 1 ? ct_launch_cfg<true, 1>(ctx, map, a, n_items, cfg, s)
                             : R == 2 ? ct_launch_cfg<true, 2>(ctx, map, a, n_items, cfg, s)
                                      : ct_launch_cfg<true, 4>(ctx, map, a, n_items, cfg, s);
