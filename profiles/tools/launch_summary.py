@@ -21,7 +21,7 @@ for r in rows[1:]:
     agg[name][1] += float(r[vi].replace(",", "")) * scale[r[ui]]
 rounds = max(c for k, (c, _) in agg.items() if "init_tree_kernel" in k)
 ONE_TIME = ("keys_kernel", "sort_", "scan_rows", "runs_count", "select", "cutptr", "tag",
-            "write_cuts", "quantise", "pack_kernel", "transpose", "predict", "at::", "init_")
+            "write_cuts", "quantise", "pack_kernel", "pack_byte", "transpose", "predict", "at::", "init_")
 per_round = {k: v for k, v in agg.items() if not any(t in k for t in ONE_TIME) or "init_tree" in k}
 one_time = {k: v for k, v in agg.items() if k not in per_round}
 tot = sum(v[1] for v in per_round.values()) / rounds
@@ -35,7 +35,7 @@ L = [f"# launch list summary (ncu --metrics gpu__time_duration.sum --clock-contr
 for k, (c, us) in sorted(per_round.items(), key=lambda x: -x[1][1]):
     L.append(f"| {k} | {c} | {us / rounds:.1f} | {100 * us / rounds / tot:.1f}% |")
 hist = sum(us for k, (c, us) in per_round.items()
-           if "hist_range" in k or "hist_cs_range" in k or "part_hist" in k) / rounds
+           if "hist_range" in k or "hist_cs_range" in k or "hist_ct_root" in k or "part_hist" in k) / rounds
 L += ["", f"Histogram kernels (root + fused level launches): {100 * hist / tot:.1f}% of the round.", "",
       "One-time kernels (cuts, packing, transpose, predict, torch):", "",
       "| kernel | launches | total us |", "|---|---|---|"]
