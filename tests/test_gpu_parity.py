@@ -440,6 +440,22 @@ def test_run_tiles_option_bounds(ctx, G):
     ctx.set_option(ctx.RUN_TILES, 0)
 
 
+@pytest.mark.parametrize("opt,good,bad,default", [("LEVEL_REPLICAS", (0, 1), (2, -1), 1),
+                                                  ("ROOT_TENSOR", (0, 1, 7), (8, -1), 0),
+                                                  ("LEVEL_HIST", (0, 3), (4,), 0), ("LEVEL_PATH", (0, 2), (3,), 0),
+                                                  ("EVAL_SLICED", (0, 1), (2,), 0), ("CUTS_GATHER", (0, 1), (2,), 0)])
+def test_option_bounds(ctx, G, opt, good, bad, default):
+    """Every tuning option accepts its documented range and rejects values outside it (GBM_E_ARG)."""
+    code = getattr(ctx, opt)
+    for v in bad:
+        with pytest.raises(G.GbmError) as e:
+            ctx.set_option(code, v)
+        assert e.value.code == -1
+    for v in good:
+        ctx.set_option(code, v)
+    ctx.set_option(code, default)
+
+
 @pytest.mark.parametrize("layout", [0, 3])
 @pytest.mark.parametrize("cfg,n,missing,align,P,depth", [
     ("tiny", 2000, 0.05, 32, 15, 5),            # 1 word per row, missing (default directions)
