@@ -3623,9 +3623,11 @@ static EvalArgs eval_args_base(const gbm_ctx *ctx, const gbm_qmatrix *q, const i
 static int launch_eval_tree(gbm_ctx *ctx, const EvalArgs &ea, const TreeDev &t, cudaStream_t s) {
     const long long units = (long long)ea.n_nodes * ea.F;
     // auto: a warp per (node, feature) once there are enough of them to fill the GPU
-    // (throughput: Epsilon 5.13 vs 5.32 ms/round), else a block per (node, feature) (latency:
-    // loss-guided Higgs 6.49 vs 7.29 ms/round)
-    const bool warp = ctx->eval_warp == 1 || (ctx->eval_warp == 0 && units >= 16ll * ctx->sm_count);
+    // (throughput: Epsilon 5.13 vs 5.32 ms/round) or with many features (YearMSD evaluation 0.151
+    // -> 0.143 ms/round, Bosch 0.483 -> 0.455 at >= 64), else a block per (node, feature)
+    // (latency: loss-guided Higgs 6.49 vs 7.29 ms/round)
+    const bool warp = ctx->eval_warp == 1 ||
+                      (ctx->eval_warp == 0 && (units >= 16ll * ctx->sm_count || ea.F >= 64));
     if (warp)
         eval_tree_kernel<<<(int)((units + E_THREADS / 32 - 1) / (E_THREADS / 32)), E_THREADS, 0, s>>>(ea, t);
     else
