@@ -72,6 +72,8 @@ CASES = [  # cfg, rows, missing, grow, p
     ("tiny", 5, 0.0, "depthwise", 8),        # ranks with no rows at all
     ("tiny", 3000, 0.0, "depthwise", 12),    # more ranks than features: ranks owning no feature
     ("epsilon", 3000, 0.0, "depthwise", 3),  # 2000 features in three slices
+    ("higgs", 1_300_000, 0.0, "depthwise", 2),   # > 296 x 2048 rows per rank: multi-tile work items per level
+    ("airline", 1_500_000, 0.01, "depthwise", 2),
 ]
 
 
