@@ -66,12 +66,15 @@ template <bool WIDE>
 __device__ void col_flush(const int *hs, int cstride, const ColGroup &cg, const int32_t *__restrict__ cut_ptr,
                           unsigned long long *dst /* slot base */) {
     const int Fg = cg.f_hi - cg.f_lo, R = 32 / Fg;
+    // a thread's words all sit in one bank column (blockDim is a multiple of 32): its feature and
+    // bin range are fixed, and its bins only grow -- look them up once, stop at the last bin
+    const int col = threadIdx.x & 31;
+    if (col >= R * Fg) return;
+    const int f = cg.f_lo + col % Fg;
+    const int c0 = __ldg(cut_ptr + f), nb = __ldg(cut_ptr + f + 1) - c0;
     for (int w = threadIdx.x; w < cstride; w += blockDim.x) {
-        const int b = w >> 5, col = w & 31;
-        if (col >= R * Fg) continue;
-        const int f = cg.f_lo + col % Fg;
-        const int c0 = __ldg(cut_ptr + f);
-        if (b >= __ldg(cut_ptr + f + 1) - c0) continue;
+        const int b = w >> 5;
+        if (b >= nb) break;
         long long G, H;
         if (WIDE) {
             G = (long long)hs[2 * cstride + w] * 32768 + (long long)(unsigned)hs[w];
