@@ -281,11 +281,17 @@ int root_ct_launch(gbm_ctx *ctx, const RootCtLaunch &L, cudaStream_t s) {
     a.hist = L.hist;
     a.totals = L.totals;
     // items: one per resident block for one feature group (every item zeroes and flushes the whole
-    // bank-column histogram; measured Higgs root 0.262 -> 0.215 ms, Airline round 15.47 -> 14.07),
-    // two per block with several groups (Epsilon root 0.586 vs 0.686 at one: wave quantisation)
+    // bank-column histogram), two per block with several groups (Epsilon root 0.586 vs 0.686 at
+    // one: wave quantisation) -- both capped by the exactness bound below
     const long long blocks = (long long)(L.wide || cfg == 6 || cfg == 7 ? 1 : 2) * ctx->sm_count;
-    const long long per = (ng == 1 ? 1 : 2) * blocks;  // items wanted
-    a.chunk = std::max<long long>((long long)TR * 16, ((L.n * ng + per - 1) / per + TR - 1) / TR * TR);
+    // exactness: a copy's int32 bank column takes at most MAX_CHUNK rows per flush (|q| <= 2^15),
+    // so an item holds at most cap rows; whole waves of items over the resident blocks
+    const long long cap = (long long)MAX_CHUNK * R / TR * TR;
+    long long waves = ng == 1 ? 1 : 2;
+    while ((L.n * ng + waves * blocks - 1) / (waves * blocks) > cap) ++waves;
+    const long long per = waves * blocks;  // items wanted
+    a.chunk = std::min<long long>(cap, std::max<long long>((long long)TR * 16,
+                                                           ((L.n * ng + per - 1) / per + TR - 1) / TR * TR));
     const long long n_items = (L.n + a.chunk - 1) / a.chunk * ng;
     int slot = -1;
     a.rows_ctr = prof_rows_slot(ctx, &slot);  // algorithmic bytes: n (F b / 8 + 8), SURVEY §8(d)

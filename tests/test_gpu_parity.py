@@ -905,6 +905,36 @@ def test_predict_many_trees_parity(ctx, G, cfg, n, rounds, grow, missing):
                                   ob.predict(Xt).view(np.uint64))
 
 
+@pytest.mark.parametrize("F,P", [(20, 15), (13, 15), (20, 30)])
+def test_root_int32_exactness_bound(ctx, G, F, P):
+    """The shared-memory bank columns are int32 and flushed per work item: with every row's pair at
+    the extreme (|q| = 2^P) and one feature constant (every row in one bin), the root histogram
+    over 10.5M rows must still be exact -- the work items (all root kernels, any shape) stay within
+    MAX_CHUNK rows per accumulator copy between flushes.  Closed forms: the constant feature's
+    only bin holds n * q, and every feature's bins sum to n * q."""
+    n = 10_500_000
+    rng = np.random.default_rng(7)
+    X = rng.integers(0, 200, (n, F)).astype(np.float32)  # > 128 bins: 8-bit symbols (every root kernel)
+    X[:, 0] = 3.0
+    Xd = dev(X)
+    qm = ctx.make_qmatrix(Xd, 256, 32)
+    del Xd
+    assert qm.bits == 8
+    qg, qh = (1 << P) - 1, 1 << P
+    q = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+    q[:, 0] = qg
+    q[:, 1] = qh
+    for shape in (0, 1, 2, 6, 7):
+        ctx.set_option(ctx.ROOT_TENSOR, shape)
+        h = ctx.build_histogram(qm, q, P).cpu().numpy()
+        cp = qm.cut_ptr_h
+        assert cp[1] - cp[0] == 1
+        np.testing.assert_array_equal(h[cp[0]], [n * qg, n * qh])
+        for f in range(F):
+            np.testing.assert_array_equal(h[cp[f]:cp[f + 1]].sum(axis=0), [n * qg, n * qh])
+    ctx.set_option(ctx.ROOT_TENSOR, 0)
+
+
 @pytest.mark.parametrize("shape", [2, 5, 7])
 @pytest.mark.parametrize("P", [15, 30])
 @pytest.mark.parametrize("cfg,n,B", [("higgs", 40_016, None), ("airline", 30_000, None), ("yearmsd", 20_000, None),
