@@ -160,7 +160,7 @@ GBM_API int64_t gbm_launch_count(gbm_ctx *ctx);
  *   registers (root_ct.cu); 1 = the staged packed rows; 2-7 = the tensor-fed root with (warps x
  *   stages x TR) 16x2x32, 12x3x32, 8x4x32, 8x2x64, 16x2x64, 16x2x128; 0 (default) = 2 with several
  *   feature groups (> 32 features) or <= 16 features, 6 for one group of 17..32 features
- *   (narrow accumulators), else 1 (measured).  Same histogram.
+ *   (measured).  Same histogram.
  * GBM_OPT_LEVEL_REPLICAS: 1 (default) = the fused level histogram of byte symbols keeps R <= 8
  *   copies of the bins of each feature with few bins (R x bins <= 128), row slot r adding into
  *   copy r mod R, folded before the flush: lanes hitting one bin of a low-cardinality feature no

@@ -252,7 +252,7 @@ int root_ct_launch(gbm_ctx *ctx, const RootCtLaunch &L, cudaStream_t s) {
     // arrive too late (Higgs: 0.31 vs 0.28 ms staged, ncu long-scoreboard 5.6 vs 1.5), 64-row
     // tiles with 16 warps x 2 stages (one block per SM) win (0.262 vs 0.285 ms)
     int cfg = ctx->root_ct;  // 2 (default shape), 3-7: the measured pipeline shapes / tile rows
-    if (cfg == 0) cfg = (ng == 1 && R == 1) ? (L.wide ? 1 : 6) : 2;
+    if (cfg == 0) cfg = (ng == 1 && R == 1) ? 6 : 2;  // (wide accumulators too: Higgs P = 30 root 0.744 -> 0.302 ms)
     if (cfg == 1) return 0;
     PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
     if (!enc) return 0;
