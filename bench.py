@@ -398,6 +398,11 @@ def run_ours(a, world, rank, local):
         cap = 2 * a.leaves - 1 if a.grow_policy == "lossguide" else (1 << (a.depth + 1)) - 1
         host_trees = {nm: torch.empty((a.steps, cap), dtype=dt, pin_memory=True)
                       for nm, dt in G.TREE_FIELDS}
+        # the device copies of X, y reuse cached allocator blocks (a process that has trained
+        # before): a first cudaMalloc of 1+ GB inside the region made the figure vary 4-25 ms/round
+        # from box to box at K = 20
+        warm = (torch.empty(Xh.shape, dtype=Xh.dtype, device=dev), torch.empty(yh.shape, dtype=yh.dtype, device=dev))
+        del warm
         barrier()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
